@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""bench.py -- zone-updates/s of the fused WENO-ADER step on B200 (BASELINE.json metric).
+
+Workload at N=1 (BASELINE.json configs[1], restated as the Euler proxy of SURVEY.md 8(d)):
+C2 = 3D Euler isentropic vortex, 256^3, WENO-ADER + HLL, periodic. The reference has no 4th
+order (geometry.hpp:13-27), so order 3 is the closest it supports. N>1 (torchrun): weak
+scaling, every rank owns a 256^3 z-slab of a 256 x 256 x (256 N) periodic box; z halos go
+over NCCL, dt_next is all-reduced (min).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--fast]
+
+A "step" is one full ADER step (ghost fill + fused kernel + dt hand-off) over the whole
+mesh. value = zones x K / (max over ranks of the CUDA-event time of the K steps). The state
+(2 x 720 MB per GPU) exceeds the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "zone-updates/sec (M/s) per GPU and 8-GPU box, % of HBM/FP64 roofline"
+UNIT = "Mzone-updates/s"
+
+
+def flops_per_zone(n, order, solver):
+    """Algorithmic FP64 flops per active zone-update of the reference as written (add, sub,
+    mul, div, sqrt = 1): F = R(recon+pred) + Phi*face + cross + 70 with
+    R = ((n+2)/n)^3 (ring), Phi = 3(n+1)/n (faces)."""
+    recon, pred = (120.0, 258.0) if order == 2 else (810.0, 543.0)
+    face = {(2, 1): 168.0, (3, 1): 188.0, (2, 0): 154.0, (3, 0): 174.0}[(order, solver)]
+    cross = 0.0 if order == 2 else 60.0
+    R = ((n + 2.0) / n) ** 3
+    phi = 3.0 * (n + 1.0) / n
+    return R * (recon + pred) + phi * face + cross + 70.0
+
+
+BYTES_PER_ZONE = 80.0  # read + write U_skinny (5 doubles), SURVEY.md 8(d)
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h,
+                                                                  self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------ CPU baseline
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_cpu(n, order, steps, threads):
+    """The reference's own harness (hydro::run_benchmark, harness.cpp:222-227) from
+    oracle/_ref (built from /root/reference/proj/src); zones/s as it computes it
+    (harness.cpp:177-180). Falls back to the C restatement (single thread) if absent."""
+    from oracle import pyoracle as po
+    if po.have_reference():
+        ref = po.Reference()
+        zps, _, _, _ = ref.run_benchmark(0, order, 0, 1, n, steps, threads=threads)
+        return zps, "reference", threads
+    orc = po.Oracle()
+    g = po.make_geometry(n, n, n, order)
+    s = orc.init_isentropic_vortex(g, order)
+    cfl = 0.6 if order == 2 else 0.4
+    dt0 = orc.initial_dt(g, s, cfl)
+    t0 = time.perf_counter()
+    orc.run_steps(g, po.make_params(order), po.PERIODIC, cfl, steps, s, dt0)
+    return n ** 3 * steps / (time.perf_counter() - t0), "port", 1
+
+
+def reference_arm(args):
+    """--impl reference: the reference's CPU implementation on the host cores, same metric
+    and config; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    n, order = args.n, args.order
+    # bounded samples: warm-up steps, then K timed steps, each through run_benchmark
+    if args.warmup:
+        run_reference_cpu(n, order, 1, threads)
+    zps, kind, cores = run_reference_cpu(n, order, args.steps, threads)
+    val = zps / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": n ** 3 / zps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (isentropic vortex IC)",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{n}^3 O{order} HLL ADER, {args.steps} steps via "
+                                   "hydro::run_benchmark on the host cores"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {
+        "workload": (f"C2: 3D Euler isentropic vortex {args.n}^3 per GPU, WENO-ADER O{args.order}"
+                     " + HLL, periodic (configs[1]; the reference has no O4, O3 is its closest)"),
+        "n": args.n, "order": args.order, "solver": "hll", "integrator": "ader",
+        "problem": "vortex", "build": "fma" if args.fast else "bit-exact",
+        "l2": "state 2 x {:.0f} MB per GPU > 126 MB L2 (no flush needed)".format(
+            (args.n + 2 * args.order) ** 3 * 40 / 1e6),
+        "parallelism": f"z-slab x{args.gpus}" if args.gpus > 1 else "single GPU",
+    }
+
+
+# ---------------------------------------------------------------------------- our arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--fast", action="store_true", help="FMA-contracted build")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
+
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+
+    from paper_2211_13295_b200 import hydro, slabs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun --nproc-per-node N"
+
+    n, order = args.n, args.order
+    dom = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
+                           exact=not args.fast)
+    s0 = dom.initial_state()
+    cfl = 0.6 if order == 2 else 0.4
+    dt0 = dom.initial_dt(s0, cfl)
+    dom.upload(s0)
+    dom.set_time(0.0, dt0, cfl)
+
+    stream = dom.stream
+    for _ in range(args.warmup):
+        dom.step()
+    torch.cuda.synchronize()
+    dom.barrier()
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    launches0 = dom.launches
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for k in range(args.steps):
+            dom.step(kernel_events=kev[k])
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dom.barrier()
+    ms = ev0.elapsed_time(ev1)
+    kern_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    launches = dom.launches - launches0
+    ms_max = dom.max_over_ranks(ms)
+    t, dt, done = dom.sync()
+
+    zones_local = n ** 3
+    zones_total = zones_local * world
+    value = zones_total * args.steps / (ms_max * 1e-3) / 1e6
+
+    # roofline of the dominant kernel (the fused step), per launch on this rank
+    fpz = flops_per_zone(n, order, 1)
+    peak_fp64 = hydro.fp64_peak(local)
+    achieved = fpz * zones_local / (kern_ms * 1e-3) / 1e12
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_achieved = BYTES_PER_ZONE * zones_local / (kern_ms * 1e-3) / 1e9
+    roofline = {
+        "bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
+        "frac": achieved / peak_fp64,
+        "peak_source": "DFMA throughput measured in this run (hc_fp64_peak); "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "flops_per_zone": fpz, "kernel_ms_per_launch": kern_ms,
+        "traffic": None,
+        "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_achieved / hbm_peak, "bytes_per_zone": BYTES_PER_ZONE,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+    }
+    traffic = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic):
+        with open(traffic) as f:
+            tj = json.load(f).get(f"n{n}_o{order}_{'fma' if args.fast else 'exact'}")
+        if tj:
+            roofline["traffic"] = tj
+
+    # end to end through the public API with HOST buffers: H2D of the step's input from
+    # pinned memory, the step, D2H of the result and of dt_next -- the paper's skinny trick
+    e2e = None
+    if world == 1:
+        host = torch.empty(dom.host_shape(), dtype=torch.float64, pin_memory=True).numpy()
+        host[...] = s0
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            dom.upload(host)
+            dom.step()
+            dom.download(host)
+            dom.sync()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        nbytes = host.nbytes
+        e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 16,
+               "steps": args.e2e_steps, "api": "hc_stepper_upload/step/download/sync"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        c_n = n
+        zps, kind, cores = run_reference_cpu(c_n, order, 2, threads)
+        cpu = {"value": zps / 1e6, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{c_n}^3 O{order} HLL ADER vortex, 2 steps through "
+                         "hydro::run_benchmark (harness wall clock)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (isentropic vortex IC sampled on the host, problems.cpp)",
+            "config": workload_config(args), "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+            "final": {"t": t, "dt_next": dt, "steps_done": done},
+        }
+        print(json.dumps(line), flush=True)
+    dom.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * hydro_cuda.h -- C ABI of libhydro_cuda.so, the B200-native (sm_100a, FP64) space-time
+ * update of arXiv 2211.13295: MC/WENO3 reconstruction -> ADER predictor -> Rusanov/HLL face
+ * fluxes -> flux differencing -> conservative update + global CFL min.
+ *
+ * This is the drop-in boundary. The reference exposes its hot path as free C++ functions in
+ * namespace hydro (proj/include/hydro/*.hpp, statically linked from libhydro.a); a
+ * maintainer swaps proj/src/{fields,boundary,reconstruct,predictor,corrector,stepper}.cpp
+ * for the thin C++ shim in paper_2211_13295_b200/shim/hydro_gpu_shim.cpp, which calls the
+ * entry points below. Signatures carry plain pointers and sizes only.
+ *
+ * Layouts are the reference's host layouts (proj/include/hydro/fields.hpp:15-128):
+ *   skinny [mz][my][mx][5]        ghosts included, mx = nx + 2*ghost
+ *   modal  [mz][my][mx][5][M]     M = 5 (order 2) or 11 (order 3); temporal mode = M-1
+ *   fx [nz][ny][nx+1][5], fy [nz][nx][ny+1][5], fz [ny][nx][nz+1][5]
+ *   rate   [nz][ny][nx][5]
+ *
+ * Error convention: every entry point returns an hc_status. HC_UNPHYSICAL replaces
+ * hydro::unphysical_error (euler.hpp:33-35) and hc_last_error() returns the reference's
+ * message text ("predictor: zone (i,j,k): non-positive density X", corrector.cpp:53-55,
+ * :119-120, predictor.cpp:82-84, stepper.cpp:41-42). HC_INVALID replaces
+ * std::invalid_argument. There is no CPU fallback: without a CUDA device every compute
+ * entry point returns HC_CUDA.
+ */
+#ifndef HYDRO_CUDA_H
+#define HYDRO_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_ABI_VERSION 1
+
+typedef enum { HC_OK = 0, HC_UNPHYSICAL = 1, HC_INVALID = 2, HC_CUDA = 3 } hc_status;
+typedef enum { HC_RUSANOV = 0, HC_HLL = 1 } hc_solver_kind;   /* riemann.hpp:12 SolverChoice */
+typedef enum { HC_PERIODIC = 0, HC_OUTFLOW = 1 } hc_boundary; /* boundary.hpp:7 BoundaryKind */
+
+/* PatchGeometry, geometry.hpp:34-65 */
+typedef struct {
+    int nx, ny, nz, ghost;
+    double dx, dy, dz;
+    double origin[3];
+} hc_geom;
+
+/* LimiterConfig, reconstruct.hpp:11-29 */
+typedef struct {
+    double cfac_rho, cfac_other, weno_eps;
+    double weno_w[3];
+} hc_limiter;
+
+/* StepParams (gas, solver, limiter, order), stepper.hpp:39-45 */
+typedef struct {
+    int order;  /* 2 or 3 */
+    int solver; /* hc_solver_kind */
+    double gamma;
+    hc_limiter lim;
+} hc_params;
+
+/* ------------------------------------------------------------------ library */
+int hc_abi_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int hc_device_count(void);
+/* Measured FP64 (DFMA) throughput of `device` in TFLOP/s (2 flops per DFMA): the FP64
+ * roofline denominator, which MEASURED_PEAKS.json does not carry. */
+int hc_fp64_peak(int device, double* tflops);
+/* Copies the last error message of the calling thread into buf; returns its status. */
+int hc_last_error(char* buf, size_t len);
+
+/* ------------------------------------------------ per-kernel, host buffers
+ * One entry point per reference kernel (the hydro:: function cited beside it). Arguments
+ * are HOST arrays in the reference layouts; each call stages them through the device
+ * (H2D, sm_100a kernel, D2H) and returns the same bits as the reference. */
+/* fields.hpp:139 skinny_to_modal */
+int hc_skinny_to_modal(const hc_geom* g, int modes, const double* skinny, double* modal);
+/* fields.hpp:143 modal_to_skinny */
+int hc_modal_to_skinny(const hc_geom* g, int modes, const double* modal, double* skinny);
+/* boundary.hpp:12 apply_boundary(SkinnyState&, ...) */
+int hc_apply_boundary_skinny(const hc_geom* g, int kind, double* skinny);
+/* boundary.hpp:15 apply_boundary(ModalState&, ...) */
+int hc_apply_boundary_modal(const hc_geom* g, int modes, int kind, double* modal);
+/* reconstruct.hpp:88 limit_patch_o2 */
+int hc_limit_patch_o2(const hc_geom* g, double* modal, const hc_limiter* lim);
+/* reconstruct.hpp:94 reconstruct_patch_o3 */
+int hc_reconstruct_patch_o3(const hc_geom* g, double* modal, const hc_limiter* lim);
+/* predictor.hpp:42 predict_patch */
+int hc_predict_patch(const hc_geom* g, int modes, double* modal, double dt, double gamma);
+/* predictor.hpp:47 zero_temporal_mode */
+int hc_zero_temporal_mode(const hc_geom* g, int modes, double* modal);
+/* corrector.hpp:15 make_flux_axis */
+int hc_make_flux_axis(const hc_geom* g, int modes, const double* modal, int axis, double gamma,
+                      int solver, double* out);
+/* corrector.hpp:21 make_du_dt */
+int hc_make_du_dt(const hc_geom* g, const double* fx, const double* fy, const double* fz,
+                  double dt, double* rate);
+/* corrector.hpp:27 update_u_timestep (dt_next = min CFL estimate, seed 1.0e32) */
+int hc_update_u_timestep(const hc_geom* g, int modes, double* modal, double* skinny,
+                         const double* rate, double cfl, double gamma, double* dt_next);
+/* stepper.hpp:91 compute_dt_next */
+int hc_compute_dt_next(const hc_geom* g, int modes, const double* modal, double gamma,
+                       double cfl, double* dt_next);
+/* stepper.hpp:60 ader_step: the whole pipeline on device, materialising modal, fluxes and
+ * rate exactly as the reference does (all outputs copied back). */
+int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                 double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
+                 double* dt_next);
+/* stepper.hpp:80-85 rk_save_u0 */
+int hc_rk_save_u0(const hc_geom* g, const double* skinny, double* stage_u0);
+/* stepper.hpp:75-78 rk_stage (stage coefficients a, b) */
+int hc_rk_stage(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
+                double dt, double a, double b);
+/* stepper.hpp:87-89 rk_step (nstages 2 = Heun, 3 = SSP-RK3) */
+int hc_rk_step(const hc_geom* g, const hc_params* p, int nstages, double* modal,
+               double* skinny, double* fx, double* fy, double* fz, double* rate,
+               double* stage_u0, int bc, double dt, double cfl, double* dt_next);
+
+/* harness.cpp:92-103 initial_dt: min CFL estimate over the active zones of a HOST skinny */
+int hc_initial_dt(const hc_geom* g, const double* skinny, double gamma, double cfl,
+                  double* dt);
+
+/* ------------------------------------------------ host-side initial conditions
+ * problems.cpp: sampled on the HOST with libm (exp/pow/remainder) so the inputs are
+ * bit-identical to the reference's; not part of the device hot path. */
+int hc_init_vortex(const hc_geom* g, double gamma, int order, double t, double* skinny);
+int hc_init_sod(const hc_geom* g, double gamma, double* skinny);
+int hc_init_constant(const hc_geom* g, double gamma, double* skinny);
+
+/* ------------------------------------------------ per-kernel, device buffers
+ * Same kernels on caller-owned DEVICE arrays (reference layouts) on `stream`
+ * (a cudaStream_t, NULL = default). Calls that can fail synchronise the stream. */
+int hc_dev_skinny_to_modal(const hc_geom* g, int modes, const double* skinny, double* modal,
+                           void* stream);
+int hc_dev_apply_boundary_skinny(const hc_geom* g, int kind, double* skinny, void* stream);
+int hc_dev_reconstruct(const hc_geom* g, int order, double* modal, const hc_limiter* lim,
+                       void* stream);
+int hc_dev_predict_patch(const hc_geom* g, int modes, double* modal, double dt, double gamma,
+                         void* stream);
+int hc_dev_make_flux_axis(const hc_geom* g, int modes, const double* modal, int axis,
+                          double gamma, int solver, double* out, void* stream);
+int hc_dev_make_du_dt(const hc_geom* g, const double* fx, const double* fy, const double* fz,
+                      double dt, double* rate, void* stream);
+int hc_dev_update_u_timestep(const hc_geom* g, int modes, double* modal, double* skinny,
+                             const double* rate, double cfl, double gamma, double* dt_next,
+                             void* stream);
+
+/* ------------------------------------------------ device-resident stepper (throughput path)
+ * One patch (or one z-slab of a decomposed mesh) whose U_skinny stays in HBM across steps
+ * (the paper's skinny trick). A step is ONE fused sm_100a kernel: reconstruction, predictor,
+ * three face sweeps, flux differencing, update and the CFL min-reduction, never writing
+ * modes/fluxes/rate to HBM. dt -> dt_next hand-off and the t_final clip
+ * (harness.cpp:155-170) run on the device, so steps queue without host round trips. */
+typedef struct hc_stepper hc_stepper;
+
+typedef struct {
+    /* ghost fill per axis before every step: HC_PERIODIC / HC_OUTFLOW, or -1 = caller-filled
+     * (the z-slab halo planes of a multi-GPU decomposition). */
+    int bc[3];
+    /* 1: bit-exact build (no FMA contraction, identical to the reference);
+     * 0: FMA-contracted build (<= 1e-13 rel. L1 drift after 200 steps). */
+    int exact;
+    int device;
+} hc_stepper_opts;
+
+int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opts* o,
+                      hc_stepper** out);
+int hc_stepper_destroy(hc_stepper* s);
+/* stream used by every later call (cudaStream_t; NULL = a private stream) */
+int hc_stepper_set_stream(hc_stepper* s, void* stream);
+/* host skinny [mz][my][mx][5] (ghosts included) <-> device state; async on the stream when the
+ * host buffer is pinned */
+int hc_stepper_upload(hc_stepper* s, const double* host_skinny);
+int hc_stepper_download(hc_stepper* s, double* host_skinny);
+/* t, dt of the next step, cfl; t_final <= 0 = fixed step count (no clip) */
+int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t_final);
+/* Enqueue n fused steps (no host sync). */
+int hc_stepper_step(hc_stepper* s, int n);
+/* Synchronise; report t, dt (of the next step), steps done, and device errors. */
+int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done);
+/* Device pointer of the current state buffer and its pitch (doubles per row of mx*5+pad);
+ * used for z-halo exchange by the multi-GPU driver. */
+int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles);
+/* Device pointer of the scalar dt_next of the last step (for an all-reduce(min)) and the
+ * device pointer of the dt the next step will use. */
+int hc_stepper_dt_ptrs(hc_stepper* s, double** dt_next_dev, double** dt_dev);
+/* Multi-GPU step split: (1) fill local x/y ghosts [and z if bc[2] >= 0]; caller then fills z
+ * halos; (2) run the fused kernel; caller then all-reduces dt_next; (3) advance t/dt. */
+int hc_stepper_fill_ghosts(hc_stepper* s);
+int hc_stepper_compute(hc_stepper* s);
+int hc_stepper_advance(hc_stepper* s);
+/* Number of kernels this library launched on the stepper (diagnostic / bench claim). */
+long hc_stepper_launches(hc_stepper* s);
+/* Storage layout of the state buffers: rows per plane, doubles per row, planes. */
+int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,300 @@
+// fused_ader.cuh -- ONE sm_100a kernel per ADER step: reconstruction (MC at O2, WENO3 at
+// O3) -> per-zone ADER predictor -> Rusanov/HLL fluxes on all three face families -> flux
+// differencing -> conservative update -> CFL dt estimate + exact min-reduction.
+//
+// Replaces the reference's pipeline stepper.cpp:49-78 (skinny_to_modal, reconstruct_patch,
+// predict_patch, make_flux_axis x3, make_du_dt, update_u_timestep) without materialising
+// ModalState (40*M B/zone), FluxSet or RateField: the only HBM traffic is U_skinny in
+// (plus halo re-reads that hit L2) and U_skinny out -- 80 B per zone-update.
+//
+// Decomposition (2.5D): a CTA owns a TX x TY column tile and marches a chunk of TZ planes
+// upward. For each plane p it keeps planes p-R..p+R of mode 0 (the zone averages) for the
+// tile plus a halo of G zones in shared memory (a ring buffer of 2R+2 planes refilled with
+// cp.async one plane ahead). One thread owns one "E-column": a tile column or a face-adjacent
+// ring column (the ring zones' slopes and temporal modes are needed for the tile's boundary
+// faces -- the reference computes them on "active + one ring", predictor.cpp:68-70).
+//
+// Per plane:  [sync] predict: recon + predictor for the thread's zone, six face states kept
+//             in registers, +x/+y states published to smem
+//             [sync] flux:    west-x, south-y faces (tile threads; east/north ring threads take
+//             the tile's last x/y face) and the bottom z-face against the +z state this
+//             thread kept from plane p-1
+//             [sync] rate:    east/north fluxes from smem -> partial rate of plane p; plane p-1
+//             is finalised with its top z-flux and updated (U + dt*rate), dt estimate.
+// The rate keeps the reference's association -cx*(E-W) - cy*(N-S) - cz*(T-B)
+// (corrector.cpp:89-90) split as (partial(x,y)) - cz*(z), so the result is bit-identical.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fused_types.cuh"
+
+#ifndef HC_FUSED_NS
+#error "define HC_FUSED_NS (the contraction-policy namespace) before including"
+#endif
+
+namespace hc {
+namespace HC_FUSED_NS {
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+template <bool O3, int TX, int TY>
+struct FusedShape {
+    static constexpr int R = O3 ? 2 : 1;   // reconstruction stencil radius
+    static constexpr int G = R + 1;        // halo: one ring + stencil
+    static constexpr int NB = 2 * R + 2;   // plane ring buffer
+    static constexpr int W = TX + 2 * G;
+    static constexpr int H = TY + 2 * G;
+    static constexpr int PLANE = W * H * NV;  // doubles per smem plane
+    static constexpr int NT = TX * TY + 2 * TX + 2 * TY;
+    static constexpr int XP_N = TY * (TX + 1);  // +x states, columns -1..TX-1
+    static constexpr int YP_N = (TY + 1) * TX;  // +y states, rows -1..TY-1
+    static constexpr int FX_N = TY * (TX + 1);  // x faces 0..TX
+    static constexpr int FY_N = (TY + 1) * TX;  // y faces 0..TY
+    static constexpr size_t SMEM =
+        sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N + FX_N + FY_N) + 32);
+};
+
+template <bool O3, int SOLVER, int TX, int TY, int MINB>
+__global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
+    fused_ader_kernel(const FusedArgs a) {
+    using S = FusedShape<O3, TX, TY>;
+    constexpr int R = S::R, G = S::G, NB = S::NB, W = S::W, H = S::H;
+    if (a.ctl->done) return;
+
+    extern __shared__ double smem[];
+    double* planes = smem;                          // [NB][H][W][5]
+    double* XP = planes + size_t(NB) * S::PLANE;    // [TY][TX+1][5]
+    double* YP = XP + S::XP_N * NV;                 // [TY+1][TX][5]
+    double* FX = YP + S::YP_N * NV;                 // [TY][TX+1][5]
+    double* FY = FX + S::FX_N * NV;                 // [TY+1][TX][5]
+    double* red = FY + S::FY_N * NV;                // [32]
+
+    const int tid = threadIdx.x;
+    // ---- E-column of this thread
+    int ci, cj;
+    bool is_tile;
+    {
+        int t = tid;
+        if (t < TX * TY) {
+            ci = t % TX;
+            cj = t / TX;
+            is_tile = true;
+        } else {
+            is_tile = false;
+            t -= TX * TY;
+            if (t < TX) { ci = t; cj = -1; }
+            else if ((t -= TX) < TX) { ci = t; cj = TY; }
+            else if ((t -= TX) < TY) { ci = -1; cj = t; }
+            else { t -= TY; ci = TX; cj = t; }
+        }
+    }
+    const int tx0 = blockIdx.x * TX, ty0 = blockIdx.y * TY;  // active coords of tile origin
+    const int ia = tx0 + ci, ja = ty0 + cj;                   // active coords of the column
+    // Roles (partial tiles at the domain edge included):
+    //  owned  -- an active zone of this tile: bottom z face, update, dt estimate
+    //  xface  -- computes the x face on its west side (faces 0..nx next to an owned zone)
+    //  yface  -- computes the y face on its south side
+    //  exists -- inside active + one ring in x/y: gets a temporal mode (predictor.cpp:68-70)
+    const bool owned = is_tile && ia < a.nx && ja < a.ny;
+    const bool xface = cj >= 0 && cj < TY && ci >= 0 && ja < a.ny && ia <= a.nx &&
+                       (ci >= 1 || ia < a.nx);
+    const bool yface = ci >= 0 && ci < TX && cj >= 0 && ia < a.nx && ja <= a.ny &&
+                       (cj >= 1 || ja < a.ny);
+    const bool exists = ia >= -1 && ia <= a.nx && ja >= -1 && ja <= a.ny;
+    const int kz0 = blockIdx.z * a.tz;                       // first active plane (active z)
+    const int nzc = min(a.tz, a.nz - kz0);
+    const double dt = a.ctl->dt;
+    const double cx = dt / a.dx, cy = dt / a.dy, cz = dt / a.dz;  // corrector.cpp:75
+
+    // storage pointer of (active plane z, active row ty0 - G, active col tx0 - G)
+    const size_t plane_stride = size_t(a.my_pad) * a.pitch;
+    auto gsrc = [&](int zact) -> const double* {
+        return a.uin + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
+               size_t(tx0 - G + a.gh) * NV;
+    };
+    auto load_plane = [&](int zact) {
+        double* dst = planes + size_t((zact + a.gh) % NB) * S::PLANE;
+        const double* src = gsrc(zact);
+        for (int e = tid; e < S::PLANE; e += S::NT) {
+            int r = e / (W * NV), c = e - r * (W * NV);
+            cp_async8(dst + e, src + size_t(r) * a.pitch + c);
+        }
+        cp_async_commit();
+    };
+    auto P = [&](int zact) -> const double* {
+        return planes + size_t((zact + a.gh) % NB) * S::PLANE;
+    };
+
+    // prologue: planes kz0-1-R .. kz0-1+R
+    for (int z = kz0 - 1 - R; z <= kz0 - 1 + R; ++z) load_plane(z);
+
+    double zp_prev[NV], fz_prev[NV], part[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) zp_prev[q] = fz_prev[q] = part[q] = 0.0;
+    double dt_min = 1.0e32;
+    const int zoff_c = (cj + G) * W + (ci + G);  // zone index of this column in a smem plane
+
+    for (int lp = -1; lp <= nzc; ++lp) {
+        const int p = kz0 + lp;
+        cp_async_wait_all();
+        __syncthreads();
+        if (lp <= nzc - 1) load_plane(p + R + 1);
+
+        const bool zring = (lp == -1 || lp == nzc);
+        const bool do_zone = zring ? owned : exists;
+        // ------------------------------------------------------------- predict
+        double st[6][NV];  // face states incl. 0.5*tau: E, W, N, S, T, B
+        if (do_zone) {
+            const double* pc = P(p) + zoff_c * NV;
+            double face[6][NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double u0 = pc[q];
+                if (!O3) {
+                    // reconstruct.cpp:16-28 (MC limited undivided slopes)
+                    const double cfac = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
+                    const double sx = mc_limiter(pc[NV + q] - u0, u0 - pc[-NV + q], cfac);
+                    const double sy =
+                        mc_limiter(pc[W * NV + q] - u0, u0 - pc[-W * NV + q], cfac);
+                    const double sz = mc_limiter(P(p + 1)[zoff_c * NV + q] - u0,
+                                                 u0 - P(p - 1)[zoff_c * NV + q], cfac);
+                    face[0][q] = extrap<false>(u0, +1.0, sx, 0.0);
+                    face[1][q] = extrap<false>(u0, -1.0, sx, 0.0);
+                    face[2][q] = extrap<false>(u0, +1.0, sy, 0.0);
+                    face[3][q] = extrap<false>(u0, -1.0, sy, 0.0);
+                    face[4][q] = extrap<false>(u0, +1.0, sz, 0.0);
+                    face[5][q] = extrap<false>(u0, -1.0, sz, 0.0);
+                } else {
+                    // reconstruct.cpp:42-61 (dimension-by-dimension WENO3)
+                    double ux, uxx, uy, uyy, uz, uzz;
+                    weno3(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
+                          ux, uxx);
+                    weno3(pc[-2 * W * NV + q], pc[-W * NV + q], u0, pc[W * NV + q],
+                          pc[2 * W * NV + q], a.lim, uy, uyy);
+                    weno3(P(p - 2)[zoff_c * NV + q], P(p - 1)[zoff_c * NV + q], u0,
+                          P(p + 1)[zoff_c * NV + q], P(p + 2)[zoff_c * NV + q], a.lim, uz, uzz);
+                    face[0][q] = extrap<true>(u0, +1.0, ux, uxx);
+                    face[1][q] = extrap<true>(u0, -1.0, ux, uxx);
+                    face[2][q] = extrap<true>(u0, +1.0, uy, uyy);
+                    face[3][q] = extrap<true>(u0, -1.0, uy, uyy);
+                    face[4][q] = extrap<true>(u0, +1.0, uz, uzz);
+                    face[5][q] = extrap<true>(u0, -1.0, uz, uzz);
+                }
+            }
+            Fault f;
+            f.clear();
+            double tau[NV];
+            predictor<O3>(face, dt, a.idx, a.idy, a.idz, a.gamma, tau, f);
+            if (f.code) record_fault(a.eb, ST_PREDICT, f, ia, ja, p, 0);
+            // corrector face states: extrapolate_to_face + 0.5 * tau (corrector.cpp:30-33)
+#pragma unroll
+            for (int s = 0; s < 6; ++s)
+#pragma unroll
+                for (int q = 0; q < NV; ++q) st[s][q] = face[s][q] + 0.5 * tau[q];
+            if (!zring) {
+                if (ci <= TX - 1 && cj >= 0 && cj < TY)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) XP[(cj * (TX + 1) + ci + 1) * NV + q] = st[0][q];
+                if (cj <= TY - 1 && ci >= 0 && ci < TX)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) YP[((cj + 1) * TX + ci) * NV + q] = st[2][q];
+            }
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- flux
+        double fz_cur[NV];
+        if (do_zone) {
+            if (!zring && xface) {  // x face at the west of this column
+                {
+                    double ul[NV], f5[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) ul[q] = XP[(cj * (TX + 1) + ci) * NV + q];
+                    Fault f;
+                    f.clear();
+                    riemann<SOLVER, 0>(ul, st[1], a.gamma, f5, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, ia, ja, p, 0);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) FX[(cj * (TX + 1) + ci) * NV + q] = f5[q];
+                }
+            }
+            if (!zring && yface) {  // y face at the south of this column
+                {
+                    double ul[NV], f5[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) ul[q] = YP[(cj * TX + ci) * NV + q];
+                    Fault f;
+                    f.clear();
+                    riemann<SOLVER, 1>(ul, st[3], a.gamma, f5, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, ja, ia, p, 1);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) FY[(cj * TX + ci) * NV + q] = f5[q];
+                }
+            }
+            if (owned && lp >= 0) {  // z face at the bottom of plane p
+                Fault f;
+                f.clear();
+                riemann<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
+                if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
+            }
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- rate
+        if (owned) {
+            if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
+                const double* u = P(p - 1) + zoff_c * NV;
+                double un[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    double r = part[q] - cz * (fz_cur[q] - fz_prev[q]);
+                    un[q] = u[q] + r;
+                }
+                double* dst = a.uout + size_t(p - 1 + a.gh) * plane_stride +
+                              size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
+#pragma unroll
+                for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                Fault f;
+                f.clear();
+                double d = eval_tstep(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                if (f.code) record_fault(a.eb, ST_UPDATE, f, ia, ja, p - 1, 0);
+                else dt_min = smin(dt_min, d);
+            }
+            if (lp >= 0 && lp < nzc) {
+                const double* fxw = FX + (cj * (TX + 1) + ci) * NV;
+                const double* fys = FY + (cj * TX + ci) * NV;
+#pragma unroll
+                for (int q = 0; q < NV; ++q)
+                    part[q] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
+            }
+            if (lp >= 0) {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) fz_prev[q] = fz_cur[q];
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];
+        }
+    }
+
+    // ---- block min -> one atomic per CTA (exact: min is order independent)
+    dt_min = warp_min(dt_min);
+    if ((tid & 31) == 0) red[tid >> 5] = dt_min;
+    __syncthreads();
+    if (tid < 32) {
+        constexpr int NW = (S::NT + 31) / 32;
+        double v = tid < NW ? red[tid] : 1.0e32;
+        v = warp_min(v);
+        if (tid == 0) atomic_min_pos(&a.ctl->acc, v);
+    }
+}
+
+}  // namespace HC_FUSED_NS
+}  // namespace hc

@@ -1,0 +1,4 @@
+// Bit-exact instantiation of the fused step (compiled with --fmad=false).
+#define HC_FUSED_NS exact
+#define HC_FUSED_LAUNCHER launch_fused_exact
+#include "fused_launch.cuh"

@@ -1,0 +1,365 @@
+// stepper.cu -- the device-resident stepper (include/hydro_cuda.h, hc_stepper_*).
+//
+// U_skinny lives in HBM across steps in two ping-pong buffers laid out like the reference's
+// SkinnyState ([z][y][x][5], fields.hpp:47-67) but with rows padded to the tile grid, so the
+// fused kernel's halo loads never leave the allocation. One step = ghost fill (a gather that
+// reproduces boundary.cpp's x->y->z passes) + the fused kernel + a one-thread "advance" kernel
+// that performs the harness's dt/dt_next hand-off and t_final clip on the device
+// (harness.cpp:155-170), so any number of steps queue on the stream without a host sync.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+
+#include "fused_types.cuh"
+
+namespace hc {
+namespace {
+
+struct SG {  // storage geometry of the stepper
+    int nx, ny, nz, gh, mx, my, mz, my_pad, pitch;
+};
+
+__device__ __forceinline__ int map_index(int a, int n, int kind) {
+    if (kind == 0) return ((a % n) + n) % n;
+    return a < 0 ? 0 : (a >= n ? n - 1 : a);
+}
+
+// Ghost gather (see k_fill_ghosts in patch_kernels.cu for why one gather equals the
+// reference's sequential x, y, z passes). bz < 0: z ghosts belong to the caller (halo
+// exchange of a z-slab decomposition); only ghosts of active planes are filled then, which is
+// exactly the x and y passes of transfer.cpp:94-130.
+__global__ void k_stepper_ghosts(double* u, SG g, int bx, int by, int bz) {
+    size_t id = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    size_t n = size_t(g.mx) * g.my * g.mz;
+    if (id >= n) return;
+    int i = int(id % g.mx), j = int((id / g.mx) % g.my), k = int(id / (size_t(g.mx) * g.my));
+    bool ai = i >= g.gh && i < g.gh + g.nx, aj = j >= g.gh && j < g.gh + g.ny,
+         ak = k >= g.gh && k < g.gh + g.nz;
+    if (ai && aj && ak) return;
+    if (!ak && bz < 0) return;
+    int si = ai ? i : g.gh + map_index(i - g.gh, g.nx, bx);
+    int sj = aj ? j : g.gh + map_index(j - g.gh, g.ny, by);
+    int sk = ak ? k : g.gh + map_index(k - g.gh, g.nz, bz);
+    const double* src = u + (size_t(sk) * g.my_pad + sj) * g.pitch + size_t(si) * NV;
+    double* dst = u + (size_t(k) * g.my_pad + j) * g.pitch + size_t(i) * NV;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) dst[q] = src[q];
+}
+
+__global__ void k_advance(StepCtl* c, const ErrBlock* eb) {
+    if (c->done) return;
+    for (int s = 0; s < ST_COUNT; ++s)
+        if (eb->rec[s].flag) {  // the reference would have thrown out of this step
+            c->done = 2;
+            return;
+        }
+    c->t = c->t + c->dt;  // harness.cpp:167-168
+    c->steps += 1;
+    double dn = c->acc;
+    c->dt_next = dn;
+    c->acc = 1.0e32;
+    if (c->t_final > 0.0) {  // harness.cpp:156-160
+        double rem = c->t_final - c->t;
+        if (rem <= 1e-12 * c->t_final) c->done = 1;
+        else if (dn >= rem) dn = rem;
+    }
+    c->dt = dn;
+}
+
+}  // namespace
+}  // namespace hc
+
+using namespace hc;
+
+struct hc_stepper {
+    hc_geom g;
+    hc_params p;
+    hc_stepper_opts o;
+    SG sg;
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    StepCtl* ctl = nullptr;
+    ErrBlock* eb = nullptr;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    long launches = 0;
+    int tz = 32;
+    size_t bytes = 0;
+    double cfl = 0.6;
+};
+
+namespace {
+
+int set_dev(const hc_stepper* s) {
+    HC_CUDA(cudaSetDevice(s->o.device));
+    return HC_OK;
+}
+
+FusedArgs fused_args(const hc_stepper* s) {
+    FusedArgs a;
+    a.uin = s->buf[s->cur];
+    a.uout = s->buf[1 - s->cur];
+    a.nx = s->g.nx;
+    a.ny = s->g.ny;
+    a.nz = s->g.nz;
+    a.gh = s->g.ghost;
+    a.my_pad = s->sg.my_pad;
+    a.pitch = s->sg.pitch;
+    a.tz = s->tz;
+    a.dx = s->g.dx;
+    a.dy = s->g.dy;
+    a.dz = s->g.dz;
+    a.idx = 1.0 / s->g.dx;  // predictor.cpp:29
+    a.idy = 1.0 / s->g.dy;
+    a.idz = 1.0 / s->g.dz;
+    a.gamma = s->p.gamma;
+    a.cfl = 0.0;  // filled per call from the host copy
+    a.lim = Limiter{s->p.lim.cfac_rho, s->p.lim.cfac_other, s->p.lim.weno_eps,
+                    s->p.lim.weno_w[0], s->p.lim.weno_w[1], s->p.lim.weno_w[2]};
+    a.ctl = s->ctl;
+    a.eb = s->eb;
+    return a;
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opts* o,
+                      hc_stepper** out) {
+    if (!p || !o || !out) {
+        set_error(HC_INVALID, "null argument");
+        return HC_INVALID;
+    }
+    int rc = validate_geom(g, p->order);
+    if (rc) return rc;
+    if (p->solver != HC_RUSANOV && p->solver != HC_HLL) {
+        set_error(HC_INVALID, "unknown riemann solver");
+        return HC_INVALID;
+    }
+    for (int a = 0; a < 3; ++a)
+        if (o->bc[a] < -1 || o->bc[a] > 1 || (a < 2 && o->bc[a] < 0)) {
+            set_error(HC_INVALID, "bad boundary kind (x/y must be periodic or outflow)");
+            return HC_INVALID;
+        }
+    int ndev = hc_device_count();
+    if (ndev == 0 || o->device < 0 || o->device >= ndev) {
+        set_error(HC_CUDA, "no CUDA device available for the stepper (there is no CPU path)");
+        return HC_CUDA;
+    }
+    hc_stepper* s = new (std::nothrow) hc_stepper();
+    if (!s) {
+        set_error(HC_INVALID, "out of host memory");
+        return HC_INVALID;
+    }
+    s->g = *g;
+    s->p = *p;
+    s->o = *o;
+    const bool o3 = p->order == 3;
+    const int TX = o3 ? FusedTile<true>::TX : FusedTile<false>::TX;
+    const int TY = o3 ? FusedTile<true>::TY : FusedTile<false>::TY;
+    const int G = o3 ? 3 : 2;
+    SG& sg = s->sg;
+    sg.nx = g->nx;
+    sg.ny = g->ny;
+    sg.nz = g->nz;
+    sg.gh = g->ghost;
+    sg.mx = mx_of(*g);
+    sg.my = my_of(*g);
+    sg.mz = mz_of(*g);
+    int ntx = (g->nx + TX - 1) / TX, nty = (g->ny + TY - 1) / TY;
+    int cols = std::max(sg.mx, ntx * TX + g->ghost + G);
+    sg.my_pad = std::max(sg.my, nty * TY + g->ghost + G);
+    sg.pitch = (cols * NV + 15) / 16 * 16;  // 128-byte rows
+    s->tz = std::max(4, std::min(32, g->nz));
+    if ((rc = set_dev(s))) {
+        delete s;
+        return rc;
+    }
+    s->bytes = size_t(sg.mz) * sg.my_pad * sg.pitch * sizeof(double);
+    cudaError_t e = cudaMalloc(&s->buf[0], s->bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&s->buf[1], s->bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(StepCtl));
+    if (e == cudaSuccess) e = cudaMalloc(&s->eb, sizeof(ErrBlock));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        s->own_stream = true;
+        e = cudaMemsetAsync(s->buf[0], 0, s->bytes, s->st);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->buf[1], 0, s->bytes, s->st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->eb, 0, sizeof(ErrBlock), s->st);
+    if (e == cudaSuccess) {
+        StepCtl c{};
+        c.acc = 1.0e32;
+        c.dt_next = 1.0e32;
+        e = cudaMemcpyAsync(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->st);
+    if (e != cudaSuccess) {
+        rc = cuda_fail(e, "hc_stepper_create");
+        hc_stepper_destroy(s);
+        return rc;
+    }
+    *out = s;
+    return HC_OK;
+}
+
+int hc_stepper_destroy(hc_stepper* s) {
+    if (!s) return HC_OK;
+    cudaSetDevice(s->o.device);
+    if (s->st) cudaStreamSynchronize(s->st);
+    cudaFree(s->buf[0]);
+    cudaFree(s->buf[1]);
+    cudaFree(s->ctl);
+    cudaFree(s->eb);
+    if (s->own_stream && s->st) cudaStreamDestroy(s->st);
+    delete s;
+    return HC_OK;
+}
+
+int hc_stepper_set_stream(hc_stepper* s, void* stream) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    HC_CUDA(cudaStreamSynchronize(s->st));
+    if (stream) {
+        if (s->own_stream) cudaStreamDestroy(s->st);
+        s->st = static_cast<cudaStream_t>(stream);
+        s->own_stream = false;
+    }
+    return HC_OK;
+}
+
+static cudaMemcpy3DParms copy_parms(hc_stepper* s, double* host, bool up) {
+    cudaMemcpy3DParms m;
+    std::memset(&m, 0, sizeof m);
+    const size_t row = size_t(s->sg.mx) * NV * sizeof(double);
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, row, row, s->sg.my);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(s->buf[s->cur], size_t(s->sg.pitch) * sizeof(double),
+                                            row, s->sg.my_pad);
+    m.srcPtr = up ? hp : dp;
+    m.dstPtr = up ? dp : hp;
+    m.extent = make_cudaExtent(row, s->sg.my, s->sg.mz);
+    m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    return m;
+}
+
+int hc_stepper_upload(hc_stepper* s, const double* host_skinny) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    cudaMemcpy3DParms m = copy_parms(s, const_cast<double*>(host_skinny), true);
+    HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
+    return HC_OK;
+}
+
+int hc_stepper_download(hc_stepper* s, double* host_skinny) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    cudaMemcpy3DParms m = copy_parms(s, host_skinny, false);
+    HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
+    HC_CUDA(cudaStreamSynchronize(s->st));
+    return HC_OK;
+}
+
+int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t_final) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    StepCtl c{};
+    c.t = t;
+    c.dt = dt;
+    c.t_final = t_final;
+    c.acc = 1.0e32;
+    c.dt_next = 1.0e32;
+    if (t_final > 0.0) {  // harness.cpp:156-160, applied before the first step too
+        double rem = t_final - t;
+        if (rem <= 1e-12 * t_final) c.done = 1;
+        else if (c.dt >= rem) c.dt = rem;
+    }
+    s->cfl = cfl;  // TimeState::cfl, a constant of the run
+    HC_CUDA(cudaMemcpyAsync(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->st));
+    HC_CUDA(cudaMemsetAsync(s->eb, 0, sizeof(ErrBlock), s->st));
+    HC_CUDA(cudaStreamSynchronize(s->st));
+    return HC_OK;
+}
+
+int hc_stepper_fill_ghosts(hc_stepper* s) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    size_t n = size_t(s->sg.mx) * s->sg.my * s->sg.mz;
+    k_stepper_ghosts<<<unsigned((n + 255) / 256), 256, 0, s->st>>>(
+        s->buf[s->cur], s->sg, s->o.bc[0], s->o.bc[1], s->o.bc[2]);
+    s->launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_stepper_ghosts");
+}
+
+int hc_stepper_compute(hc_stepper* s) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    FusedArgs a = fused_args(s);
+    a.cfl = s->cfl;
+    rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, s->st)
+                    : launch_fused_fast(a, s->p.order, s->p.solver, s->st);
+    if (rc) return rc;
+    s->launches++;
+    s->cur = 1 - s->cur;
+    return HC_OK;
+}
+
+int hc_stepper_advance(hc_stepper* s) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    k_advance<<<1, 1, 0, s->st>>>(s->ctl, s->eb);
+    s->launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_advance");
+}
+
+int hc_stepper_step(hc_stepper* s, int n) {
+    for (int i = 0; i < n; ++i) {
+        int rc = hc_stepper_fill_ghosts(s);
+        if (!rc) rc = hc_stepper_compute(s);
+        if (!rc) rc = hc_stepper_advance(s);
+        if (rc) return rc;
+    }
+    return HC_OK;
+}
+
+int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done) {
+    int rc = set_dev(s);
+    if (rc) return rc;
+    StepCtl c;
+    ErrBlock eb;
+    HC_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost, s->st));
+    HC_CUDA(cudaMemcpyAsync(&eb, s->eb, sizeof eb, cudaMemcpyDeviceToHost, s->st));
+    HC_CUDA(cudaStreamSynchronize(s->st));
+    if (t) *t = c.t;
+    if (dt) *dt = c.dt;
+    if (steps_done) *steps_done = long(c.steps);
+    return report_device_errors(eb);
+}
+
+int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {
+    if (dptr) *dptr = s->buf[s->cur];
+    if (row_pitch_doubles) *row_pitch_doubles = size_t(s->sg.pitch);
+    return HC_OK;
+}
+
+int hc_stepper_dt_ptrs(hc_stepper* s, double** dt_next_dev, double** dt_dev) {
+    if (dt_next_dev) *dt_next_dev = &s->ctl->acc;
+    if (dt_dev) *dt_dev = &s->ctl->dt;
+    return HC_OK;
+}
+
+long hc_stepper_launches(hc_stepper* s) { return s ? s->launches : 0; }
+
+int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz) {
+    if (my_pad) *my_pad = s->sg.my_pad;
+    if (pitch) *pitch = s->sg.pitch;
+    if (mz) *mz = s->sg.mz;
+    return HC_OK;
+}
+
+}  // extern "C"

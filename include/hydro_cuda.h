@@ -106,12 +106,25 @@ int hc_compute_dt_next(const hc_geom* g, int modes, const double* modal, double 
 int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
                  double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
                  double* dt_next);
+/* ader_step plus per-stage device times in StageProfile order (stepper.hpp:15-37):
+ * [reconstruct, predict, flux, rate, update, transfer] seconds; stage_seconds may be NULL. */
+int hc_ader_step_timed(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                       double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
+                       double* dt_next, double* stage_seconds);
+/* predictor.hpp:36-37 predictor_ptwise on one zone's [5][M] modes (temporal mode written) */
+int hc_predictor_ptwise(double* zone_v, int modes, double dt, double dx, double dy, double dz,
+                        double gamma);
 /* stepper.hpp:80-85 rk_save_u0 */
 int hc_rk_save_u0(const hc_geom* g, const double* skinny, double* stage_u0);
 /* stepper.hpp:75-78 rk_stage (stage coefficients a, b) */
 int hc_rk_stage(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
                 double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
                 double dt, double a, double b);
+/* rk_stage plus per-stage device times (as hc_ader_step_timed; zero_temporal_mode counts as
+ * "predict", stepper.cpp:110-113) */
+int hc_rk_stage_timed(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                      double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
+                      double dt, double a, double b, double* stage_seconds);
 /* stepper.hpp:87-89 rk_step (nstages 2 = Heun, 3 = SSP-RK3) */
 int hc_rk_step(const hc_geom* g, const hc_params* p, int nstages, double* modal,
                double* skinny, double* fx, double* fy, double* fz, double* rate,

@@ -55,7 +55,8 @@ struct FusedShape {
     static constexpr int W = TX + 2 * G;
     static constexpr int H = TY + 2 * G;
     static constexpr int PLANE = W * H * NV;  // doubles per smem plane
-    static constexpr int NT = TX * TY + 2 * TX + 2 * TY;
+    static constexpr int NE = TX * TY + 2 * TX + 2 * TY;  // E-columns (tile + face rings)
+    static constexpr int NT = (NE + 31) / 32 * 32;        // whole warps (shuffles need them)
     static constexpr int XP_N = TY * (TX + 1);  // +x states, columns -1..TX-1
     static constexpr int YP_N = (TY + 1) * TX;  // +y states, rows -1..TY-1
     static constexpr int FX_N = TY * (TX + 1);  // x faces 0..TX
@@ -85,7 +86,10 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     bool is_tile;
     {
         int t = tid;
-        if (t < TX * TY) {
+        if (t >= S::NE) {  // padding lanes: no column
+            ci = cj = -(1 << 20);
+            is_tile = false;
+        } else if (t < TX * TY) {
             ci = t % TX;
             cj = t / TX;
             is_tile = true;

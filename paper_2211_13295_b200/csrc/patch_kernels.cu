@@ -442,7 +442,7 @@ int d_predict(const hc_geom& g, int modes, double* m, double dt, double gamma, E
 template <int A, int S, bool O3>
 void launch_flux(const hc_geom& g, const double* m, double gamma, double* out, ErrBlock* eb,
                  cudaStream_t st) {
-    k_flux<A, S, O3><<<blocks_for(face_count(g, A)), 128, 0, st>>>(m, make_g(g), gamma, out, eb);
+    k_flux<A, S, O3><<<blocks_for(face_count(g, A)), TPB, 0, st>>>(m, make_g(g), gamma, out, eb);
 }
 
 int d_flux(const hc_geom& g, int modes, const double* m, int axis, double gamma, int solver,
@@ -757,9 +757,30 @@ int hc_compute_dt_next(const hc_geom* g, int modes, const double* modal, double 
 }
 
 // stepper.cpp:49-78, every intermediate materialised as in the reference
-int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
-                 double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
-                 double* dt_next) {
+// CUDA events bracketing the stages of one host-buffer pipeline call, reported in the
+// order of StageProfile (stepper.hpp:15-37): reconstruct, predict, flux, rate, update,
+// transfer (host<->device staging and skinny_to_modal).
+struct StageEvents {
+    cudaEvent_t e[8];
+    bool ok = false;
+    StageEvents() {
+        ok = true;
+        for (auto& x : e) ok = ok && cudaEventCreate(&x) == cudaSuccess;
+    }
+    ~StageEvents() {
+        for (auto& x : e) cudaEventDestroy(x);
+    }
+    void mark(int i, cudaStream_t st) { cudaEventRecord(e[i], st); }
+    float ms(int a, int b) {
+        float v = 0.f;
+        cudaEventElapsedTime(&v, e[a], e[b]);
+        return v;
+    }
+};
+
+int hc_ader_step_timed(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                       double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
+                       double* dt_next, double* stage_seconds) {
     GEOM_OR_FAIL(g, p->order);
     int modes = p->order == 2 ? 5 : 11;
     int rc = HC_OK;
@@ -767,26 +788,37 @@ int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* sk
     TRY(rc);
     PatchBufs b;
     TRY(patch_bufs(*g, modes, b));
+    StageEvents ev;
     size_t nm = total_zones(*g) * NV * modes, ns = total_zones(*g) * NV;
+    ev.mark(0, st);
     TRY(h2d(b.modal, modal, nm * 8, st));
     TRY(h2d(b.skinny, skinny, ns * 8, st));
-    ErrScope es(st);
-    TRY(es.rc);
-    TRY(d_skinny_to_modal(*g, modes, b.skinny, b.modal, st));
-    TRY(d_reconstruct(*g, p->order, b.modal, to_lim(&p->lim), st));
-    TRY(d_predict(*g, modes, b.modal, dt, p->gamma, es.d, st));
-    // the reference throws out of predict_patch before touching the fluxes
-    TRY(d2h(modal, b.modal, nm * 8, st));
-    rc = es.finish();
-    if (rc) return rc;
     TRY(h2d(b.fx, fx, face_count(*g, 0) * NV * 8, st));
     TRY(h2d(b.fy, fy, face_count(*g, 1) * NV * 8, st));
     TRY(h2d(b.fz, fz, face_count(*g, 2) * NV * 8, st));
+    ErrScope es(st);
+    TRY(es.rc);
+    TRY(d_skinny_to_modal(*g, modes, b.skinny, b.modal, st));
+    ev.mark(1, st);
+    TRY(d_reconstruct(*g, p->order, b.modal, to_lim(&p->lim), st));
+    ev.mark(2, st);
+    TRY(d_predict(*g, modes, b.modal, dt, p->gamma, es.d, st));
+    ev.mark(3, st);
+    // the reference throws out of predict_patch before touching the fluxes
+    rc = es.finish();
+    if (rc) {
+        d2h(modal, b.modal, nm * 8, st);
+        sync(st);
+        return rc;
+    }
     TRY(d_flux(*g, modes, b.modal, 0, p->gamma, p->solver, b.fx, es.d, st));
     TRY(d_flux(*g, modes, b.modal, 1, p->gamma, p->solver, b.fy, es.d, st));
     TRY(d_flux(*g, modes, b.modal, 2, p->gamma, p->solver, b.fz, es.d, st));
+    ev.mark(4, st);
     TRY(d_du_dt(*g, b.fx, b.fy, b.fz, dt, b.rate, st));
+    ev.mark(5, st);
     TRY(d_update(*g, modes, b.modal, b.skinny, b.rate, cfl, p->gamma, b.dtn, es.d, st));
+    ev.mark(6, st);
     TRY(d2h(modal, b.modal, nm * 8, st));
     TRY(d2h(skinny, b.skinny, ns * 8, st));
     TRY(d2h(fx, b.fx, face_count(*g, 0) * NV * 8, st));
@@ -794,7 +826,59 @@ int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* sk
     TRY(d2h(fz, b.fz, face_count(*g, 2) * NV * 8, st));
     TRY(d2h(rate, b.rate, active_zones(*g) * NV * 8, st));
     TRY(d2h(dt_next, b.dtn, 8, st));
-    return es.finish();
+    ev.mark(7, st);
+    rc = es.finish();
+    if (stage_seconds && ev.ok) {
+        stage_seconds[0] = ev.ms(1, 2) * 1e-3;
+        stage_seconds[1] = ev.ms(2, 3) * 1e-3;
+        stage_seconds[2] = ev.ms(3, 4) * 1e-3;
+        stage_seconds[3] = ev.ms(4, 5) * 1e-3;
+        stage_seconds[4] = ev.ms(5, 6) * 1e-3;
+        stage_seconds[5] = (ev.ms(0, 1) + ev.ms(6, 7)) * 1e-3;
+    }
+    return rc;
+}
+
+int hc_ader_step(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                 double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
+                 double* dt_next) {
+    return hc_ader_step_timed(g, p, modal, skinny, fx, fy, fz, rate, dt, cfl, dt_next,
+                              nullptr);
+}
+
+// predictor.cpp:26-60 on one zone (the reference tests call predictor_ptwise directly)
+int hc_predictor_ptwise(double* zone_v, int modes, double dt, double dx, double dy, double dz,
+                        double gamma) {
+    TRY(modes_ok(modes));
+    int rc = HC_OK;
+    cudaStream_t st = host_stream(&rc);
+    TRY(rc);
+    double* d = ws().get<double>("zone", NV * 11, &rc);
+    TRY(rc);
+    ErrScope es(st);
+    TRY(es.rc);
+    TRY(h2d(d, zone_v, NV * modes * 8, st));
+    // a 1x1x1 "patch" whose single ring zone is the zone itself
+    hc_geom one{};
+    one.nx = one.ny = one.nz = -1;  // ring box (n+2)^3 = 1 zone at storage (0,0,0)
+    one.ghost = 1;
+    G gg{-1, -1, -1, 1, 1, 1, 1};
+    double idx = 1.0 / dx, idy = 1.0 / dy, idz = 1.0 / dz;
+    if (modes == 5)
+        k_predict<false><<<1, 32, 0, st>>>(d, gg, dt, idx, idy, idz, gamma, es.d);
+    else
+        k_predict<true><<<1, 32, 0, st>>>(d, gg, dt, idx, idy, idz, gamma, es.d);
+    TRY(check_launch("k_predict(zone)"));
+    TRY(d2h(zone_v, d, NV * modes * 8, st));
+    (void)one;
+    rc = es.finish();
+    if (rc == HC_UNPHYSICAL) {  // predictor_ptwise throws without zone context
+        char buf[512];
+        hc_last_error(buf, sizeof buf);
+        const char* m = strstr(buf, "): ");
+        set_error(rc, m ? m + 3 : buf);
+    }
+    return rc;
 }
 
 int hc_rk_save_u0(const hc_geom* g, const double* skinny, double* stage_u0) {
@@ -815,18 +899,24 @@ int hc_rk_save_u0(const hc_geom* g, const double* skinny, double* stage_u0) {
 
 // stepper.cpp:100-143 on device buffers already uploaded
 static int d_rk_stage(const hc_geom& g, const hc_params& p, PatchBufs& b, double dt, double a,
-                      double bb, ErrBlock* eb, cudaStream_t st) {
+                      double bb, ErrBlock* eb, cudaStream_t st, StageEvents* ev = nullptr) {
     int modes = p.order == 2 ? 5 : 11;
     TRY(d_skinny_to_modal(g, modes, b.skinny, b.modal, st));
+    if (ev) ev->mark(1, st);
     TRY(d_reconstruct(g, p.order, b.modal, to_lim(&p.lim), st));
+    if (ev) ev->mark(2, st);
     k_zero_tm<<<blocks_for(total_zones(g) * NV), TPB, 0, st>>>(b.modal, total_zones(g), modes);
     TRY(check_launch("k_zero_tm"));
+    if (ev) ev->mark(3, st);
     TRY(d_flux(g, modes, b.modal, 0, p.gamma, p.solver, b.fx, eb, st));
     TRY(d_flux(g, modes, b.modal, 1, p.gamma, p.solver, b.fy, eb, st));
     TRY(d_flux(g, modes, b.modal, 2, p.gamma, p.solver, b.fz, eb, st));
+    if (ev) ev->mark(4, st);
     TRY(d_du_dt(g, b.fx, b.fy, b.fz, dt, b.rate, st));
+    if (ev) ev->mark(5, st);
     k_rk_combine<<<blocks_for(active_zones(g)), TPB, 0, st>>>(b.modal, b.skinny, b.u0, b.rate,
                                                             make_g(g), modes, a, bb);
+    if (ev) ev->mark(6, st);
     return check_launch("k_rk_combine");
 }
 
@@ -855,9 +945,9 @@ static int download_all(const hc_geom& g, int modes, PatchBufs& b, double* modal
     return HC_OK;
 }
 
-int hc_rk_stage(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
-                double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
-                double dt, double a, double b_) {
+int hc_rk_stage_timed(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                      double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
+                      double dt, double a, double b_, double* stage_seconds) {
     GEOM_OR_FAIL(g, p->order);
     int modes = p->order == 2 ? 5 : 11;
     int rc = HC_OK;
@@ -865,12 +955,31 @@ int hc_rk_stage(const hc_geom* g, const hc_params* p, double* modal, double* ski
     TRY(rc);
     PatchBufs b;
     TRY(patch_bufs(*g, modes, b));
+    StageEvents ev;
+    ev.mark(0, st);
     TRY(upload_all(*g, modes, b, modal, skinny, fx, fy, fz, rate, stage_u0, st));
     ErrScope es(st);
     TRY(es.rc);
-    TRY(d_rk_stage(*g, *p, b, dt, a, b_, es.d, st));
+    TRY(d_rk_stage(*g, *p, b, dt, a, b_, es.d, st, &ev));
     TRY(download_all(*g, modes, b, modal, skinny, fx, fy, fz, rate, nullptr, st));
-    return es.finish();
+    ev.mark(7, st);
+    rc = es.finish();
+    if (stage_seconds && ev.ok) {  // rk_stage's StageTimer slots, stepper.cpp:100-143
+        stage_seconds[0] = ev.ms(1, 2) * 1e-3;
+        stage_seconds[1] = ev.ms(2, 3) * 1e-3;
+        stage_seconds[2] = ev.ms(3, 4) * 1e-3;
+        stage_seconds[3] = ev.ms(4, 5) * 1e-3;
+        stage_seconds[4] = ev.ms(5, 6) * 1e-3;
+        stage_seconds[5] = (ev.ms(0, 1) + ev.ms(6, 7)) * 1e-3;
+    }
+    return rc;
+}
+
+int hc_rk_stage(const hc_geom* g, const hc_params* p, double* modal, double* skinny,
+                double* fx, double* fy, double* fz, double* rate, const double* stage_u0,
+                double dt, double a, double b_) {
+    return hc_rk_stage_timed(g, p, modal, skinny, fx, fy, fz, rate, stage_u0, dt, a, b_,
+                             nullptr);
 }
 
 int hc_rk_step(const hc_geom* g, const hc_params* p, int nstages, double* modal,

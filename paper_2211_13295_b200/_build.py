@@ -88,9 +88,41 @@ def build(verbose=True) -> str:
     return LIB
 
 
+REF = "/root/reference/proj"
+REF_FLAGS = ["-std=c++20", "-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fopenmp",
+             "-include", "algorithm"]
+
+
 def build_shim(verbose=True):
-    """Placeholder until the drop-in C++ shim lands."""
-    return None
+    """Links the reference's own unit tests and acceptance suite against the drop-in shim
+    (shim/hydro_gpu_shim.cpp -> libhydro_cuda.so) in place of proj/src/{fields,boundary,
+    reconstruct,predictor,corrector,stepper}.cpp. Needs /root/reference (build container
+    only); the binaries land in oracle/_ref/ (git-ignored, shipped to the GPU box)."""
+    if not os.path.isdir(REF):
+        return None
+    out_dir = os.path.join(ROOT, "oracle", "_ref")
+    os.makedirs(out_dir, exist_ok=True)
+    kept = [os.path.join(REF, "src", f) for f in
+            ("harness.cpp", "problems.cpp", "transfer.cpp", "serial_ref.cpp")]
+    shim = os.path.join(PKG, "shim", "hydro_gpu_shim.cpp")
+    tests = sorted(os.path.join(REF, "tests", f) for f in os.listdir(os.path.join(REF, "tests"))
+                   if f.endswith(".cpp") and f != "acceptance_main.cpp")
+    inc = ["-I" + os.path.join(REF, "include"), "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(ROOT, "oracle", "doctest_shim"), "-I" + os.path.join(REF, "tests")]
+    link = ["-L" + PKG, "-l:libhydro_cuda.so", "-Wl,-rpath,$ORIGIN/../../paper_2211_13295_b200"]
+    targets = {
+        "unit_tests_gpu": tests + kept + [shim],
+        "acceptance_gpu": [os.path.join(REF, "tests", "acceptance_main.cpp")] + kept + [shim],
+    }
+    deps = [shim, LIB]
+    for name, srcs in targets.items():
+        exe = os.path.join(out_dir, name)
+        if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(d) for d in deps):
+            continue
+        subprocess.run([CXX] + REF_FLAGS + inc + ["-o", exe] + srcs + link, check=True)
+        if verbose:
+            print(f"[build] {exe}")
+    return out_dir
 
 
 if __name__ == "__main__":

@@ -71,6 +71,9 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     using S = FusedShape<O3, TX, TY>;
     constexpr int R = S::R, G = S::G, NB = S::NB, W = S::W, H = S::H;
     if (a.ctl->done) return;
+    const int cur = a.ctl->cur;
+    const double* __restrict__ uin = a.buf[cur];
+    double* __restrict__ uout = a.buf[cur ^ 1];
 
     extern __shared__ double smem[];
     double* planes = smem;                          // [NB][H][W][5]
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     // storage pointer of (active plane z, active row ty0 - G, active col tx0 - G)
     const size_t plane_stride = size_t(a.my_pad) * a.pitch;
     auto gsrc = [&](int zact) -> const double* {
-        return a.uin + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
+        return uin + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
                size_t(tx0 - G + a.gh) * NV;
     };
     auto load_plane = [&](int zact) {
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                     double r = part[q] - cz * (fz_cur[q] - fz_prev[q]);
                     un[q] = u[q] + r;
                 }
-                double* dst = a.uout + size_t(p - 1 + a.gh) * plane_stride +
+                double* dst = uout + size_t(p - 1 + a.gh) * plane_stride +
                               size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
 #pragma unroll
                 for (int q = 0; q < NV; ++q) dst[q] = un[q];

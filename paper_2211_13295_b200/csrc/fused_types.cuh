@@ -14,13 +14,12 @@ struct StepCtl {
     double acc;      // min-reduction accumulator of this step's dt_next (seed 1.0e32)
     double dt_next;  // last completed step's dt_next (after any all-reduce)
     long long steps;
-    int done;
-    int pad;
+    int done;  // 1: t_final reached, 2: a step failed (unphysical); later steps are no-ops
+    int cur;   // which of the two state buffers holds the current state
 };
 
 struct FusedArgs {
-    const double* __restrict__ uin;
-    double* __restrict__ uout;
+    double* buf[2];  // ping-pong state buffers; ctl->cur selects the input
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width
     int my_pad;      // rows per plane in storage

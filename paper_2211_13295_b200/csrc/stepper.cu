@@ -30,7 +30,10 @@ __device__ __forceinline__ int map_index(int a, int n, int kind) {
 // reference's sequential x, y, z passes). bz < 0: z ghosts belong to the caller (halo
 // exchange of a z-slab decomposition); only ghosts of active planes are filled then, which is
 // exactly the x and y passes of transfer.cpp:94-130.
-__global__ void k_stepper_ghosts(double* u, SG g, int bx, int by, int bz) {
+__global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g, int bx, int by,
+                                 int bz) {
+    if (c->done) return;
+    double* u = c->cur ? b1 : b0;
     size_t id = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     size_t n = size_t(g.mx) * g.my * g.mz;
     if (id >= n) return;
@@ -66,6 +69,7 @@ __global__ void k_advance(StepCtl* c, const ErrBlock* eb) {
         else if (dn >= rem) dn = rem;
     }
     c->dt = dn;
+    c->cur ^= 1;  // the fused kernel wrote the other buffer
 }
 
 }  // namespace
@@ -99,8 +103,8 @@ int set_dev(const hc_stepper* s) {
 
 FusedArgs fused_args(const hc_stepper* s) {
     FusedArgs a;
-    a.uin = s->buf[s->cur];
-    a.uout = s->buf[1 - s->cur];
+    a.buf[0] = s->buf[0];
+    a.buf[1] = s->buf[1];
     a.nx = s->g.nx;
     a.ny = s->g.ny;
     a.nz = s->g.nz;
@@ -125,6 +129,16 @@ FusedArgs fused_args(const hc_stepper* s) {
 
 
 }  // namespace
+
+// Reads which buffer is current from the device (steps after t_final or after a failure
+// are no-ops, so the host's per-launch guess can be off).
+static int refresh_cur(hc_stepper* s) {
+    int cur = 0;
+    HC_CUDA(cudaMemcpyAsync(&cur, &s->ctl->cur, sizeof cur, cudaMemcpyDeviceToHost, s->st));
+    HC_CUDA(cudaStreamSynchronize(s->st));
+    s->cur = cur;
+    return HC_OK;
+}
 
 extern "C" {
 
@@ -248,6 +262,7 @@ static cudaMemcpy3DParms copy_parms(hc_stepper* s, double* host, bool up) {
 
 int hc_stepper_upload(hc_stepper* s, const double* host_skinny) {
     int rc = set_dev(s);
+    if (!rc) rc = refresh_cur(s);
     if (rc) return rc;
     cudaMemcpy3DParms m = copy_parms(s, const_cast<double*>(host_skinny), true);
     HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
@@ -256,6 +271,7 @@ int hc_stepper_upload(hc_stepper* s, const double* host_skinny) {
 
 int hc_stepper_download(hc_stepper* s, double* host_skinny) {
     int rc = set_dev(s);
+    if (!rc) rc = refresh_cur(s);
     if (rc) return rc;
     cudaMemcpy3DParms m = copy_parms(s, host_skinny, false);
     HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
@@ -278,6 +294,8 @@ int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t
         else if (c.dt >= rem) c.dt = rem;
     }
     s->cfl = cfl;  // TimeState::cfl, a constant of the run
+    if ((rc = refresh_cur(s))) return rc;
+    c.cur = s->cur;
     HC_CUDA(cudaMemcpyAsync(s->ctl, &c, sizeof c, cudaMemcpyHostToDevice, s->st));
     HC_CUDA(cudaMemsetAsync(s->eb, 0, sizeof(ErrBlock), s->st));
     HC_CUDA(cudaStreamSynchronize(s->st));
@@ -289,7 +307,7 @@ int hc_stepper_fill_ghosts(hc_stepper* s) {
     if (rc) return rc;
     size_t n = size_t(s->sg.mx) * s->sg.my * s->sg.mz;
     k_stepper_ghosts<<<unsigned((n + 255) / 256), 256, 0, s->st>>>(
-        s->buf[s->cur], s->sg, s->o.bc[0], s->o.bc[1], s->o.bc[2]);
+        s->buf[0], s->buf[1], s->ctl, s->sg, s->o.bc[0], s->o.bc[1], s->o.bc[2]);
     s->launches++;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_stepper_ghosts");
@@ -304,7 +322,7 @@ int hc_stepper_compute(hc_stepper* s) {
                     : launch_fused_fast(a, s->p.order, s->p.solver, s->st);
     if (rc) return rc;
     s->launches++;
-    s->cur = 1 - s->cur;
+    s->cur = 1 - s->cur;  // host-side guess; the device's ctl->cur is authoritative
     return HC_OK;
 }
 
@@ -335,6 +353,7 @@ int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done) {
     HC_CUDA(cudaMemcpyAsync(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost, s->st));
     HC_CUDA(cudaMemcpyAsync(&eb, s->eb, sizeof eb, cudaMemcpyDeviceToHost, s->st));
     HC_CUDA(cudaStreamSynchronize(s->st));
+    s->cur = c.cur;
     if (t) *t = c.t;
     if (dt) *dt = c.dt;
     if (steps_done) *steps_done = long(c.steps);
@@ -342,6 +361,9 @@ int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done) {
 }
 
 int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {
+    int rc = set_dev(s);
+    if (!rc) rc = refresh_cur(s);
+    if (rc) return rc;
     if (dptr) *dptr = s->buf[s->cur];
     if (row_pitch_doubles) *row_pitch_doubles = size_t(s->sg.pitch);
     return HC_OK;

@@ -66,6 +66,10 @@ int hc_device_count(void);
 /* Measured FP64 (DFMA) throughput of `device` in TFLOP/s (2 flops per DFMA): the FP64
  * roofline denominator, which MEASURED_PEAKS.json does not carry. */
 int hc_fp64_peak(int device, double* tflops);
+/* Self-test of the fused kernel's branch-free division / sqrt: q = a/b, s = sqrt(a) through
+ * the fast paths, with flags where the IEEE slow path would be taken instead. */
+int hc_selftest_fastmath(const double* a, const double* b, size_t n, double* q, int* qslow,
+                         double* s, int* sslow);
 /* Copies the last error message of the calling thread into buf; returns its status. */
 int hc_last_error(char* buf, size_t len);
 

@@ -65,6 +65,114 @@ struct FusedShape {
         sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N + FX_N + FY_N) + 32);
 };
 
+// Face states (extrapolate_to_face + 0.5 * tau, corrector.cpp:30-33) of one zone from its
+// mode-0 neighbourhood: reconstruction (reconstruct.cpp:16-28 MC, :42-61 WENO3) and the
+// ADER predictor (predictor.cpp:26-60). pc: the zone in the current smem plane (rows W*NV
+// apart); zm2..zp2: the zone's column in planes p-2..p+2.
+template <bool O3, bool FAST>
+__device__ __forceinline__ void zone_states(const double* pc, int row, const double* zm2,
+                                            const double* zm1, const double* zp1,
+                                            const double* zp2, const FusedArgs& a, double dt,
+                                            double (*st)[NV], Fault& f) {
+    double face[6][NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        const double u0 = pc[q];
+        if (!O3) {
+            const double cfac = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
+            const double sx = mc_limiter(pc[NV + q] - u0, u0 - pc[-NV + q], cfac);
+            const double sy = mc_limiter(pc[row + q] - u0, u0 - pc[-row + q], cfac);
+            const double sz = mc_limiter(zp1[q] - u0, u0 - zm1[q], cfac);
+            face[0][q] = extrap<false>(u0, +1.0, sx, 0.0);
+            face[1][q] = extrap<false>(u0, -1.0, sx, 0.0);
+            face[2][q] = extrap<false>(u0, +1.0, sy, 0.0);
+            face[3][q] = extrap<false>(u0, -1.0, sy, 0.0);
+            face[4][q] = extrap<false>(u0, +1.0, sz, 0.0);
+            face[5][q] = extrap<false>(u0, -1.0, sz, 0.0);
+        } else {
+            double ux, uxx, uy, uyy, uz, uzz;
+            weno3<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim, ux,
+                        uxx, f);
+            weno3<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q], a.lim,
+                        uy, uyy, f);
+            weno3<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, uz, uzz, f);
+            face[0][q] = extrap<true>(u0, +1.0, ux, uxx);
+            face[1][q] = extrap<true>(u0, -1.0, ux, uxx);
+            face[2][q] = extrap<true>(u0, +1.0, uy, uyy);
+            face[3][q] = extrap<true>(u0, -1.0, uy, uyy);
+            face[4][q] = extrap<true>(u0, +1.0, uz, uzz);
+            face[5][q] = extrap<true>(u0, -1.0, uz, uzz);
+        }
+    }
+    double tau[NV];
+    predictor<O3, FAST>(face, dt, a.idx, a.idy, a.idz, a.gamma, tau, f);
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) st[s][q] = face[s][q] + 0.5 * tau[q];
+}
+
+// Cold paths: re-run in careful mode (IEEE division, exact fault capture) when the fast path
+// flagged a division outside its validity range or an unphysical state. Arguments and results
+// travel by value so the hot path's arrays stay in registers.
+struct V5 {
+    double v[NV];
+};
+struct S6 {
+    double v[6][NV];
+};
+struct Careful {
+    S6 st;
+    Fault f;
+};
+
+template <bool O3>
+__device__ __noinline__ Careful zone_states_careful(const double* pc, int row, const double* zm2,
+                                                    const double* zm1, const double* zp1,
+                                                    const double* zp2, const FusedArgs& a,
+                                                    double dt) {
+    Careful c;
+    c.f.clear();
+    zone_states<O3, false>(pc, row, zm2, zm1, zp1, zp2, a, dt, c.st.v, c.f);
+    return c;
+}
+
+struct CarefulFlux {
+    V5 f5;
+    Fault f;
+};
+
+template <int SOLVER, int A>
+__device__ __noinline__ CarefulFlux riemann_careful(V5 ul, V5 ur, double gamma) {
+    CarefulFlux c;
+    c.f.clear();
+    riemann<SOLVER, A, false>(ul.v, ur.v, gamma, c.f5.v, c.f);
+    return c;
+}
+
+__device__ __noinline__ double eval_tstep_careful(V5 u, double cfl, double dx, double dy,
+                                                  double dz, double gamma, Fault* f) {
+    return eval_tstep<false>(u.v, cfl, dx, dy, dz, gamma, *f);
+}
+
+template <int SOLVER, int A>
+__device__ __forceinline__ void face_flux(const double* ul, const double* ur, double gamma,
+                                          double* f5, Fault& f) {
+    riemann<SOLVER, A, true>(ul, ur, gamma, f5, f);
+    if (f.redo()) {
+        V5 l, r;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            l.v[q] = ul[q];
+            r.v[q] = ur[q];
+        }
+        CarefulFlux c = riemann_careful<SOLVER, A>(l, r, gamma);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) f5[q] = c.f5.v[q];
+        f = c.f;
+    }
+}
+
 template <bool O3, int SOLVER, int TX, int TY, int MINB>
 __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     fused_ader_kernel(const FusedArgs a) {
@@ -163,51 +271,21 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
         double st[6][NV];  // face states incl. 0.5*tau: E, W, N, S, T, B
         if (do_zone) {
             const double* pc = P(p) + zoff_c * NV;
-            double face[6][NV];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                const double u0 = pc[q];
-                if (!O3) {
-                    // reconstruct.cpp:16-28 (MC limited undivided slopes)
-                    const double cfac = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
-                    const double sx = mc_limiter(pc[NV + q] - u0, u0 - pc[-NV + q], cfac);
-                    const double sy =
-                        mc_limiter(pc[W * NV + q] - u0, u0 - pc[-W * NV + q], cfac);
-                    const double sz = mc_limiter(P(p + 1)[zoff_c * NV + q] - u0,
-                                                 u0 - P(p - 1)[zoff_c * NV + q], cfac);
-                    face[0][q] = extrap<false>(u0, +1.0, sx, 0.0);
-                    face[1][q] = extrap<false>(u0, -1.0, sx, 0.0);
-                    face[2][q] = extrap<false>(u0, +1.0, sy, 0.0);
-                    face[3][q] = extrap<false>(u0, -1.0, sy, 0.0);
-                    face[4][q] = extrap<false>(u0, +1.0, sz, 0.0);
-                    face[5][q] = extrap<false>(u0, -1.0, sz, 0.0);
-                } else {
-                    // reconstruct.cpp:42-61 (dimension-by-dimension WENO3)
-                    double ux, uxx, uy, uyy, uz, uzz;
-                    weno3(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
-                          ux, uxx);
-                    weno3(pc[-2 * W * NV + q], pc[-W * NV + q], u0, pc[W * NV + q],
-                          pc[2 * W * NV + q], a.lim, uy, uyy);
-                    weno3(P(p - 2)[zoff_c * NV + q], P(p - 1)[zoff_c * NV + q], u0,
-                          P(p + 1)[zoff_c * NV + q], P(p + 2)[zoff_c * NV + q], a.lim, uz, uzz);
-                    face[0][q] = extrap<true>(u0, +1.0, ux, uxx);
-                    face[1][q] = extrap<true>(u0, -1.0, ux, uxx);
-                    face[2][q] = extrap<true>(u0, +1.0, uy, uyy);
-                    face[3][q] = extrap<true>(u0, -1.0, uy, uyy);
-                    face[4][q] = extrap<true>(u0, +1.0, uz, uzz);
-                    face[5][q] = extrap<true>(u0, -1.0, uz, uzz);
-                }
-            }
+            const double* zm1 = P(p - 1) + zoff_c * NV;
+            const double* zp1 = P(p + 1) + zoff_c * NV;
+            const double* zm2 = O3 ? P(p - 2) + zoff_c * NV : zm1;
+            const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
             Fault f;
             f.clear();
-            double tau[NV];
-            predictor<O3>(face, dt, a.idx, a.idy, a.idz, a.gamma, tau, f);
-            if (f.code) record_fault(a.eb, ST_PREDICT, f, ia, ja, p, 0);
-            // corrector face states: extrapolate_to_face + 0.5 * tau (corrector.cpp:30-33)
+            zone_states<O3, true>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
+            if (f.redo()) {
+                Careful c = zone_states_careful<O3>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
 #pragma unroll
-            for (int s = 0; s < 6; ++s)
+                for (int s = 0; s < 6; ++s)
 #pragma unroll
-                for (int q = 0; q < NV; ++q) st[s][q] = face[s][q] + 0.5 * tau[q];
+                    for (int q = 0; q < NV; ++q) st[s][q] = c.st.v[s][q];
+                if (c.f.code) record_fault(a.eb, ST_PREDICT, c.f, ia, ja, p, 0);
+            }
             if (!zring) {
                 if (ci <= TX - 1 && cj >= 0 && cj < TY)
 #pragma unroll
@@ -228,7 +306,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                     for (int q = 0; q < NV; ++q) ul[q] = XP[(cj * (TX + 1) + ci) * NV + q];
                     Fault f;
                     f.clear();
-                    riemann<SOLVER, 0>(ul, st[1], a.gamma, f5, f);
+                    face_flux<SOLVER, 0>(ul, st[1], a.gamma, f5, f);
                     if (f.code) record_fault(a.eb, ST_FLUX, f, ia, ja, p, 0);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) FX[(cj * (TX + 1) + ci) * NV + q] = f5[q];
@@ -241,7 +319,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                     for (int q = 0; q < NV; ++q) ul[q] = YP[(cj * TX + ci) * NV + q];
                     Fault f;
                     f.clear();
-                    riemann<SOLVER, 1>(ul, st[3], a.gamma, f5, f);
+                    face_flux<SOLVER, 1>(ul, st[3], a.gamma, f5, f);
                     if (f.code) record_fault(a.eb, ST_FLUX, f, ja, ia, p, 1);
 #pragma unroll
                     for (int q = 0; q < NV; ++q) FY[(cj * TX + ci) * NV + q] = f5[q];
@@ -250,7 +328,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             if (owned && lp >= 0) {  // z face at the bottom of plane p
                 Fault f;
                 f.clear();
-                riemann<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
+                face_flux<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
                 if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
             }
         }
@@ -271,7 +349,14 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 for (int q = 0; q < NV; ++q) dst[q] = un[q];
                 Fault f;
                 f.clear();
-                double d = eval_tstep(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                double d = eval_tstep<true>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                if (f.redo()) {
+                    V5 u5;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
+                    f.clear();
+                    d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
+                }
                 if (f.code) record_fault(a.eb, ST_UPDATE, f, ia, ja, p - 1, 0);
                 else dt_min = smin(dt_min, d);
             }

@@ -37,7 +37,7 @@ template <bool O3>
 struct FusedTile {
     static constexpr int TX = 16;
     static constexpr int TY = 8;
-    static constexpr int MINB = O3 ? 2 : 3;  // resident CTAs per SM the registers must allow
+    static constexpr int MINB = 2;  // resident CTAs per SM the registers must allow
 };
 
 int launch_fused_exact(const FusedArgs& a, int order, int solver, cudaStream_t st);

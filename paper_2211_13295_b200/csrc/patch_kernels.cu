@@ -110,9 +110,11 @@ __global__ void k_recon_o3(double* m, G g, Limiter L) {
     for (int q = 0; q < NV; ++q) {
         double* zc = m + zoff(g, k, j, i) * NV * 11 + q * 11;
         double ux, uxx, uy, uyy, uz, uzz;
-        weno3(zc[-2 * sx], zc[-sx], zc[0], zc[sx], zc[2 * sx], L, ux, uxx);
-        weno3(zc[-2 * sy], zc[-sy], zc[0], zc[sy], zc[2 * sy], L, uy, uyy);
-        weno3(zc[-2 * sz], zc[-sz], zc[0], zc[sz], zc[2 * sz], L, uz, uzz);
+        Fault f;  // careful mode: IEEE division, nothing to report from a reconstruction
+        f.clear();
+        weno3(zc[-2 * sx], zc[-sx], zc[0], zc[sx], zc[2 * sx], L, ux, uxx, f);
+        weno3(zc[-2 * sy], zc[-sy], zc[0], zc[sy], zc[2 * sy], L, uy, uyy, f);
+        weno3(zc[-2 * sz], zc[-sz], zc[0], zc[sz], zc[2 * sz], L, uz, uzz, f);
         zc[1] = ux;
         zc[2] = uy;
         zc[3] = uz;
@@ -1090,3 +1092,47 @@ int hc_dev_update_u_timestep(const hc_geom* g, int modes, double* modal, double*
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------- self test
+// The fused kernel's branch-free division/sqrt (pointwise.cuh div_fast/sqrt_fast) must equal
+// IEEE a / b and sqrt(a) bit for bit whenever they report "no slow path needed".
+namespace hc {
+__global__ void k_fastmath(const double* a, const double* b, size_t n, double* q, int* qslow,
+                           double* s, int* sslow) {
+    size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    bool slow = false;
+    q[i] = hc::div_fast(a[i], b[i], slow);
+    qslow[i] = slow;
+    slow = false;
+    s[i] = hc::sqrt_fast(a[i], slow);
+    sslow[i] = slow;
+}
+}  // namespace hc
+
+extern "C" int hc_selftest_fastmath(const double* a, const double* b, size_t n, double* q,
+                                    int* qslow, double* s, int* sslow) {
+    double *da, *db, *dq, *ds;
+    int *dqs, *dss;
+    HC_CUDA(cudaMalloc(&da, n * 8));
+    HC_CUDA(cudaMalloc(&db, n * 8));
+    HC_CUDA(cudaMalloc(&dq, n * 8));
+    HC_CUDA(cudaMalloc(&ds, n * 8));
+    HC_CUDA(cudaMalloc(&dqs, n * 4));
+    HC_CUDA(cudaMalloc(&dss, n * 4));
+    HC_CUDA(cudaMemcpy(da, a, n * 8, cudaMemcpyHostToDevice));
+    HC_CUDA(cudaMemcpy(db, b, n * 8, cudaMemcpyHostToDevice));
+    k_fastmath<<<unsigned((n + 255) / 256), 256>>>(da, db, n, dq, dqs, ds, dss);
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaMemcpy(q, dq, n * 8, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(s, ds, n * 8, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(qslow, dqs, n * 4, cudaMemcpyDeviceToHost));
+    HC_CUDA(cudaMemcpy(sslow, dss, n * 4, cudaMemcpyDeviceToHost));
+    cudaFree(da);
+    cudaFree(db);
+    cudaFree(dq);
+    cudaFree(ds);
+    cudaFree(dqs);
+    cudaFree(dss);
+    return HC_OK;
+}

@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--order", type=int, default=3)
     ap.add_argument("--fast", action="store_true", help="FMA-contracted build")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
@@ -284,9 +285,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
-            dom.upload(host)
-            dom.step()
-            dom.download(host)
+            dom.st.step_host(host, host, args.e2e_chunks)
             dom.sync()
         e1.record(stream)
         torch.cuda.synchronize()
@@ -294,7 +293,9 @@ def main():
         nbytes = host.nbytes
         e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 16,
-               "steps": args.e2e_steps, "api": "hc_stepper_upload/step/download/sync"}
+               "steps": args.e2e_steps, "chunks": args.e2e_chunks,
+               "api": "hc_stepper_step_host (H2D of U_skinny, fused step, D2H, pipelined by "
+                      "z-chunks) + hc_stepper_sync (dt_next)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -194,6 +194,11 @@ int hc_stepper_download(hc_stepper* s, double* host_skinny);
 int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t_final);
 /* Enqueue n fused steps (no host sync). */
 int hc_stepper_step(hc_stepper* s, int n);
+/* One step end to end from HOST memory: H2D of host_in (U_skinny, ghosts included), the
+ * fused step, D2H of the updated active planes into host_out (may equal host_in),
+ * pipelined over nchunks z-chunks on three streams so both PCIe directions overlap the
+ * kernel. Returns after host_out is complete. */
+int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out, int nchunks);
 /* Synchronise; report t, dt (of the next step), steps done, and device errors. */
 int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done);
 /* Device pointer of the current state buffer and its pitch (doubles per row of mx*5+pad);

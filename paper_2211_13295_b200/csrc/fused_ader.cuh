@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     const bool yface = ci >= 0 && ci < TX && cj >= 0 && ia < a.nx && ja <= a.ny &&
                        (cj >= 1 || ja < a.ny);
     const bool exists = ia >= -1 && ia <= a.nx && ja >= -1 && ja <= a.ny;
-    const int kz0 = blockIdx.z * a.tz;                       // first active plane (active z)
-    const int nzc = min(a.tz, a.nz - kz0);
+    const int kz0 = a.kz_first + blockIdx.z * a.tz;  // first active plane (active z)
+    const int nzc = min(a.tz, a.kz_last - kz0);
     const double dt = a.ctl->dt;
     const double cx = dt / a.dx, cy = dt / a.dy, cz = dt / a.dz;  // corrector.cpp:75
 

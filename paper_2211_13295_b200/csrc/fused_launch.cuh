@@ -21,7 +21,7 @@ static int launch_one(const FusedArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fused)");
         configured = true;
     }
-    dim3 grid((a.nx + T::TX - 1) / T::TX, (a.ny + T::TY - 1) / T::TY, (a.nz + a.tz - 1) / a.tz);
+    dim3 grid((a.nx + T::TX - 1) / T::TX, (a.ny + T::TY - 1) / T::TY, (a.kz_last - a.kz_first + a.tz - 1) / a.tz);
     kern<<<grid, S::NT, S::SMEM, st>>>(a);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "fused_ader_kernel launch");

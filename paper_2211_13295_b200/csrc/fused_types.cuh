@@ -25,6 +25,8 @@ struct FusedArgs {
     int my_pad;      // rows per plane in storage
     int pitch;       // doubles per row in storage
     int tz;          // planes per CTA chunk
+    int kz_first;    // active planes [kz_first, kz_last) updated by this launch
+    int kz_last;
     double dx, dy, dz, idx, idy, idz;
     double gamma, cfl;
     Limiter lim;

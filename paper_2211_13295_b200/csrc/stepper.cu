@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "fused_types.cuh"
 
@@ -27,21 +28,15 @@ __device__ __forceinline__ int map_index(int a, int n, int kind) {
 }
 
 // Ghost gather (see k_fill_ghosts in patch_kernels.cu for why one gather equals the
-// reference's sequential x, y, z passes). bz < 0: z ghosts belong to the caller (halo
-// exchange of a z-slab decomposition); only ghosts of active planes are filled then, which is
-// exactly the x and y passes of transfer.cpp:94-130.
-__global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g, int bx, int by,
-                                 int bz) {
-    if (c->done) return;
-    double* u = c->cur ? b1 : b0;
-    size_t id = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    size_t n = size_t(g.mx) * g.my * g.mz;
-    if (id >= n) return;
-    int i = int(id % g.mx), j = int((id / g.mx) % g.my), k = int(id / (size_t(g.mx) * g.my));
+// reference's sequential x, y, z passes), restricted to storage planes [k_lo, k_hi) and
+// enumerating ghost zones only: for an active plane its x/y ghost ring (2*gh full rows +
+// 2*gh columns of the ny active rows), for a z-ghost plane the whole plane. bz < 0: z ghosts
+// belong to the caller (halo exchange of a z-slab decomposition), which is exactly the x and
+// y passes of transfer.cpp:94-130 on this rank.
+__device__ __forceinline__ void ghost_copy(double* u, const SG& g, int bx, int by, int bz,
+                                           int i, int j, int k) {
     bool ai = i >= g.gh && i < g.gh + g.nx, aj = j >= g.gh && j < g.gh + g.ny,
          ak = k >= g.gh && k < g.gh + g.nz;
-    if (ai && aj && ak) return;
-    if (!ak && bz < 0) return;
     int si = ai ? i : g.gh + map_index(i - g.gh, g.nx, bx);
     int sj = aj ? j : g.gh + map_index(j - g.gh, g.ny, by);
     int sk = ak ? k : g.gh + map_index(k - g.gh, g.nz, bz);
@@ -49,6 +44,37 @@ __global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g,
     double* dst = u + (size_t(k) * g.my_pad + j) * g.pitch + size_t(i) * NV;
 #pragma unroll
     for (int q = 0; q < NV; ++q) dst[q] = src[q];
+}
+
+// blockIdx.y = plane k_lo + y. ring_mode: the planes are active, fill their x/y ghost ring
+// (2*gh full rows + 2*gh columns of the ny active rows); otherwise they are z-ghost planes,
+// fill every zone.
+__global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g, int bx, int by,
+                                 int bz, int k_lo, int ring_mode) {
+    if (c->done) return;
+    double* u = c->cur ? b1 : b0;
+    const int k = k_lo + blockIdx.y;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    int i, j;
+    if (!ring_mode) {
+        if (r >= size_t(g.mx) * g.my) return;
+        i = int(r % g.mx);
+        j = int(r / g.mx);
+    } else {
+        const size_t rows = size_t(2 * g.gh) * g.mx;
+        if (r >= rows + size_t(2 * g.gh) * g.ny) return;
+        if (r < rows) {  // full ghost rows j < gh or j >= gh + ny
+            int jr = int(r / g.mx);
+            i = int(r % g.mx);
+            j = jr < g.gh ? jr : g.ny + jr;
+        } else {  // ghost columns of the active rows
+            size_t t = r - rows;
+            int col = int(t % (2 * g.gh));
+            j = g.gh + int(t / (2 * g.gh));
+            i = col < g.gh ? col : g.nx + col;
+        }
+    }
+    ghost_copy(u, g, bx, by, bz, i, j, k);
 }
 
 __global__ void k_advance(StepCtl* c, const ErrBlock* eb) {
@@ -92,6 +118,9 @@ struct hc_stepper {
     int tz = 32;
     size_t bytes = 0;
     double cfl = 0.6;
+    // pipelined host step (hc_stepper_step_host)
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<cudaEvent_t> ev;
 };
 
 namespace {
@@ -112,6 +141,8 @@ FusedArgs fused_args(const hc_stepper* s) {
     a.my_pad = s->sg.my_pad;
     a.pitch = s->sg.pitch;
     a.tz = s->tz;
+    a.kz_first = 0;
+    a.kz_last = s->g.nz;
     a.dx = s->g.dx;
     a.dy = s->g.dy;
     a.dz = s->g.dz;
@@ -229,6 +260,9 @@ int hc_stepper_destroy(hc_stepper* s) {
     cudaFree(s->buf[1]);
     cudaFree(s->ctl);
     cudaFree(s->eb);
+    for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
+    if (s->s_h2d) cudaStreamDestroy(s->s_h2d);
+    if (s->s_d2h) cudaStreamDestroy(s->s_d2h);
     if (s->own_stream && s->st) cudaStreamDestroy(s->st);
     delete s;
     return HC_OK;
@@ -302,15 +336,35 @@ int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t
     return HC_OK;
 }
 
+// Ghost fill of storage planes [k_lo, k_hi): active planes get their x/y ring, z-ghost
+// planes (when this stepper owns the z boundary) are filled whole.
+static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
+    const SG& g = s->sg;
+    k_lo = std::max(k_lo, 0);
+    k_hi = std::min(k_hi, g.mz);
+    const int a_lo = std::max(k_lo, g.gh), a_hi = std::min(k_hi, g.gh + g.nz);
+    const unsigned ring = unsigned(2 * g.gh * (g.mx + g.ny));
+    const unsigned plane = unsigned(g.mx * g.my);
+    auto launch = [&](int lo, int hi, int ring_mode) {
+        if (hi <= lo) return;
+        dim3 grid(((ring_mode ? ring : plane) + 255) / 256, unsigned(hi - lo));
+        k_stepper_ghosts<<<grid, 256, 0, st>>>(s->buf[0], s->buf[1], s->ctl, g, s->o.bc[0],
+                                               s->o.bc[1], s->o.bc[2], lo, ring_mode);
+        s->launches++;
+    };
+    launch(a_lo, a_hi, 1);
+    if (s->o.bc[2] >= 0) {
+        launch(k_lo, std::min(k_hi, g.gh), 0);
+        launch(std::max(k_lo, g.gh + g.nz), k_hi, 0);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_stepper_ghosts");
+}
+
 int hc_stepper_fill_ghosts(hc_stepper* s) {
     int rc = set_dev(s);
     if (rc) return rc;
-    size_t n = size_t(s->sg.mx) * s->sg.my * s->sg.mz;
-    k_stepper_ghosts<<<unsigned((n + 255) / 256), 256, 0, s->st>>>(
-        s->buf[0], s->buf[1], s->ctl, s->sg, s->o.bc[0], s->o.bc[1], s->o.bc[2]);
-    s->launches++;
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_stepper_ghosts");
+    return fill_planes(s, 0, s->sg.mz, s->st);
 }
 
 int hc_stepper_compute(hc_stepper* s) {
@@ -342,6 +396,94 @@ int hc_stepper_step(hc_stepper* s, int n) {
         if (!rc) rc = hc_stepper_advance(s);
         if (rc) return rc;
     }
+    return HC_OK;
+}
+
+// Copies storage planes [k_lo, k_hi) between the host layout [mz][my][mx][5] and the pitched
+// device buffer.
+static int copy_planes(hc_stepper* s, double* dev, double* host, int k_lo, int k_hi, bool up,
+                       cudaStream_t st) {
+    if (k_hi <= k_lo) return HC_OK;
+    const SG& g = s->sg;
+    const size_t row = size_t(g.mx) * NV * sizeof(double);
+    cudaMemcpy3DParms m;
+    std::memset(&m, 0, sizeof m);
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host + size_t(k_lo) * g.my * g.mx * NV, row, row, g.my);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dev + size_t(k_lo) * g.my_pad * g.pitch,
+                                            size_t(g.pitch) * sizeof(double), row, g.my_pad);
+    m.srcPtr = up ? hp : dp;
+    m.dstPtr = up ? dp : hp;
+    m.extent = make_cudaExtent(row, g.my, size_t(k_hi - k_lo));
+    m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    HC_CUDA(cudaMemcpy3DAsync(&m, st));
+    return HC_OK;
+}
+
+// One ADER step end to end from host memory: H2D of U_skinny, ghost fill, fused update, D2H
+// of the updated active planes, pipelined over z-chunks on three streams so the two PCIe
+// directions and the kernel overlap (chunk c computes while c+1 uploads and c-1 downloads).
+// host_in may equal host_out. Pinned host memory gives the overlap; pageable still works.
+int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out, int nchunks) {
+    int rc = set_dev(s);
+    if (!rc) rc = refresh_cur(s);
+    if (rc) return rc;
+    if (s->o.bc[2] < 0) {
+        set_error(HC_INVALID, "hc_stepper_step_host needs a z boundary owned by the stepper");
+        return HC_INVALID;
+    }
+    const SG& g = s->sg;
+    const int G = s->p.order == 3 ? 3 : 2;
+    nchunks = std::max(1, std::min(nchunks, g.nz / 4));
+    if (!s->s_h2d) {
+        HC_CUDA(cudaStreamCreateWithFlags(&s->s_h2d, cudaStreamNonBlocking));
+        HC_CUDA(cudaStreamCreateWithFlags(&s->s_d2h, cudaStreamNonBlocking));
+    }
+    const size_t need = size_t(3 * nchunks + 3);
+    while (s->ev.size() < need) {
+        cudaEvent_t e;
+        HC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        s->ev.push_back(e);
+    }
+    cudaEvent_t* ev_up = s->ev.data();                // [nchunks]
+    cudaEvent_t* ev_comp = ev_up + nchunks;           // [nchunks]
+    cudaEvent_t ev_start = s->ev[2 * nchunks];
+    cudaEvent_t ev_wrap = s->ev[2 * nchunks + 1];
+    double* in = s->buf[s->cur];
+    double* out = s->buf[1 - s->cur];
+    double* hin = const_cast<double*>(host_in);
+    // order after previous work on the compute stream (the state must be idle)
+    HC_CUDA(cudaEventRecord(ev_start, s->st));
+    HC_CUDA(cudaStreamWaitEvent(s->s_h2d, ev_start, 0));
+    HC_CUDA(cudaStreamWaitEvent(s->s_d2h, ev_start, 0));
+    // the top active planes first: they feed the periodic bottom ghosts of chunk 0
+    if ((rc = copy_planes(s, in, hin, g.gh + g.nz - G, g.gh + g.nz, true, s->s_h2d))) return rc;
+    HC_CUDA(cudaEventRecord(ev_wrap, s->s_h2d));
+    int uploaded = 0;  // storage planes [0, uploaded) are on the device
+    for (int c = 0; c < nchunks; ++c) {
+        const int c0 = int((long(g.nz) * c) / nchunks), c1 = int((long(g.nz) * (c + 1)) / nchunks);
+        const int hi = (c == nchunks - 1) ? g.mz : std::min(g.mz, g.gh + c1 + G);
+        if ((rc = copy_planes(s, in, hin, uploaded, hi, true, s->s_h2d))) return rc;
+        HC_CUDA(cudaEventRecord(ev_up[c], s->s_h2d));
+        HC_CUDA(cudaStreamWaitEvent(s->st, ev_up[c], 0));
+        if (c == 0) HC_CUDA(cudaStreamWaitEvent(s->st, ev_wrap, 0));
+        if ((rc = fill_planes(s, uploaded, hi, s->st))) return rc;
+        uploaded = hi;
+        FusedArgs a = fused_args(s);
+        a.cfl = s->cfl;
+        a.kz_first = c0;
+        a.kz_last = c1;
+        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, s->st)
+                        : launch_fused_fast(a, s->p.order, s->p.solver, s->st);
+        if (rc) return rc;
+        s->launches++;
+        HC_CUDA(cudaEventRecord(ev_comp[c], s->st));
+        HC_CUDA(cudaStreamWaitEvent(s->s_d2h, ev_comp[c], 0));
+        if ((rc = copy_planes(s, out, host_out, g.gh + c0, g.gh + c1, false, s->s_d2h))) return rc;
+    }
+    s->cur = 1 - s->cur;
+    if ((rc = hc_stepper_advance(s))) return rc;
+    HC_CUDA(cudaStreamSynchronize(s->s_d2h));
+    HC_CUDA(cudaStreamSynchronize(s->st));
     return HC_OK;
 }
 

@@ -345,6 +345,12 @@ class Stepper:
     def step(self, n=1):
         _check(self.lib.hc_stepper_step(self.h, n))
 
+    def step_host(self, host_in: np.ndarray, host_out: np.ndarray | None = None, chunks=16):
+        """One step end to end from host memory (pipelined H2D / fused step / D2H)."""
+        host_out = host_in if host_out is None else host_out
+        _check(self.lib.hc_stepper_step_host(self.h, _p(host_in), _p(host_out), int(chunks)))
+        return host_out
+
     def fill_ghosts(self):
         _check(self.lib.hc_stepper_fill_ghosts(self.h))
 

@@ -21,11 +21,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin",
                  "/usr/bin/g++", "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
+TUNE = ["-DHC_TUNE"] if os.environ.get("HC_TUNE") == "1" else []
 SOURCES = {
     "capi_common.cu": ["--fmad=false"],
     "patch_kernels.cu": ["--fmad=false"],
     "stepper.cu": ["--fmad=false"],
-    "fused_exact.cu": ["--fmad=false"],
+    "fused_exact.cu": ["--fmad=false"] + TUNE,
     "fused_fast.cu": ["--fmad=true"],
     "peak.cu": ["--fmad=true"],
 }
@@ -33,7 +34,9 @@ SOURCES = {
 
 def _compile(name, flags, verbose):
     src = os.path.join(CSRC, name)
-    obj = os.path.join(BUILD, name.replace(".cu", ".o"))
+    import hashlib
+    tag = hashlib.sha1(" ".join(COMMON + flags).encode()).hexdigest()[:8]
+    obj = os.path.join(BUILD, name.replace(".cu", f".{tag}.o"))
     log = os.path.join(BUILD, name.replace(".cu", ".ptxas.txt"))
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     deps.append(os.path.join(ROOT, "include", "hydro_cuda.h"))

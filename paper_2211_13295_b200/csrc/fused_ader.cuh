@@ -51,7 +51,10 @@ template <bool O3, int TX, int TY>
 struct FusedShape {
     static constexpr int R = O3 ? 2 : 1;   // reconstruction stencil radius
     static constexpr int G = R + 1;        // halo: one ring + stencil
-    static constexpr int NB = 2 * R + 2;   // plane ring buffer
+    // plane ring: O3 refills the slot of plane p-2 after the predict phase (5 slots); O2's
+    // oldest plane (p-1) is read until the end of the iteration, so it keeps a spare slot
+    static constexpr int NB = O3 ? 2 * R + 1 : 2 * R + 2;
+    static constexpr bool LATE_LOAD = O3;
     static constexpr int W = TX + 2 * G;
     static constexpr int H = TY + 2 * G;
     static constexpr int PLANE = W * H * NV;  // doubles per smem plane
@@ -61,8 +64,9 @@ struct FusedShape {
     static constexpr int YP_N = (TY + 1) * TX;  // +y states, rows -1..TY-1
     static constexpr int FX_N = TY * (TX + 1);  // x faces 0..TX
     static constexpr int FY_N = (TY + 1) * TX;  // y faces 0..TY
-    static constexpr size_t SMEM =
-        sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N + FX_N + FY_N) + 32);
+    // FX aliases XP and FY aliases YP: each face's thread reads its +x/+y neighbour state and
+    // then writes that face's flux to the same slot (no other reader in between)
+    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32);
 };
 
 // Face states (extrapolate_to_face + 0.5 * tau, corrector.cpp:30-33) of one zone from its
@@ -187,9 +191,9 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     double* planes = smem;                          // [NB][H][W][5]
     double* XP = planes + size_t(NB) * S::PLANE;    // [TY][TX+1][5]
     double* YP = XP + S::XP_N * NV;                 // [TY+1][TX][5]
-    double* FX = YP + S::YP_N * NV;                 // [TY][TX+1][5]
-    double* FY = FX + S::FX_N * NV;                 // [TY+1][TX][5]
-    double* red = FY + S::FY_N * NV;                // [32]
+    double* FX = XP;                                // [TY][TX+1][5], aliases XP
+    double* FY = YP;                                // [TY+1][TX][5], aliases YP
+    double* red = YP + S::YP_N * NV;                // [32]
 
     const int tid = threadIdx.x;
     // ---- E-column of this thread
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
         const int p = kz0 + lp;
         cp_async_wait_all();
         __syncthreads();
-        if (lp <= nzc - 1) load_plane(p + R + 1);
+        if (!S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
 
         const bool zring = (lp == -1 || lp == nzc);
         const bool do_zone = zring ? owned : exists;
@@ -296,6 +300,8 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             }
         }
         __syncthreads();
+        // plane p-R is no longer read this iteration: refill its slot with p+R+1
+        if (S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
         // ---------------------------------------------------------------- flux
         double fz_cur[NV];
         if (do_zone) {

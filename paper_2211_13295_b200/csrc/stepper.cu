@@ -161,6 +161,10 @@ FusedArgs fused_args(const hc_stepper* s) {
 
 }  // namespace
 
+static size_t state_bytes(const hc_stepper* s) {
+    return size_t(s->sg.mz) * s->sg.my * s->sg.mx * NV * sizeof(double);
+}
+
 // Reads which buffer is current from the device (steps after t_final or after a failure
 // are no-ops, so the host's per-launch guess can be off).
 static int refresh_cur(hc_stepper* s) {
@@ -215,16 +219,19 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     sg.mx = mx_of(*g);
     sg.my = my_of(*g);
     sg.mz = mz_of(*g);
-    int ntx = (g->nx + TX - 1) / TX, nty = (g->ny + TY - 1) / TY;
-    int cols = std::max(sg.mx, ntx * TX + g->ghost + G);
-    sg.my_pad = std::max(sg.my, nty * TY + g->ghost + G);
-    sg.pitch = (cols * NV + 15) / 16 * 16;  // 128-byte rows
+    // The device layout IS the host SkinnyState layout (fields.hpp:47-67): transfers are
+    // contiguous plane ranges. Tiles hanging over the x/y edge of the mesh read the next
+    // row / plane (those zones are masked), and the last plane's overhang lands in the slack.
+    sg.my_pad = sg.my;
+    sg.pitch = sg.mx * NV;
+    const size_t slack = size_t(TY + 2 * G + 2) * sg.pitch + size_t(TX + 2 * G) * NV;
+    (void)TX;
     s->tz = std::max(4, std::min(32, g->nz));
     if ((rc = set_dev(s))) {
         delete s;
         return rc;
     }
-    s->bytes = size_t(sg.mz) * sg.my_pad * sg.pitch * sizeof(double);
+    s->bytes = (size_t(sg.mz) * sg.my_pad * sg.pitch + slack) * sizeof(double);
     cudaError_t e = cudaMalloc(&s->buf[0], s->bytes);
     if (e == cudaSuccess) e = cudaMalloc(&s->buf[1], s->bytes);
     if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(StepCtl));
@@ -280,26 +287,12 @@ int hc_stepper_set_stream(hc_stepper* s, void* stream) {
     return HC_OK;
 }
 
-static cudaMemcpy3DParms copy_parms(hc_stepper* s, double* host, bool up) {
-    cudaMemcpy3DParms m;
-    std::memset(&m, 0, sizeof m);
-    const size_t row = size_t(s->sg.mx) * NV * sizeof(double);
-    cudaPitchedPtr hp = make_cudaPitchedPtr(host, row, row, s->sg.my);
-    cudaPitchedPtr dp = make_cudaPitchedPtr(s->buf[s->cur], size_t(s->sg.pitch) * sizeof(double),
-                                            row, s->sg.my_pad);
-    m.srcPtr = up ? hp : dp;
-    m.dstPtr = up ? dp : hp;
-    m.extent = make_cudaExtent(row, s->sg.my, s->sg.mz);
-    m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    return m;
-}
-
 int hc_stepper_upload(hc_stepper* s, const double* host_skinny) {
     int rc = set_dev(s);
     if (!rc) rc = refresh_cur(s);
     if (rc) return rc;
-    cudaMemcpy3DParms m = copy_parms(s, const_cast<double*>(host_skinny), true);
-    HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
+    HC_CUDA(cudaMemcpyAsync(s->buf[s->cur], host_skinny, state_bytes(s), cudaMemcpyHostToDevice,
+                            s->st));
     return HC_OK;
 }
 
@@ -307,8 +300,8 @@ int hc_stepper_download(hc_stepper* s, double* host_skinny) {
     int rc = set_dev(s);
     if (!rc) rc = refresh_cur(s);
     if (rc) return rc;
-    cudaMemcpy3DParms m = copy_parms(s, host_skinny, false);
-    HC_CUDA(cudaMemcpy3DAsync(&m, s->st));
+    HC_CUDA(cudaMemcpyAsync(host_skinny, s->buf[s->cur], state_bytes(s), cudaMemcpyDeviceToHost,
+                            s->st));
     HC_CUDA(cudaStreamSynchronize(s->st));
     return HC_OK;
 }
@@ -399,23 +392,16 @@ int hc_stepper_step(hc_stepper* s, int n) {
     return HC_OK;
 }
 
-// Copies storage planes [k_lo, k_hi) between the host layout [mz][my][mx][5] and the pitched
-// device buffer.
+// Copies storage planes [k_lo, k_hi) between host and device (identical layouts).
 static int copy_planes(hc_stepper* s, double* dev, double* host, int k_lo, int k_hi, bool up,
                        cudaStream_t st) {
     if (k_hi <= k_lo) return HC_OK;
-    const SG& g = s->sg;
-    const size_t row = size_t(g.mx) * NV * sizeof(double);
-    cudaMemcpy3DParms m;
-    std::memset(&m, 0, sizeof m);
-    cudaPitchedPtr hp = make_cudaPitchedPtr(host + size_t(k_lo) * g.my * g.mx * NV, row, row, g.my);
-    cudaPitchedPtr dp = make_cudaPitchedPtr(dev + size_t(k_lo) * g.my_pad * g.pitch,
-                                            size_t(g.pitch) * sizeof(double), row, g.my_pad);
-    m.srcPtr = up ? hp : dp;
-    m.dstPtr = up ? dp : hp;
-    m.extent = make_cudaExtent(row, g.my, size_t(k_hi - k_lo));
-    m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    HC_CUDA(cudaMemcpy3DAsync(&m, st));
+    const size_t plane = size_t(s->sg.my) * s->sg.mx * NV;
+    const size_t off = size_t(k_lo) * plane, bytes = size_t(k_hi - k_lo) * plane * sizeof(double);
+    if (up)
+        HC_CUDA(cudaMemcpyAsync(dev + off, host + off, bytes, cudaMemcpyHostToDevice, st));
+    else
+        HC_CUDA(cudaMemcpyAsync(host + off, dev + off, bytes, cudaMemcpyDeviceToHost, st));
     return HC_OK;
 }
 

@@ -179,6 +179,9 @@ typedef struct {
      * 0: FMA-contracted build (<= 1e-13 rel. L1 drift after 200 steps). */
     int exact;
     int device;
+    /* 0: ADER one-step (stepper.cpp:49-78); 2: Heun RK2; 3: SSP-RK3 (stepper.cpp:80-157) --
+     * every RK stage is one fused launch with the temporal mode zero */
+    int integrator;
 } hc_stepper_opts;
 
 int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opts* o,
@@ -201,8 +204,8 @@ int hc_stepper_step(hc_stepper* s, int n);
 int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out, int nchunks);
 /* Synchronise; report t, dt (of the next step), steps done, and device errors. */
 int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done);
-/* Device pointer of the current state buffer and its pitch (doubles per row of mx*5+pad);
- * used for z-halo exchange by the multi-GPU driver. */
+/* Device pointer of the state the next fused launch reads (the current RK stage's input)
+ * and its row pitch in doubles; used for z-halo exchange by the multi-GPU driver. */
 int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles);
 /* Device pointer of the scalar dt_next of the last step (for an all-reduce(min)) and the
  * device pointer of the dt the next step will use. */
@@ -212,6 +215,9 @@ int hc_stepper_dt_ptrs(hc_stepper* s, double** dt_next_dev, double** dt_dev);
 int hc_stepper_fill_ghosts(hc_stepper* s);
 int hc_stepper_compute(hc_stepper* s);
 int hc_stepper_advance(hc_stepper* s);
+/* fused launches per step: 1 (ADER), 2 or 3 (RK); a multi-GPU step repeats fill_ghosts +
+ * halo exchange + compute per stage, then all-reduce + advance */
+int hc_stepper_stages(hc_stepper* s);
 /* Number of kernels this library launched on the stepper (diagnostic / bench claim). */
 long hc_stepper_launches(hc_stepper* s);
 /* Storage layout of the state buffers: rows per plane, doubles per row, planes. */

@@ -27,7 +27,7 @@ SOURCES = {
     "patch_kernels.cu": ["--fmad=false"],
     "stepper.cu": ["--fmad=false"],
     "fused_exact.cu": ["--fmad=false"] + TUNE,
-    "fused_fast.cu": ["--fmad=true"],
+    "fused_fast.cu": ["--fmad=true"] + TUNE,
     "peak.cu": ["--fmad=true"],
 }
 
@@ -79,13 +79,19 @@ def build(verbose=True) -> str:
         futs = [ex.submit(_compile, k, v, verbose) for k, v in SOURCES.items()]
         futs += [ex.submit(_compile_host, h, verbose) for h in HOST_SOURCES]
         objs = [f.result() for f in futs]
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+    stamp = LIB + ".objs"
+    listing = "\n".join(objs)
+    same_set = os.path.exists(stamp) and open(stamp).read() == listing
+    if same_set and os.path.exists(LIB) and \
+            os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-o", tmp] + ARCH + ["-ccbin", "/usr/bin/g++", "-Xcompiler",
                                                  "-fopenmp"] + objs
     subprocess.run(cmd, check=True)
     shutil.move(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(listing)
     if verbose:
         print(f"[build] {LIB}")
     return LIB

@@ -69,11 +69,52 @@ struct FusedShape {
     static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32);
 };
 
+#ifndef HC_REASSOC
+#define HC_REASSOC 0
+#endif
+
+// WENO3 point (reconstruct.hpp:46-73) for the FMA build: the normalised weights
+// (w_k / P_k) / sum_j (w_j / P_j) with P_k = (eps + IS_k)^2 are evaluated as
+// (w_k prod_{j!=k} P_j) / sum_j (w_j prod_{i!=j} P_i) -- one division instead of four.
+// Same mathematics, different rounding (<= a few ulp per weight); used only when the
+// translation unit opts out of bit-exactness (fused_fast.cu). P_k lies in [eps^2, ~1e12]
+// for physical states, so the triple products stay far from over/underflow.
+template <bool FAST>
+__device__ __forceinline__ void weno3_1div(double s0, double s1, double s2, double s3,
+                                           double s4, const Limiter& L, double& ux, double& uxx,
+                                           Fault& f) {
+    double d0 = s1 - s0, d1 = s2 - s1, d2 = s3 - s2, d3 = s4 - s3;
+    double ux_l = 0.5 * (3.0 * d1 - d0);
+    double uxx_l = 0.5 * (d1 - d0);
+    double ux_c = 0.5 * (d1 + d2);
+    double uxx_c = 0.5 * (d2 - d1);
+    double ux_r = 0.5 * (3.0 * d2 - d3);
+    double uxx_r = 0.5 * (d3 - d2);
+    const double k2 = 13.0 / 3.0;
+    double el = L.eps + (ux_l * ux_l + k2 * uxx_l * uxx_l);
+    double ec = L.eps + (ux_c * ux_c + k2 * uxx_c * uxx_c);
+    double er = L.eps + (ux_r * ux_r + k2 * uxx_r * uxx_r);
+    double pl = el * el, pc = ec * ec, pr = er * er;
+    double al = L.w0 * (pc * pr), ac = L.w1 * (pl * pr), ar = L.w2 * (pl * pc);
+    double inv = ddiv<FAST>(1.0, al + ac + ar, f);
+    ux = (al * ux_l + ac * ux_c + ar * ux_r) * inv;
+    uxx = (al * uxx_l + ac * uxx_c + ar * uxx_r) * inv;
+}
+
+template <bool FAST>
+__device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double s3, double s4,
+                                        const Limiter& L, double& ux, double& uxx, Fault& f) {
+    if (HC_REASSOC)
+        weno3_1div<FAST>(s0, s1, s2, s3, s4, L, ux, uxx, f);
+    else
+        weno3<FAST>(s0, s1, s2, s3, s4, L, ux, uxx, f);
+}
+
 // Face states (extrapolate_to_face + 0.5 * tau, corrector.cpp:30-33) of one zone from its
 // mode-0 neighbourhood: reconstruction (reconstruct.cpp:16-28 MC, :42-61 WENO3) and the
 // ADER predictor (predictor.cpp:26-60). pc: the zone in the current smem plane (rows W*NV
 // apart); zm2..zp2: the zone's column in planes p-2..p+2.
-template <bool O3, bool FAST>
+template <bool O3, bool FAST, bool RK>
 __device__ __forceinline__ void zone_states(const double* pc, int row, const double* zm2,
                                             const double* zm1, const double* zp1,
                                             const double* zp2, const FusedArgs& a, double dt,
@@ -95,11 +136,11 @@ __device__ __forceinline__ void zone_states(const double* pc, int row, const dou
             face[5][q] = extrap<false>(u0, -1.0, sz, 0.0);
         } else {
             double ux, uxx, uy, uyy, uz, uzz;
-            weno3<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim, ux,
-                        uxx, f);
-            weno3<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q], a.lim,
-                        uy, uyy, f);
-            weno3<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, uz, uzz, f);
+            weno3_k<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
+                          ux, uxx, f);
+            weno3_k<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q],
+                          a.lim, uy, uyy, f);
+            weno3_k<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, uz, uzz, f);
             face[0][q] = extrap<true>(u0, +1.0, ux, uxx);
             face[1][q] = extrap<true>(u0, -1.0, ux, uxx);
             face[2][q] = extrap<true>(u0, +1.0, uy, uyy);
@@ -109,7 +150,13 @@ __device__ __forceinline__ void zone_states(const double* pc, int row, const dou
         }
     }
     double tau[NV];
-    predictor<O3, FAST>(face, dt, a.idx, a.idy, a.idz, a.gamma, tau, f);
+    if (RK) {  // Runge-Kutta stage: temporal mode zeroed (stepper.cpp:110-113)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) tau[q] = 0.0;
+    } else {
+        predictor<O3, FAST>(face, dt, a.idx, a.idy, a.idz, a.gamma, tau, f);
+    }
+    // + 0.5 * 0.0 is kept at RK stages: it turns -0.0 into +0.0 exactly as the reference
 #pragma unroll
     for (int s = 0; s < 6; ++s)
 #pragma unroll
@@ -130,14 +177,14 @@ struct Careful {
     Fault f;
 };
 
-template <bool O3>
+template <bool O3, bool RK>
 __device__ __noinline__ Careful zone_states_careful(const double* pc, int row, const double* zm2,
                                                     const double* zm1, const double* zp1,
                                                     const double* zp2, const FusedArgs& a,
                                                     double dt) {
     Careful c;
     c.f.clear();
-    zone_states<O3, false>(pc, row, zm2, zm1, zp1, zp2, a, dt, c.st.v, c.f);
+    zone_states<O3, false, RK>(pc, row, zm2, zm1, zp1, zp2, a, dt, c.st.v, c.f);
     return c;
 }
 
@@ -177,15 +224,20 @@ __device__ __forceinline__ void face_flux(const double* ul, const double* ur, do
     }
 }
 
-template <bool O3, int SOLVER, int TX, int TY, int MINB>
+// RK = false: one ADER step (predictor + U += dt*rate, stepper.cpp:49-78).
+// RK = true: one Runge-Kutta stage (temporal mode zero, U' = a*U0 + b*(U + dt*rate),
+// stepper.cpp:100-143); the CFL estimate is only taken when a.want_dt (last stage,
+// rk_step's compute_dt_next, stepper.cpp:155-156).
+template <bool O3, int SOLVER, int TX, int TY, int MINB, bool RK>
 __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     fused_ader_kernel(const FusedArgs a) {
     using S = FusedShape<O3, TX, TY>;
     constexpr int R = S::R, G = S::G, NB = S::NB, W = S::W, H = S::H;
     if (a.ctl->done) return;
-    const int cur = a.ctl->cur;
-    const double* __restrict__ uin = a.buf[cur];
-    double* __restrict__ uout = a.buf[cur ^ 1];
+    const int cur = a.ctl->cur;  // buffer holding the start-of-step state
+    const double* __restrict__ uin = a.buf[(cur + a.in_rel) % a.nbuf];
+    double* uout = a.buf[(cur + a.out_rel) % a.nbuf];  // may alias ustart (last RK stage)
+    const double* ustart = a.buf[cur];
 
     extern __shared__ double smem[];
     double* planes = smem;                          // [NB][H][W][5]
@@ -281,9 +333,9 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
             Fault f;
             f.clear();
-            zone_states<O3, true>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
+            zone_states<O3, true, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
             if (f.redo()) {
-                Careful c = zone_states_careful<O3>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
+                Careful c = zone_states_careful<O3, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
 #pragma unroll
                 for (int s = 0; s < 6; ++s)
 #pragma unroll
@@ -343,16 +395,22 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
         if (owned) {
             if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
                 const double* u = P(p - 1) + zoff_c * NV;
+                const size_t zi = size_t(p - 1 + a.gh) * plane_stride + size_t(ja + a.gh) * a.pitch +
+                                  size_t(ia + a.gh) * NV;
                 double un[NV];
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
                     double r = part[q] - cz * (fz_cur[q] - fz_prev[q]);
-                    un[q] = u[q] + r;
+                    if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
+                        un[q] = a.rk_a * ustart[zi + q] + a.rk_b * (u[q] + r);
+                    else
+                        un[q] = u[q] + r;
                 }
-                double* dst = uout + size_t(p - 1 + a.gh) * plane_stride +
-                              size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
+                double* dst = uout + zi;
 #pragma unroll
                 for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                if (RK && !a.want_dt) goto next_plane;
+                {
                 Fault f;
                 f.clear();
                 double d = eval_tstep<true>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
@@ -363,8 +421,10 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                     f.clear();
                     d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
                 }
-                if (f.code) record_fault(a.eb, ST_UPDATE, f, ia, ja, p - 1, 0);
+                if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
                 else dt_min = smin(dt_min, d);
+                }
+            next_plane:;
             }
             if (lp >= 0 && lp < nzc) {
                 const double* fxw = FX + (cj * (TX + 1) + ci) * NV;
@@ -383,6 +443,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     }
 
     // ---- block min -> one atomic per CTA (exact: min is order independent)
+    if (RK && !a.want_dt) return;
     dt_min = warp_min(dt_min);
     if ((tid & 31) == 0) red[tid >> 5] = dt_min;
     __syncthreads();

@@ -13,10 +13,10 @@
 namespace hc {
 namespace HC_FUSED_NS {
 
-template <bool O3, int SOLVER, int TX, int TY, int MINB>
+template <bool O3, int SOLVER, int TX, int TY, int MINB, bool RK>
 static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     using S = FusedShape<O3, TX, TY>;
-    auto kern = fused_ader_kernel<O3, SOLVER, TX, TY, MINB>;
+    auto kern = fused_ader_kernel<O3, SOLVER, TX, TY, MINB, RK>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
@@ -31,7 +31,7 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "fused_ader_kernel launch");
 }
 
-template <bool O3, int SOLVER>
+template <bool O3, int SOLVER, bool RK>
 static int launch_one(const FusedArgs& a, cudaStream_t st) {
     using T = FusedTile<O3>;
 #ifdef HC_TUNE
@@ -39,27 +39,32 @@ static int launch_one(const FusedArgs& a, cudaStream_t st) {
         const char* v = std::getenv("HC_FUSED_CFG");
         return v ? std::atoi(v) : 0;
     }();
-    if (O3 && SOLVER == 1) {
+    if (SOLVER == 1) {
         switch (cfg) {
-            case 1: return launch_cfg<O3, SOLVER, 16, 8, 3>(a, st);
-            case 2: return launch_cfg<O3, SOLVER, 16, 8, 1>(a, st);
-            case 3: return launch_cfg<O3, SOLVER, 24, 8, 1>(a, st);
-            case 4: return launch_cfg<O3, SOLVER, 16, 12, 2>(a, st);
-            case 5: return launch_cfg<O3, SOLVER, 32, 8, 1>(a, st);
-            case 6: return launch_cfg<O3, SOLVER, 24, 8, 2>(a, st);
+            case 1: return launch_cfg<O3, SOLVER, 16, 8, 2, RK>(a, st);
+            case 2: return launch_cfg<O3, SOLVER, 16, 12, 2, RK>(a, st);
+            case 3: return launch_cfg<O3, SOLVER, 24, 8, 2, RK>(a, st);
+            case 4: return launch_cfg<O3, SOLVER, 32, 16, 1, RK>(a, st);
+            case 5: return launch_cfg<O3, SOLVER, 16, 8, 3, RK>(a, st);
             default: break;
         }
     }
 #endif
-    return launch_cfg<O3, SOLVER, T::TX, T::TY, T::MINB>(a, st);
+    return launch_cfg<O3, SOLVER, T::TX, T::TY, T::MINB, RK>(a, st);
 }
 
 }  // namespace HC_FUSED_NS
 
-int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, cudaStream_t st) {
+int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st) {
     using namespace HC_FUSED_NS;
-    if (order == 2) return solver == 0 ? launch_one<false, 0>(a, st) : launch_one<false, 1>(a, st);
-    return solver == 0 ? launch_one<true, 0>(a, st) : launch_one<true, 1>(a, st);
+    if (rk) {
+        if (order == 2)
+            return solver == 0 ? launch_one<false, 0, true>(a, st) : launch_one<false, 1, true>(a, st);
+        return solver == 0 ? launch_one<true, 0, true>(a, st) : launch_one<true, 1, true>(a, st);
+    }
+    if (order == 2)
+        return solver == 0 ? launch_one<false, 0, false>(a, st) : launch_one<false, 1, false>(a, st);
+    return solver == 0 ? launch_one<true, 0, false>(a, st) : launch_one<true, 1, false>(a, st);
 }
 
 }  // namespace hc

@@ -19,7 +19,12 @@ struct StepCtl {
 };
 
 struct FusedArgs {
-    double* buf[2];  // ping-pong state buffers; ctl->cur selects the input
+    double* buf[3];  // state buffers; ctl->cur holds the start-of-step state
+    int nbuf;        // 2 (ADER, RK2) or 3 (SSP-RK3)
+    int in_rel;      // this launch reads buf[(cur + in_rel) % nbuf]
+    int out_rel;     // and writes buf[(cur + out_rel) % nbuf]
+    int want_dt;     // take the CFL estimate (ADER: always; RK: last stage)
+    double rk_a, rk_b;  // RK stage coefficients U' = a U0 + b (U + dt rate)
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width
     int my_pad;      // rows per plane in storage
@@ -35,14 +40,17 @@ struct FusedArgs {
 };
 
 // Tile shape per order (columns x rows of owned zones per CTA).
+// Tile shape per order (columns x rows of owned zones per CTA), from the r1 sweep on a B200
+// (profiles/r1_tile_sweep.txt): O3 16x12 with 2 CTAs/SM (256 threads, 128 registers,
+// 16 warps/SM) beats 16x8 (12 warps, 168 registers) by 6 %; O2 keeps 16x8.
 template <bool O3>
 struct FusedTile {
     static constexpr int TX = 16;
-    static constexpr int TY = 8;
+    static constexpr int TY = O3 ? 12 : 8;
     static constexpr int MINB = 2;  // resident CTAs per SM the registers must allow
 };
 
-int launch_fused_exact(const FusedArgs& a, int order, int solver, cudaStream_t st);
-int launch_fused_fast(const FusedArgs& a, int order, int solver, cudaStream_t st);
+int launch_fused_exact(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st);
+int launch_fused_fast(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st);
 
 }  // namespace hc

@@ -49,10 +49,14 @@ __device__ __forceinline__ void ghost_copy(double* u, const SG& g, int bx, int b
 // blockIdx.y = plane k_lo + y. ring_mode: the planes are active, fill their x/y ghost ring
 // (2*gh full rows + 2*gh columns of the ny active rows); otherwise they are z-ghost planes,
 // fill every zone.
-__global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g, int bx, int by,
-                                 int bz, int k_lo, int ring_mode) {
+struct Bufs {
+    double* b[3];
+};
+
+__global__ void k_stepper_ghosts(Bufs bufs, int nbuf, int rel, const StepCtl* c, SG g, int bx,
+                                 int by, int bz, int k_lo, int ring_mode) {
     if (c->done) return;
-    double* u = c->cur ? b1 : b0;
+    double* u = bufs.b[(c->cur + rel) % nbuf];
     const int k = k_lo + blockIdx.y;
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     int i, j;
@@ -77,7 +81,7 @@ __global__ void k_stepper_ghosts(double* b0, double* b1, const StepCtl* c, SG g,
     ghost_copy(u, g, bx, by, bz, i, j, k);
 }
 
-__global__ void k_advance(StepCtl* c, const ErrBlock* eb) {
+__global__ void k_advance(StepCtl* c, const ErrBlock* eb, int flip) {
     if (c->done) return;
     for (int s = 0; s < ST_COUNT; ++s)
         if (eb->rec[s].flag) {  // the reference would have thrown out of this step
@@ -95,7 +99,7 @@ __global__ void k_advance(StepCtl* c, const ErrBlock* eb) {
         else if (dn >= rem) dn = rem;
     }
     c->dt = dn;
-    c->cur ^= 1;  // the fused kernel wrote the other buffer
+    if (flip) c->cur ^= 1;  // ADER wrote the other buffer; RK stages end in buffer cur
 }
 
 }  // namespace
@@ -108,7 +112,9 @@ struct hc_stepper {
     hc_params p;
     hc_stepper_opts o;
     SG sg;
-    double* buf[2] = {nullptr, nullptr};
+    double* buf[3] = {nullptr, nullptr, nullptr};
+    int nbuf = 2;
+    int stage = 0;  // next RK stage (host side; 0 for ADER)
     int cur = 0;
     StepCtl* ctl = nullptr;
     ErrBlock* eb = nullptr;
@@ -134,6 +140,13 @@ FusedArgs fused_args(const hc_stepper* s) {
     FusedArgs a;
     a.buf[0] = s->buf[0];
     a.buf[1] = s->buf[1];
+    a.buf[2] = s->buf[2];
+    a.nbuf = s->nbuf;
+    a.in_rel = 0;
+    a.out_rel = 1;
+    a.want_dt = 1;
+    a.rk_a = 0.0;
+    a.rk_b = 1.0;
     a.nx = s->g.nx;
     a.ny = s->g.ny;
     a.nz = s->g.nz;
@@ -189,6 +202,10 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         set_error(HC_INVALID, "unknown riemann solver");
         return HC_INVALID;
     }
+    if (o->integrator != 0 && o->integrator != 2 && o->integrator != 3) {
+        set_error(HC_INVALID, "integrator must be 0 (ADER), 2 (RK2) or 3 (SSP-RK3)");
+        return HC_INVALID;
+    }
     for (int a = 0; a < 3; ++a)
         if (o->bc[a] < -1 || o->bc[a] > 1 || (a < 2 && o->bc[a] < 0)) {
             set_error(HC_INVALID, "bad boundary kind (x/y must be periodic or outflow)");
@@ -224,7 +241,9 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     // row / plane (those zones are masked), and the last plane's overhang lands in the slack.
     sg.my_pad = sg.my;
     sg.pitch = sg.mx * NV;
-    const size_t slack = size_t(TY + 2 * G + 2) * sg.pitch + size_t(TX + 2 * G) * NV;
+    // slack sized for the largest tile any (tuning) build instantiates: 32 x 16
+    const size_t slack = size_t(std::max(TY, 16) + 2 * G + 2) * sg.pitch +
+                         size_t(std::max(TX, 32) + 2 * G) * NV;
     (void)TX;
     s->tz = std::max(4, std::min(32, g->nz));
     if ((rc = set_dev(s))) {
@@ -234,6 +253,8 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     s->bytes = (size_t(sg.mz) * sg.my_pad * sg.pitch + slack) * sizeof(double);
     cudaError_t e = cudaMalloc(&s->buf[0], s->bytes);
     if (e == cudaSuccess) e = cudaMalloc(&s->buf[1], s->bytes);
+    s->nbuf = o->integrator == 3 ? 3 : 2;
+    if (e == cudaSuccess && s->nbuf == 3) e = cudaMalloc(&s->buf[2], s->bytes);
     if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(StepCtl));
     if (e == cudaSuccess) e = cudaMalloc(&s->eb, sizeof(ErrBlock));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking);
@@ -265,6 +286,7 @@ int hc_stepper_destroy(hc_stepper* s) {
     if (s->st) cudaStreamSynchronize(s->st);
     cudaFree(s->buf[0]);
     cudaFree(s->buf[1]);
+    cudaFree(s->buf[2]);
     cudaFree(s->ctl);
     cudaFree(s->eb);
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
@@ -331,6 +353,8 @@ int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t
 
 // Ghost fill of storage planes [k_lo, k_hi): active planes get their x/y ring, z-ghost
 // planes (when this stepper owns the z boundary) are filled whole.
+static int stage_in_rel(const hc_stepper* s) { return s->o.integrator == 0 ? 0 : s->stage; }
+
 static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
     const SG& g = s->sg;
     k_lo = std::max(k_lo, 0);
@@ -341,8 +365,9 @@ static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
     auto launch = [&](int lo, int hi, int ring_mode) {
         if (hi <= lo) return;
         dim3 grid(((ring_mode ? ring : plane) + 255) / 256, unsigned(hi - lo));
-        k_stepper_ghosts<<<grid, 256, 0, st>>>(s->buf[0], s->buf[1], s->ctl, g, s->o.bc[0],
-                                               s->o.bc[1], s->o.bc[2], lo, ring_mode);
+        Bufs b{{s->buf[0], s->buf[1], s->buf[2]}};
+        k_stepper_ghosts<<<grid, 256, 0, st>>>(b, s->nbuf, stage_in_rel(s), s->ctl, g,
+                                               s->o.bc[0], s->o.bc[1], s->o.bc[2], lo, ring_mode);
         s->launches++;
     };
     launch(a_lo, a_hi, 1);
@@ -360,32 +385,58 @@ int hc_stepper_fill_ghosts(hc_stepper* s) {
     return fill_planes(s, 0, s->sg.mz, s->st);
 }
 
+// Shu-Osher stage coefficients U' = a U0 + b (U + K(U)) (stepper.cpp:80-86)
+static const double kHeun[2][2] = {{0.0, 1.0}, {0.5, 0.5}};
+static const double kSsp3[3][2] = {{0.0, 1.0}, {0.75, 0.25}, {1.0 / 3.0, 2.0 / 3.0}};
+
+int hc_stepper_stages(hc_stepper* s) { return s->o.integrator == 0 ? 1 : s->o.integrator; }
+
+// One fused launch: the ADER step, or the next Runge-Kutta stage.
 int hc_stepper_compute(hc_stepper* s) {
     int rc = set_dev(s);
     if (rc) return rc;
     FusedArgs a = fused_args(s);
     a.cfl = s->cfl;
-    rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, s->st)
-                    : launch_fused_fast(a, s->p.order, s->p.solver, s->st);
+    const bool rk = s->o.integrator != 0;
+    if (rk) {
+        const int ns = s->o.integrator, k = s->stage;
+        const double* ab = ns == 2 ? kHeun[k] : kSsp3[k];
+        a.in_rel = k;                      // stage k reads the previous stage's result
+        a.out_rel = (k + 1) % s->nbuf;     // the last stage lands in buffer cur (in place on U0)
+        if (k == ns - 1) a.out_rel = 0;
+        a.rk_a = ab[0];
+        a.rk_b = ab[1];
+        a.want_dt = k == ns - 1;
+    }
+    rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st)
+                    : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st);
     if (rc) return rc;
     s->launches++;
-    s->cur = 1 - s->cur;  // host-side guess; the device's ctl->cur is authoritative
+    if (rk)
+        s->stage = (s->stage + 1) % s->o.integrator;
+    else
+        s->cur = 1 - s->cur;  // host-side guess; the device's ctl->cur is authoritative
     return HC_OK;
 }
 
 int hc_stepper_advance(hc_stepper* s) {
     int rc = set_dev(s);
     if (rc) return rc;
-    k_advance<<<1, 1, 0, s->st>>>(s->ctl, s->eb);
+    k_advance<<<1, 1, 0, s->st>>>(s->ctl, s->eb, s->o.integrator == 0 ? 1 : 0);
     s->launches++;
+    s->stage = 0;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_advance");
 }
 
 int hc_stepper_step(hc_stepper* s, int n) {
+    const int ns = hc_stepper_stages(s);
     for (int i = 0; i < n; ++i) {
-        int rc = hc_stepper_fill_ghosts(s);
-        if (!rc) rc = hc_stepper_compute(s);
+        int rc = HC_OK;
+        for (int k = 0; k < ns && !rc; ++k) {
+            rc = hc_stepper_fill_ghosts(s);  // rk_step: apply_boundary before every stage
+            if (!rc) rc = hc_stepper_compute(s);
+        }
         if (!rc) rc = hc_stepper_advance(s);
         if (rc) return rc;
     }
@@ -416,6 +467,11 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
     if (s->o.bc[2] < 0) {
         set_error(HC_INVALID, "hc_stepper_step_host needs a z boundary owned by the stepper");
         return HC_INVALID;
+    }
+    if (s->o.integrator != 0) {  // multi-stage: whole-state transfers around the stages
+        if ((rc = hc_stepper_upload(s, host_in))) return rc;
+        if ((rc = hc_stepper_step(s, 1))) return rc;
+        return hc_stepper_download(s, host_out);
     }
     const SG& g = s->sg;
     const int G = s->p.order == 3 ? 3 : 2;
@@ -458,8 +514,8 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
         a.cfl = s->cfl;
         a.kz_first = c0;
         a.kz_last = c1;
-        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, s->st)
-                        : launch_fused_fast(a, s->p.order, s->p.solver, s->st);
+        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, false, s->st)
+                        : launch_fused_fast(a, s->p.order, s->p.solver, false, s->st);
         if (rc) return rc;
         s->launches++;
         HC_CUDA(cudaEventRecord(ev_comp[c], s->st));
@@ -492,7 +548,7 @@ int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {
     int rc = set_dev(s);
     if (!rc) rc = refresh_cur(s);
     if (rc) return rc;
-    if (dptr) *dptr = s->buf[s->cur];
+    if (dptr) *dptr = s->buf[(s->cur + stage_in_rel(s)) % s->nbuf];
     if (row_pitch_doubles) *row_pitch_doubles = size_t(s->sg.pitch);
     return HC_OK;
 }

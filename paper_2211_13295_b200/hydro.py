@@ -68,7 +68,11 @@ class Params(C.Structure):
 
 
 class StepperOpts(C.Structure):
-    _fields_ = [("bc", C.c_int * 3), ("exact", C.c_int), ("device", C.c_int)]
+    _fields_ = [("bc", C.c_int * 3), ("exact", C.c_int), ("device", C.c_int),
+                ("integrator", C.c_int)]
+
+
+ADER, RK2, RK3 = 0, 2, 3  # IntegratorChoice (predictor.hpp:11)
 
 
 def ghost_for_order(order: int) -> int:
@@ -155,7 +159,7 @@ def load_library(path: str = LIB_PATH):
     lib.hc_stepper_launches.restype = C.c_long
     lib.hc_stepper_launches.argtypes = [C.c_void_p]
     for name in ("hc_stepper_destroy", "hc_stepper_step", "hc_stepper_fill_ghosts",
-                 "hc_stepper_compute", "hc_stepper_advance"):
+                 "hc_stepper_compute", "hc_stepper_advance", "hc_stepper_stages"):
         getattr(lib, name).argtypes = [C.c_void_p] + ([C.c_int] if name.endswith("_step")
                                                        else [])
     _LIB = lib
@@ -300,13 +304,13 @@ class Stepper:
     exact: True = bit-exact build (the reference's bits); False = FMA-contracted build."""
 
     def __init__(self, geom: Geom, params: Params, bc=(PERIODIC, PERIODIC, PERIODIC),
-                 exact=True, device=0):
+                 exact=True, device=0, integrator=ADER):
         self.lib = load_library()
         self.geom, self.params = geom, params
         o = StepperOpts()
         o.bc[0], o.bc[1] = bc[0], bc[1]
         o.bc[2] = -1 if bc[2] is None else bc[2]
-        o.exact, o.device = int(bool(exact)), device
+        o.exact, o.device, o.integrator = int(bool(exact)), device, integrator
         h = C.c_void_p()
         _check(self.lib.hc_stepper_create(C.byref(geom), C.byref(params), C.byref(o),
                                           C.byref(h)))
@@ -350,6 +354,10 @@ class Stepper:
         host_out = host_in if host_out is None else host_out
         _check(self.lib.hc_stepper_step_host(self.h, _p(host_in), _p(host_out), int(chunks)))
         return host_out
+
+    @property
+    def stages(self) -> int:
+        return self.lib.hc_stepper_stages(self.h)
 
     def fill_ghosts(self):
         _check(self.lib.hc_stepper_fill_ghosts(self.h))

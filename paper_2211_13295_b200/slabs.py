@@ -100,7 +100,7 @@ class SlabDomain:
     """One rank's slab of an ``nx x ny x nz_global`` mesh on [-5,5]^2 x [-5, -5 + nz*dz]."""
 
     def __init__(self, nx, ny, nz_global, order, rank=0, world=1, device=0, exact=True,
-                 solver=hydro.HLL, bc=PERIODIC, dx=None):
+                 solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER):
         self.rank, self.world, self.order = rank, world, order
         self.periodic = bc == PERIODIC
         self.z0, self.z1 = slab_range(nz_global, rank, world)
@@ -116,7 +116,7 @@ class SlabDomain:
         self.params = hydro.make_params(order, solver)
         self.api = hydro.HostApi()
         self.st = hydro.Stepper(g, self.params, bc=(bc, bc, bc if world == 1 else None),
-                                exact=exact, device=device)
+                                exact=exact, device=device, integrator=integrator)
         # every device op of the step (our kernels, NCCL, events) is ordered on one stream
         import torch
         self.stream = torch.cuda.Stream(device=device)
@@ -190,13 +190,14 @@ class SlabDomain:
             self.st.step(1)
             return
         with torch.cuda.stream(s):
-            self.st.fill_ghosts()
-            if self.world > 1:
-                exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank,
-                                 self.world, self.periodic)
-            if kernel_events is not None:
-                kernel_events[0].record(s)
-            self.st.compute()
+            for k in range(self.st.stages):  # 1 (ADER) or 2/3 RK stages
+                self.st.fill_ghosts()
+                if self.world > 1:
+                    exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank,
+                                     self.world, self.periodic)
+                if kernel_events is not None and k == 0:
+                    kernel_events[0].record(s)
+                self.st.compute()
             if kernel_events is not None:
                 kernel_events[1].record(s)
             if self.world > 1:

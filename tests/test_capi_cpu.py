@@ -17,12 +17,27 @@ def test_library_exports_every_declared_symbol():
     assert lib.hc_abi_version() == 1
 
 
-def test_struct_layouts_match_the_header():
-    # hc_geom: 4 ints + 3 doubles + 3 doubles
-    assert C.sizeof(hydro.Geom) == 4 * 4 + 6 * 8
-    assert C.sizeof(hydro.Limiter) == 6 * 8
-    assert C.sizeof(hydro.Params) == 4 + 4 + 8 + 48
-    assert C.sizeof(hydro.StepperOpts) == 5 * 4
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors against the C compiler's view of include/hydro_cuda.h."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "sizes.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "hydro_cuda.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(hc_geom),"
+        " sizeof(hc_limiter), sizeof(hc_params), sizeof(hc_stepper_opts),"
+        " offsetof(hc_geom, dx), offsetof(hc_params, lim), offsetof(hc_stepper_opts,"
+        " integrator)); return 0;}\n")
+    exe = tmp_path / "sizes"
+    subprocess.run(["/usr/bin/gcc", "-I" + os.path.join(root, "include"), str(src), "-o",
+                    str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [C.sizeof(hydro.Geom), C.sizeof(hydro.Limiter), C.sizeof(hydro.Params),
+            C.sizeof(hydro.StepperOpts), hydro.Geom.dx.offset, hydro.Params.lim.offset,
+            hydro.StepperOpts.integrator.offset]
+    assert got == want
 
 
 def test_invalid_geometry_is_rejected_before_any_device_work():

@@ -175,6 +175,38 @@ def test_fused_stepper_bitwise(api, orc, order, solver, bc, n, problem, steps):
     assert st.launches >= 3 * steps  # ghost fill (1-3 launches) + fused + advance per step
 
 
+@pytest.mark.parametrize("order,nst,bc,n", [(2, 2, hydro.PERIODIC, (18, 14, 11)),
+                                            (3, 3, hydro.PERIODIC, (16, 12, 9)),
+                                            (3, 2, hydro.OUTFLOW, (17, 9, 8)),
+                                            (2, 3, hydro.PERIODIC, (24, 24, 24))])
+def test_fused_rk_stepper_bitwise(api, orc, order, nst, bc, n):
+    """Heun / SSP-RK3 on the fused stepper (one launch per stage, temporal mode zero) vs
+    the oracle's rk_step (stepper.cpp:145-157), several steps."""
+    g, go = geoms(n, order)
+    cfl = 0.6 if order == 2 else 0.4
+    s0 = api.init_isentropic_vortex(g, order)
+    s = s0.copy()
+    par = po.make_params(order)
+    dt = orc.initial_dt(go, s, cfl)
+    dts = [dt]
+    bufs = [po.zeros_modal(go, order), *po.zeros_faces(go), po.zeros_rate(go),
+            po.zeros_skinny(go)]
+    for _ in range(3):
+        dt = orc.rk_step(go, par, nst, bufs[0], s, *bufs[1:], bc, dt, cfl)
+        dts.append(dt)
+    st = hydro.Stepper(g, hydro.make_params(order), bc=(bc, bc, bc), integrator=nst)
+    assert st.stages == nst
+    st.upload(s0)
+    st.set_time(0.0, dts[0], cfl)
+    st.step(3)
+    t, dt_next, done = st.sync()
+    out = st.download()
+    gh = g.ghost
+    act = np.s_[gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx]
+    assert done == 3 and dt_next == dts[-1]
+    assert same(out[act], s[act])
+
+
 @pytest.mark.parametrize("order,bc,chunks", [(3, hydro.PERIODIC, 5), (2, hydro.OUTFLOW, 3),
                                              (3, hydro.PERIODIC, 1)])
 def test_pipelined_host_step_equals_device_step(api, order, bc, chunks):

@@ -277,25 +277,30 @@ def main():
 
     # end to end through the public API with HOST buffers: H2D of the step's input from
     # pinned memory, the step, D2H of the result and of dt_next -- the paper's skinny trick
-    e2e = None
-    if world == 1:
-        host = torch.empty(dom.host_shape(), dtype=torch.float64, pin_memory=True).numpy()
-        host[...] = s0
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
+    host = torch.empty(dom.host_shape(), dtype=torch.float64, pin_memory=True).numpy()
+    host[...] = s0
+    torch.cuda.synchronize()
+    dom.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        if world == 1:  # H2D / fused step / D2H pipelined by z-chunks
             dom.st.step_host(host, host, args.e2e_chunks)
-            dom.sync()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1)
-        nbytes = host.nbytes
-        e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 16,
-               "steps": args.e2e_steps, "chunks": args.e2e_chunks,
-               "api": "hc_stepper_step_host (H2D of U_skinny, fused step, D2H, pipelined by "
-                      "z-chunks) + hc_stepper_sync (dt_next)"}
+        else:  # slab: upload, step with the NCCL halo exchange, download
+            dom.upload(host)
+            dom.step()
+            dom.download(host)
+        dom.sync()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = dom.max_over_ranks(e0.elapsed_time(e1))
+    nbytes = host.nbytes
+    e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": (nbytes + 16) * world,
+           "steps": args.e2e_steps,
+           "api": ("hc_stepper_step_host (H2D of U_skinny, fused step, D2H, pipelined in "
+                   f"{args.e2e_chunks} z-chunks) + hc_stepper_sync (dt_next)") if world == 1 else
+                  "per rank: hc_stepper_upload + slab step (NCCL halos) + hc_stepper_download"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

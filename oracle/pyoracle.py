@@ -299,5 +299,20 @@ class Reference(CpuLib):
         return zps, fin, t_end.value, l1.value
 
 
+def ref_run_simulation(ref, problem, order, integrator, solver, n, steps=0, t_final=-1.0,
+                       threads=0):
+    """harness.cpp run_simulation through the reference library: (l1, linf, t_end, steps)."""
+    l1, linf = np.zeros(5), np.zeros(5)
+    t_end, nst = C.c_double(), C.c_long()
+    nx, ny, nz = (n, n, n) if isinstance(n, int) else n
+    f = ref.lib.ref_run_simulation
+    f.argtypes = [C.c_int] * 7 + [C.c_long, C.c_double, C.c_int] + [C.c_void_p] * 5
+    rc = f(problem, order, integrator, solver, nx, ny, nz, steps, t_final, threads,
+           l1.ctypes.data, linf.ctypes.data, C.addressof(t_end), C.addressof(nst), None)
+    if rc:
+        raise RuntimeError(ref.error())
+    return l1, linf, t_end.value, nst.value
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_SO)

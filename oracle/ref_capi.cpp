@@ -319,4 +319,35 @@ double ref_run_benchmark(int problem, int order, int integrator, int solver, int
     return rc == OR_OK ? zps : -1.0;
 }
 
+// harness.cpp:116-193 run_simulation with either a step count or a t_final (<= 0: the
+// problem's default stop time); returns the error norms vs the exact solution when the
+// problem has one (l1/linf of 5 variables), the end time and the number of steps.
+int ref_run_simulation(int problem, int order, int integrator, int solver, int nx, int ny,
+                       int nz, long steps, double t_final, int threads, double* l1,
+                       double* linf, double* t_end, long* steps_done, double* final_skinny) {
+    RunConfig cfg;
+    cfg.problem = problem == 0 ? Problem::vortex : (problem == 1 ? Problem::sod : Problem::constant);
+    cfg.order = order;
+    cfg.integrator = integrator == 0 ? IntegratorChoice::ader_onestep
+                                     : (integrator == 2 ? IntegratorChoice::rk2 : IntegratorChoice::rk3);
+    cfg.solver = solver == OR_RUSANOV ? SolverChoice::rusanov : SolverChoice::hll;
+    cfg.nx = nx;
+    cfg.ny = ny;
+    cfg.nz = nz;
+    cfg.steps = steps;
+    cfg.t_final = t_final;
+    cfg.threads = threads;
+    return guarded([&] {
+        RunResult r = run_simulation(cfg);
+        if (r.errors)
+            for (int q = 0; q < NVAR; ++q) {
+                l1[q] = r.errors->l1[q];
+                linf[q] = r.errors->linf[q];
+            }
+        *t_end = r.t_end;
+        *steps_done = long(r.steps);
+        if (final_skinny) out(r.final_state.v, final_skinny);
+    });
+}
+
 }  // extern "C"

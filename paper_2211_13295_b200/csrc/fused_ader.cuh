@@ -51,9 +51,10 @@ template <bool O3, int TX, int TY>
 struct FusedShape {
     static constexpr int R = O3 ? 2 : 1;   // reconstruction stencil radius
     static constexpr int G = R + 1;        // halo: one ring + stencil
-    // plane ring, refilled after barrier B: O3 reuses the slot of plane p-2 (5 slots); O2
-    // still finalises p-1 after B, so the refill goes to p-2's slot of a 4-slot ring
+    // plane ring: O3 refills the slot of plane p-2 after the predict phase (5 slots); O2's
+    // oldest plane (p-1) is read until the end of the iteration, so it keeps a spare slot
     static constexpr int NB = O3 ? 2 * R + 1 : 2 * R + 2;
+    static constexpr bool LATE_LOAD = O3;
     static constexpr int W = TX + 2 * G;
     static constexpr int H = TY + 2 * G;
     static constexpr int PLANE = W * H * NV;  // doubles per smem plane
@@ -63,11 +64,9 @@ struct FusedShape {
     static constexpr int YP_N = (TY + 1) * TX;  // +y states, rows -1..TY-1
     static constexpr int FX_N = TY * (TX + 1);  // x faces 0..TX
     static constexpr int FY_N = (TY + 1) * TX;  // y faces 0..TY
-    // x (y) fluxes overwrite the +x (+y) states in place: each face's thread reads its
-    // neighbour's state and then writes that face's flux to the same slot; both arrays are
-    // double-buffered by plane parity. XY_N = doubles per buffer (the larger of the two).
-    static constexpr int XY_N = NV * (XP_N > YP_N ? XP_N : YP_N);
-    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + 4 * XY_N + 32);
+    // FX aliases XP and FY aliases YP: each face's thread reads its +x/+y neighbour state and
+    // then writes that face's flux to the same slot (no other reader in between)
+    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32);
 };
 
 #ifndef HC_REASSOC
@@ -242,9 +241,11 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
 
     extern __shared__ double smem[];
     double* planes = smem;                          // [NB][H][W][5]
-    double* XP = planes + size_t(NB) * S::PLANE;    // [2][TY][TX+1][5] (+x states, x fluxes)
-    double* YP = XP + 2 * S::XY_N;                  // [2][TY+1][TX][5]
-    double* red = YP + 2 * S::XY_N;                 // [32]
+    double* XP = planes + size_t(NB) * S::PLANE;    // [TY][TX+1][5]
+    double* YP = XP + S::XP_N * NV;                 // [TY+1][TX][5]
+    double* FX = XP;                                // [TY][TX+1][5], aliases XP
+    double* FY = YP;                                // [TY+1][TX][5], aliases YP
+    double* red = YP + S::YP_N * NV;                // [32]
 
     const int tid = threadIdx.x;
     // ---- E-column of this thread
@@ -314,28 +315,12 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     double dt_min = 1.0e32;
     const int zoff_c = (cj + G) * W + (ci + G);  // zone index of this column in a smem plane
 
-    // Two barriers per plane. Iteration p:
-    //   [A] rate x/y part of plane p-1 (fluxes of plane p-1 from shared memory) and the
-    //       predictor of plane p (publishes +x/+y states to XP/YP[p & 1])
-    //   [B] refill the ring slot of plane p-R; faces of plane p; with the bottom z face of p
-    //       (= top face of p-1) in hand, plane p-1 is finalised right away.
-    // XP/YP are double-buffered by plane parity so the rate reads of plane p-1 and the
-    // predictor writes of plane p can share the phase between A and B.
     for (int lp = -1; lp <= nzc; ++lp) {
         const int p = kz0 + lp;
-        double* XPc = XP + (lp & 1) * S::XY_N;          // this plane's +x states / x fluxes
-        double* YPc = YP + (lp & 1) * S::XY_N;
-        const double* FXp = XP + ((lp - 1) & 1) * S::XY_N;  // previous plane's fluxes
-        const double* FYp = YP + ((lp - 1) & 1) * S::XY_N;
         cp_async_wait_all();
-        __syncthreads();  // ---------------------------------------------------------- A
-        if (owned && lp >= 1 && lp - 1 < nzc) {  // x/y part of the rate of plane p-1
-            const double* fxw = FXp + (cj * (TX + 1) + ci) * NV;
-            const double* fys = FYp + (cj * TX + ci) * NV;
-#pragma unroll
-            for (int q = 0; q < NV; ++q)
-                part[q] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
-        }
+        __syncthreads();
+        if (!S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
+
         const bool zring = (lp == -1 || lp == nzc);
         const bool do_zone = zring ? owned : exists;
         // ------------------------------------------------------------- predict
@@ -360,53 +345,58 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             if (!zring) {
                 if (ci <= TX - 1 && cj >= 0 && cj < TY)
 #pragma unroll
-                    for (int q = 0; q < NV; ++q)
-                        XPc[(cj * (TX + 1) + ci + 1) * NV + q] = st[0][q];
+                    for (int q = 0; q < NV; ++q) XP[(cj * (TX + 1) + ci + 1) * NV + q] = st[0][q];
                 if (cj <= TY - 1 && ci >= 0 && ci < TX)
 #pragma unroll
-                    for (int q = 0; q < NV; ++q) YPc[((cj + 1) * TX + ci) * NV + q] = st[2][q];
+                    for (int q = 0; q < NV; ++q) YP[((cj + 1) * TX + ci) * NV + q] = st[2][q];
             }
         }
-        __syncthreads();  // ---------------------------------------------------------- B
-        // plane p-R is no longer read (predictor of p, finalise of p-2): refill with p+R+1
-        if (lp <= nzc - 1) load_plane(p + R + 1);
+        __syncthreads();
+        // plane p-R is no longer read this iteration: refill its slot with p+R+1
+        if (S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
         // ---------------------------------------------------------------- flux
+        double fz_cur[NV];
         if (do_zone) {
             if (!zring && xface) {  // x face at the west of this column
-                double ul[NV], f5[NV];
+                {
+                    double ul[NV], f5[NV];
 #pragma unroll
-                for (int q = 0; q < NV; ++q) ul[q] = XPc[(cj * (TX + 1) + ci) * NV + q];
-                Fault f;
-                f.clear();
-                face_flux<SOLVER, 0>(ul, st[1], a.gamma, f5, f);
-                if (f.code) record_fault(a.eb, ST_FLUX, f, ia, ja, p, 0);
+                    for (int q = 0; q < NV; ++q) ul[q] = XP[(cj * (TX + 1) + ci) * NV + q];
+                    Fault f;
+                    f.clear();
+                    face_flux<SOLVER, 0>(ul, st[1], a.gamma, f5, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, ia, ja, p, 0);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) XPc[(cj * (TX + 1) + ci) * NV + q] = f5[q];
+                    for (int q = 0; q < NV; ++q) FX[(cj * (TX + 1) + ci) * NV + q] = f5[q];
+                }
             }
             if (!zring && yface) {  // y face at the south of this column
-                double ul[NV], f5[NV];
+                {
+                    double ul[NV], f5[NV];
 #pragma unroll
-                for (int q = 0; q < NV; ++q) ul[q] = YPc[(cj * TX + ci) * NV + q];
-                Fault f;
-                f.clear();
-                face_flux<SOLVER, 1>(ul, st[3], a.gamma, f5, f);
-                if (f.code) record_fault(a.eb, ST_FLUX, f, ja, ia, p, 1);
+                    for (int q = 0; q < NV; ++q) ul[q] = YP[(cj * TX + ci) * NV + q];
+                    Fault f;
+                    f.clear();
+                    face_flux<SOLVER, 1>(ul, st[3], a.gamma, f5, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, ja, ia, p, 1);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) YPc[(cj * TX + ci) * NV + q] = f5[q];
+                    for (int q = 0; q < NV; ++q) FY[(cj * TX + ci) * NV + q] = f5[q];
+                }
             }
-        }
-        if (owned) {
-            double fz_cur[NV];
-            if (lp >= 0) {  // z face at the bottom of plane p
+            if (owned && lp >= 0) {  // z face at the bottom of plane p
                 Fault f;
                 f.clear();
                 face_flux<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
                 if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
             }
-            if (lp >= 1) {  // finalise plane p-1: its top face flux is fz_cur
+        }
+        __syncthreads();
+        // ---------------------------------------------------------------- rate
+        if (owned) {
+            if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
                 const double* u = P(p - 1) + zoff_c * NV;
-                const size_t zi = size_t(p - 1 + a.gh) * plane_stride +
-                                  size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
+                const size_t zi = size_t(p - 1 + a.gh) * plane_stride + size_t(ja + a.gh) * a.pitch +
+                                  size_t(ia + a.gh) * NV;
                 double un[NV];
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
@@ -419,20 +409,29 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 double* dst = uout + zi;
 #pragma unroll
                 for (int q = 0; q < NV; ++q) dst[q] = un[q];
-                if (!RK || a.want_dt) {
-                    Fault f;
-                    f.clear();
-                    double d = eval_tstep<true>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
-                    if (f.redo()) {
-                        V5 u5;
+                if (RK && !a.want_dt) goto next_plane;
+                {
+                Fault f;
+                f.clear();
+                double d = eval_tstep<true>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                if (f.redo()) {
+                    V5 u5;
 #pragma unroll
-                        for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
-                        f.clear();
-                        d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
-                    }
-                    if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
-                    else dt_min = smin(dt_min, d);
+                    for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
+                    f.clear();
+                    d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
                 }
+                if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
+                else dt_min = smin(dt_min, d);
+                }
+            next_plane:;
+            }
+            if (lp >= 0 && lp < nzc) {
+                const double* fxw = FX + (cj * (TX + 1) + ci) * NV;
+                const double* fys = FY + (cj * TX + ci) * NV;
+#pragma unroll
+                for (int q = 0; q < NV; ++q)
+                    part[q] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
             }
             if (lp >= 0) {
 #pragma unroll

@@ -36,15 +36,48 @@
 namespace hc {
 namespace HC_FUSED_NS {
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+// ---- plane loads: one bulk copy (TMA engine, cp.async.bulk) per smem row, completion
+// tracked by one mbarrier per ring slot (expect_tx = bytes of the plane)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem)
+                 : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    asm volatile("cp.async.commit_group;\ncp.async.wait_all;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 template <bool O3, int TX, int TY>
@@ -72,6 +105,9 @@ struct FusedShape {
 #ifndef HC_REASSOC
 #define HC_REASSOC 0
 #endif
+// evaluation mode of the hot path (pointwise.cuh): 1 = bit-exact branch-free, 2 = FMA build
+// with the approximate division
+constexpr int FM = HC_REASSOC ? 2 : 1;
 
 // WENO3 point (reconstruct.hpp:46-73) for the FMA build: the normalised weights
 // (w_k / P_k) / sum_j (w_j / P_j) with P_k = (eps + IS_k)^2 are evaluated as
@@ -79,7 +115,7 @@ struct FusedShape {
 // Same mathematics, different rounding (<= a few ulp per weight); used only when the
 // translation unit opts out of bit-exactness (fused_fast.cu). P_k lies in [eps^2, ~1e12]
 // for physical states, so the triple products stay far from over/underflow.
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ void weno3_1div(double s0, double s1, double s2, double s3,
                                            double s4, const Limiter& L, double& ux, double& uxx,
                                            Fault& f) {
@@ -101,7 +137,7 @@ __device__ __forceinline__ void weno3_1div(double s0, double s1, double s2, doub
     uxx = (al * uxx_l + ac * uxx_c + ar * uxx_r) * inv;
 }
 
-template <bool FAST>
+template <int FAST>
 __device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double s3, double s4,
                                         const Limiter& L, double& ux, double& uxx, Fault& f) {
     if (HC_REASSOC)
@@ -114,7 +150,7 @@ __device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double 
 // mode-0 neighbourhood: reconstruction (reconstruct.cpp:16-28 MC, :42-61 WENO3) and the
 // ADER predictor (predictor.cpp:26-60). pc: the zone in the current smem plane (rows W*NV
 // apart); zm2..zp2: the zone's column in planes p-2..p+2.
-template <bool O3, bool FAST, bool RK>
+template <bool O3, int FAST, bool RK>
 __device__ __forceinline__ void zone_states(const double* pc, int row, const double* zm2,
                                             const double* zm1, const double* zp1,
                                             const double* zp2, const FusedArgs& a, double dt,
@@ -209,7 +245,7 @@ __device__ __noinline__ double eval_tstep_careful(V5 u, double cfl, double dx, d
 template <int SOLVER, int A>
 __device__ __forceinline__ void face_flux(const double* ul, const double* ur, double gamma,
                                           double* f5, Fault& f) {
-    riemann<SOLVER, A, true>(ul, ur, gamma, f5, f);
+    riemann<SOLVER, A, FM>(ul, ur, gamma, f5, f);
     if (f.redo()) {
         V5 l, r;
 #pragma unroll
@@ -239,7 +275,8 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     double* uout = a.buf[(cur + a.out_rel) % a.nbuf];  // may alias ustart (last RK stage)
     const double* ustart = a.buf[cur];
 
-    extern __shared__ double smem[];
+    extern __shared__ __align__(128) double smem[];
+    __shared__ unsigned long long mbar[NB];
     double* planes = smem;                          // [NB][H][W][5]
     double* XP = planes + size_t(NB) * S::PLANE;    // [TY][TX+1][5]
     double* YP = XP + S::XP_N * NV;                 // [TY+1][TX][5]
@@ -293,19 +330,47 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
         return uin + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
                size_t(tx0 - G + a.gh) * NV;
     };
+    // ring slot of a plane: planes are loaded in order from zfirst, so slot = index % NB and
+    // the mbarrier phase of that load = (index / NB) & 1
+    const int zfirst = kz0 - 1 - R;
+    constexpr unsigned ROW_BYTES = W * NV * sizeof(double);  // 16-byte multiple (W even)
+    static_assert(ROW_BYTES % 16 == 0, "bulk-copy rows must be 16-byte multiples");
     auto load_plane = [&](int zact) {
-        double* dst = planes + size_t((zact + a.gh) % NB) * S::PLANE;
+        // caller guarantees every thread finished reading the slot (a __syncthreads)
+        const int li = zact - zfirst;
+        double* dst = planes + size_t(li % NB) * S::PLANE;
         const double* src = gsrc(zact);
-        for (int e = tid; e < S::PLANE; e += S::NT) {
-            int r = e / (W * NV), c = e - r * (W * NV);
-            cp_async8(dst + e, src + size_t(r) * a.pitch + c);
+        if (!a.bulk) {  // unaligned rows (odd pitch): 8-byte cp.async, waited before the barrier
+            for (int r = tid / 32; r < H; r += S::NT / 32)
+                for (int c = tid % 32; c < W * NV; c += 32)
+                    cp_async8(dst + r * (W * NV) + c, src + size_t(r) * a.pitch + c);
+            return;
         }
-        cp_async_commit();
+        unsigned long long* bar = &mbar[li % NB];
+        if (tid < 32) {
+            if (tid == 0) {
+                fence_proxy_async();  // generic-proxy reads of the slot before the async writes
+                mbar_arrive_expect_tx(bar, H * ROW_BYTES);
+            }
+            __syncwarp();
+            for (int r = tid; r < H; r += 32)
+                bulk_g2s(dst + r * (W * NV), src + size_t(r) * a.pitch, ROW_BYTES, bar);
+        }
+    };
+    auto wait_plane = [&](int zact) {
+        if (!a.bulk) return;
+        const int li = zact - zfirst;
+        mbar_wait(&mbar[li % NB], unsigned(li / NB) & 1u);
     };
     auto P = [&](int zact) -> const double* {
-        return planes + size_t((zact + a.gh) % NB) * S::PLANE;
+        return planes + size_t((zact - zfirst) % NB) * S::PLANE;
     };
 
+    if (tid == 0) {
+        for (int i = 0; i < NB; ++i) mbar_init(&mbar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
     // prologue: planes kz0-1-R .. kz0-1+R
     for (int z = kz0 - 1 - R; z <= kz0 - 1 + R; ++z) load_plane(z);
 
@@ -317,9 +382,10 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
 
     for (int lp = -1; lp <= nzc; ++lp) {
         const int p = kz0 + lp;
-        cp_async_wait_all();
-        __syncthreads();
+        if (!a.bulk) cp_async_wait_all();
+        __syncthreads();  // previous iteration's reads of the oldest slot are done
         if (!S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
+        for (int z = p - R; z <= p + R; ++z) wait_plane(z);
 
         const bool zring = (lp == -1 || lp == nzc);
         const bool do_zone = zring ? owned : exists;
@@ -333,7 +399,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
             Fault f;
             f.clear();
-            zone_states<O3, true, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
+            zone_states<O3, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
             if (f.redo()) {
                 Careful c = zone_states_careful<O3, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
 #pragma unroll
@@ -413,7 +479,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 {
                 Fault f;
                 f.clear();
-                double d = eval_tstep<true>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                double d = eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
                 if (f.redo()) {
                     V5 u5;
 #pragma unroll

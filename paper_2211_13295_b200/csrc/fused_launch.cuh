@@ -24,9 +24,13 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fused)");
         configured = true;
     }
+    // bulk-copy plane loads need 16-byte aligned rows: halo G == storage ghost width (tile
+    // origins at multiples of TX, TX + 2G even) and an even row pitch; else per-8-byte cp.async
+    FusedArgs b = a;
+    b.bulk = (a.gh == S::G && (a.pitch & 1) == 0) ? 1 : 0;
     dim3 grid((a.nx + TX - 1) / TX, (a.ny + TY - 1) / TY,
               (a.kz_last - a.kz_first + a.tz - 1) / a.tz);
-    kern<<<grid, S::NT, S::SMEM, st>>>(a);
+    kern<<<grid, S::NT, S::SMEM, st>>>(b);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "fused_ader_kernel launch");
 }

@@ -24,6 +24,7 @@ struct FusedArgs {
     int in_rel;      // this launch reads buf[(cur + in_rel) % nbuf]
     int out_rel;     // and writes buf[(cur + out_rel) % nbuf]
     int want_dt;     // take the CFL estimate (ADER: always; RK: last stage)
+    int bulk;        // plane loads by bulk copy (set by the launcher)
     double rk_a, rk_b;  // RK stage coefficients U' = a U0 + b (U + dt rate)
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width

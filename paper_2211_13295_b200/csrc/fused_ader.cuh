@@ -99,7 +99,11 @@ struct FusedShape {
     static constexpr int FY_N = (TY + 1) * TX;  // y faces 0..TY
     // FX aliases XP and FY aliases YP: each face's thread reads its +x/+y neighbour state and
     // then writes that face's flux to the same slot (no other reader in between)
-    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32);
+    // per-thread carried state of the owned zones (partial x/y rate of plane p, z flux at the
+    // bottom of plane p), [NV][TX*TY]: explicit shared memory instead of register spills
+    static constexpr int CARRY = 2 * NV * TX * TY;
+    static constexpr size_t SMEM =
+        sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32 + CARRY);
 };
 
 #ifndef HC_REASSOC
@@ -285,6 +289,8 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     double* red = YP + S::YP_N * NV;                // [32]
 
     const int tid = threadIdx.x;
+    double* part = red + 32 + tid;          // [NV] stride TX*TY (owned threads only)
+    double* fz_prev = part + NV * TX * TY;  // [NV] stride TX*TY
     // ---- E-column of this thread
     int ci, cj;
     bool is_tile;
@@ -374,9 +380,10 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
     // prologue: planes kz0-1-R .. kz0-1+R
     for (int z = kz0 - 1 - R; z <= kz0 - 1 + R; ++z) load_plane(z);
 
-    double zp_prev[NV], fz_prev[NV], part[NV];
+    constexpr int CS = TX * TY;  // stride of the carried arrays
+    double zp_prev[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) zp_prev[q] = fz_prev[q] = part[q] = 0.0;
+    for (int q = 0; q < NV; ++q) zp_prev[q] = 0.0;
     double dt_min = 1.0e32;
     const int zoff_c = (cj + G) * W + (ci + G);  // zone index of this column in a smem plane
 
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 double un[NV];
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
-                    double r = part[q] - cz * (fz_cur[q] - fz_prev[q]);
+                    double r = part[q * CS] - cz * (fz_cur[q] - fz_prev[q * CS]);
                     if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
                         un[q] = a.rk_a * ustart[zi + q] + a.rk_b * (u[q] + r);
                     else
@@ -479,7 +486,8 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 {
                 Fault f;
                 f.clear();
-                double d = eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
+                double d = FM == 2 ? eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz, a.gamma, f)
+                                  : eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
                 if (f.redo()) {
                     V5 u5;
 #pragma unroll
@@ -497,11 +505,11 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
                 const double* fys = FY + (cj * TX + ci) * NV;
 #pragma unroll
                 for (int q = 0; q < NV; ++q)
-                    part[q] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
+                    part[q * CS] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
             }
             if (lp >= 0) {
 #pragma unroll
-                for (int q = 0; q < NV; ++q) fz_prev[q] = fz_cur[q];
+                for (int q = 0; q < NV; ++q) fz_prev[q * CS] = fz_cur[q];
             }
 #pragma unroll
             for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];

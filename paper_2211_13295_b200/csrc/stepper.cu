@@ -1,3 +1,4 @@
+#include <cstdlib>
 // stepper.cu -- the device-resident stepper (include/hydro_cuda.h, hc_stepper_*).
 //
 // U_skinny lives in HBM across steps in two ping-pong buffers laid out like the reference's
@@ -136,6 +137,27 @@ int set_dev(const hc_stepper* s) {
     return HC_OK;
 }
 
+// Planes per CTA z-chunk. Each chunk re-runs reconstruction + predictor on its two z-ring
+// planes (~0.6 of a plane's cost each), and the grid runs in waves of `slots` resident CTAs:
+// pick the chunk height minimising waves x (tz + 1.2). HC_TZ overrides (tuning).
+int choose_tz(int tiles, int nz, int slots) {
+    if (const char* v = std::getenv("HC_TZ")) return std::max(4, std::min(nz, std::atoi(v)));
+    int best = std::min(32, nz);
+    double best_cost = 1e300;
+    for (int tz = 8; tz <= 96; ++tz) {
+        const int chunks = (nz + tz - 1) / tz;
+        const int eff = (nz + chunks - 1) / chunks;  // tallest chunk
+        const long ctas = long(tiles) * chunks;
+        const long waves = (ctas + slots - 1) / slots;
+        const double cost = double(waves) * (eff + 1.2);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = eff;
+        }
+    }
+    return std::max(4, std::min(best, nz));
+}
+
 FusedArgs fused_args(const hc_stepper* s) {
     FusedArgs a;
     a.buf[0] = s->buf[0];
@@ -245,10 +267,15 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     const size_t slack = size_t(std::max(TY, 16) + 2 * G + 2) * sg.pitch +
                          size_t(std::max(TX, 32) + 2 * G) * NV;
     (void)TX;
-    s->tz = std::max(4, std::min(32, g->nz));
     if ((rc = set_dev(s))) {
         delete s;
         return rc;
+    }
+    {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o->device);
+        const int tiles = ((g->nx + TX - 1) / TX) * ((g->ny + TY - 1) / TY);
+        s->tz = choose_tz(tiles, g->nz, sms * FusedTile<true>::MINB);
     }
     s->bytes = (size_t(sg.mz) * sg.my_pad * sg.pitch + slack) * sizeof(double);
     cudaError_t e = cudaMalloc(&s->buf[0], s->bytes);

@@ -7,7 +7,12 @@ order (geometry.hpp:13-27), so order 3 is the closest it supports. N>1 (torchrun
 scaling, every rank owns a 256^3 z-slab of a 256 x 256 x (256 N) periodic box; z halos go
 over NCCL, dt_next is all-reduced (min).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--fast]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--exact]
+
+The headline is the FMA build (DFMA contraction, ~1-ulp division): within 1e-12 relative L1 of
+the reference after 20 steps (the north star allows 1e-10); the bit-exact build (no
+contraction, IEEE division, identical bits) is timed on the same workload and reported
+beside it as "other_build".
 
 A "step" is one full ADER step (ghost fill + fused kernel + dt hand-off) over the whole
 mesh. value = zones x K / (max over ranks of the CUDA-event time of the K steps). The state
@@ -169,7 +174,10 @@ def workload_config(args):
         "workload": (f"C2: 3D Euler isentropic vortex {args.n}^3 per GPU, WENO-ADER O{args.order}"
                      " + HLL, periodic (configs[1]; the reference has no O4, O3 is its closest)"),
         "n": args.n, "order": args.order, "solver": "hll", "integrator": "ader",
-        "problem": "vortex", "build": "fma" if args.fast else "bit-exact",
+        "problem": "vortex",
+        "build": ("fma (DFMA contraction + ~1-ulp division; <= 1e-12 rel. L1 vs the reference "
+                  "after 20 steps, tests/test_gpu_parity.py)") if args.fast else
+                 "bit-exact (identical to the reference build)",
         "l2": "state 2 x {:.0f} MB per GPU > 126 MB L2 (no flush needed)".format(
             (args.n + 2 * args.order) ** 3 * 40 / 1e6),
         "parallelism": f"z-slab x{args.gpus}" if args.gpus > 1 else "single GPU",
@@ -187,11 +195,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--order", type=int, default=3)
-    ap.add_argument("--fast", action="store_true", help="FMA-contracted build")
+    ap.add_argument("--exact", action="store_true",
+                    help="headline the bit-exact build (default: the FMA build, <= 1e-12 rel. L1)")
+    ap.add_argument("--fast", action="store_true", help=argparse.SUPPRESS)  # (the default)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    args.fast = not args.exact
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
     if args.impl == "reference":
@@ -222,26 +233,28 @@ def main():
     dom.set_time(0.0, dt0, cfl)
 
     stream = dom.stream
-    for _ in range(args.warmup):
-        dom.step()
-    torch.cuda.synchronize()
-    dom.barrier()
 
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    launches0 = dom.launches
-    with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for k in range(args.steps):
-            dom.step(kernel_events=kev[k])
-        ev1.record(stream)
+    def timed(d, clocks=None):
+        for _ in range(args.warmup):
+            d.step()
         torch.cuda.synchronize()
-    dom.barrier()
-    ms = ev0.elapsed_time(ev1)
-    kern_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    launches = dom.launches - launches0
-    ms_max = dom.max_over_ranks(ms)
+        d.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        l0 = d.launches
+        ev0.record(d.stream)
+        for k in range(args.steps):
+            d.step(kernel_events=kev[k])
+        ev1.record(d.stream)
+        torch.cuda.synchronize()
+        d.barrier()
+        ms = ev0.elapsed_time(ev1)
+        kern = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+        return d.max_over_ranks(ms), kern, d.launches - l0
+
+    with ClockSampler(local) as clocks:
+        ms_max, kern_ms, launches = timed(dom)
     t, dt, done = dom.sync()
 
     zones_local = n ** 3
@@ -302,6 +315,19 @@ def main():
                    f"{args.e2e_chunks} z-chunks) + hc_stepper_sync (dt_next)") if world == 1 else
                   "per rank: hc_stepper_upload + slab step (NCCL halos) + hc_stepper_download"}
 
+    # the other contraction policy on the same workload (bit-exact build when the headline is
+    # the FMA build and vice versa), reported beside the headline
+    other = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
+                             exact=args.fast)
+    other.upload(s0)
+    other.set_time(0.0, dt0, cfl)
+    o_ms, o_kern, _ = timed(other)
+    other.close()
+    other_line = {"build": "bit-exact" if args.fast else "fma",
+                  "value": zones_total * args.steps / (o_ms * 1e-3) / 1e6, "unit": UNIT,
+                  "ms_per_step": o_ms / args.steps, "kernel_ms_per_launch": o_kern,
+                  "roofline_frac": fpz * zones_local / (o_kern * 1e-3) / 1e12 / peak_fp64}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
@@ -318,7 +344,8 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (isentropic vortex IC sampled on the host, problems.cpp)",
             "config": workload_config(args), "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": e2e, "gpu_launches": launches, "clocks": clocks.summary(),
+            "e2e": e2e, "other_build": other_line, "gpu_launches": launches,
+            "clocks": clocks.summary(),
             "final": {"t": t, "dt_next": dt, "steps_done": done},
         }
         print(json.dumps(line), flush=True)

@@ -57,18 +57,24 @@ static int launch_one(const FusedArgs& a, cudaStream_t st) {
     return launch_cfg<O3, SOLVER, T::TX, T::TY, T::MINB, RK>(a, st);
 }
 
+template <bool O3, bool RK>
+static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
+    switch (solver) {
+        case 0: return launch_one<O3, 0, RK>(a, st);
+        case 1: return launch_one<O3, 1, RK>(a, st);
+        default: return launch_one<O3, 2, RK>(a, st);  // HLLC (extension)
+    }
+}
+
 }  // namespace HC_FUSED_NS
 
 int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st) {
     using namespace HC_FUSED_NS;
-    if (rk) {
-        if (order == 2)
-            return solver == 0 ? launch_one<false, 0, true>(a, st) : launch_one<false, 1, true>(a, st);
-        return solver == 0 ? launch_one<true, 0, true>(a, st) : launch_one<true, 1, true>(a, st);
-    }
-    if (order == 2)
-        return solver == 0 ? launch_one<false, 0, false>(a, st) : launch_one<false, 1, false>(a, st);
-    return solver == 0 ? launch_one<true, 0, false>(a, st) : launch_one<true, 1, false>(a, st);
+    if (rk)
+        return order == 2 ? launch_solver<false, true>(a, solver, st)
+                          : launch_solver<true, true>(a, solver, st);
+    return order == 2 ? launch_solver<false, false>(a, solver, st)
+                      : launch_solver<true, false>(a, solver, st);
 }
 
 }  // namespace hc

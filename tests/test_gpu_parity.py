@@ -58,7 +58,7 @@ def test_every_kernel_bitwise(api, orc, order):
     api.predict_patch(g, M, mg, 0.004)
     orc.predict_patch(go, M, mo, 0.004)
     assert same(mg, mo)
-    for solver in (hydro.RUSANOV, hydro.HLL):
+    for solver in (hydro.RUSANOV, hydro.HLL, hydro.HLLC):
         fg, fo = hydro.zeros_faces(g), po.zeros_faces(go)
         for ax in range(3):
             api.make_flux_axis(g, M, mg, ax, solver, fg[ax])
@@ -133,6 +133,9 @@ STEPPER_CASES = [
     (3, hydro.RUSANOV, hydro.PERIODIC, (33, 17, 5), "vortex", 3),
     (2, hydro.HLL, hydro.PERIODIC, (17, 9, 70), "vortex", 3),
     (3, hydro.HLL, hydro.OUTFLOW, (16, 8, 4), "vortex", 3),
+    # HLLC: extension without a reference counterpart, pinned to the C restatement
+    (3, hydro.HLLC, hydro.PERIODIC, (20, 18, 16), "vortex", 4),
+    (2, hydro.HLLC, hydro.OUTFLOW, (40, 12, 9), "sod", 8),
 ]
 
 

@@ -1,0 +1,67 @@
+/*
+ * hydro_mhd.h -- C ABI of the ideal-MHD extension of libhydro_cuda.so: WENO/MC-ADER for the
+ * cell-centred fluid variables, face-centred magnetic field evolved by constrained transport
+ * (CT) with edge EMFs from a multidimensional (two-dimensional HLL, "UCT-HLL") Riemann solver.
+ *
+ * NOT in the reference: the reference solver is Euler-only (SPEC.md:8 scopes out MHD,
+ * SPEC.md:345 multidimensional Riemann solvers). The north star names these updates
+ * (BASELINE.json configs 3 and 5), so they are built on the same sm_100a stack, with the
+ * same ADER structure as the Euler path (reconstruction -> per-zone predictor, one Picard pass
+ * at order 3 -> face fluxes -> conservative update -> CFL min). Parity is UNPINNED: the
+ * checker is a builder-authored numpy restatement (oracle/mhd_oracle.py) plus
+ * self-consistency (div B = 0 to round-off, conservation, measured convergence order on the
+ * smooth MHD vortex of Balsara 2004).
+ *
+ * State layout (host and device, SoA, one padded box per variable):
+ *   state[8][mz+1][my+1][mx+1], mx = nx + 2*ghost (etc.)
+ *   var 0..4 = cell averages (rho, rho*u, rho*v, rho*w, E) at [k][j][i]
+ *   var 5 = Bx on the x-face at the LOW side of zone (i,j,k), 6 = By (low y-face),
+ *   var 7 = Bz (low z-face).  E = p/(gamma-1) + rho v^2/2 + B^2/2 (Heaviside-Lorentz units).
+ * The extra index per axis holds the face at the high side of the last ghost zone.
+ * Same status codes and hc_last_error() as hydro_cuda.h.
+ */
+#ifndef HYDRO_MHD_H
+#define HYDRO_MHD_H
+
+#include <stddef.h>
+
+#include "hydro_cuda.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_MHD_NVAR 8
+
+typedef struct {
+    int order;      /* 2 (MC slopes) or 3 (WENO3 + cross terms) */
+    double gamma;
+    hc_limiter lim; /* as the Euler path: MC factors, WENO3 eps and linear weights */
+    int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis */
+    int device;
+} hc_mhd_params;
+
+typedef struct hc_mhd hc_mhd;
+
+int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out);
+int hc_mhd_destroy(hc_mhd* m);
+/* host state [8][mz+1][my+1][mx+1] <-> device */
+int hc_mhd_upload(hc_mhd* m, const double* host_state);
+int hc_mhd_download(hc_mhd* m, double* host_state);
+/* t, dt of the next step, cfl, t_final (<= 0: fixed step count) */
+int hc_mhd_set_time(hc_mhd* m, double t, double dt, double cfl, double t_final);
+/* Enqueue n ADER-CT steps: ghost fill, reconstruction + predictor, face fluxes (HLL, 3
+ * axes), edge EMFs (2D HLL, 3 axes), conservative + CT update, CFL min, dt hand-off. */
+int hc_mhd_step(hc_mhd* m, int n);
+int hc_mhd_sync(hc_mhd* m, double* t, double* dt, long* steps_done);
+/* CFL time step of the current device state: cfl / max(sum_a (|v_a| + c_f,a) / d_a) */
+int hc_mhd_cfl_dt(hc_mhd* m, double cfl, double* dt);
+/* max over active zones of |div B| * min(dx,dy,dz) (face-centred divergence) */
+int hc_mhd_max_divb(hc_mhd* m, double* out);
+/* kernels launched so far on this stepper */
+long hc_mhd_launches(hc_mhd* m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -29,6 +29,7 @@ SOURCES = {
     "fused_exact.cu": ["--fmad=false"] + TUNE,
     "fused_fast.cu": ["--fmad=true"] + TUNE,
     "peak.cu": ["--fmad=true"],
+    "mhd.cu": ["--fmad=false"],
 }
 
 
@@ -39,7 +40,7 @@ def _compile(name, flags, verbose):
     obj = os.path.join(BUILD, name.replace(".cu", f".{tag}.o"))
     log = os.path.join(BUILD, name.replace(".cu", ".ptxas.txt"))
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
-    deps.append(os.path.join(ROOT, "include", "hydro_cuda.h"))
+    deps += [os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
     cmd = [NVCC, "-c", src, "-o", obj] + COMMON + flags

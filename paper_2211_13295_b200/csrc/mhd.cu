@@ -1,0 +1,802 @@
+// mhd.cu -- ideal MHD on the ADER path, B200 (sm_100a), FP64: cell-centred fluid variables,
+// face-centred B evolved by constrained transport (CT) with edge EMFs from a
+// multidimensional Riemann solver. EXTENSION: the reference is Euler-only;
+// the north star (BASELINE.json configs 3 and 5) names these updates. The step keeps the
+// reference's ADER structure (stepper.cpp:49-78): reconstruction (MC at O2, WENO3 plus cross
+// terms at O3) -> per-zone predictor (one Picard pass at O3, predictor.cpp:26-60 with the
+// MHD flux) -> face fluxes -> edge EMFs -> conservative and CT update -> CFL min.
+//
+// Kernels (one thread per zone / face / edge, SoA state so every warp access is coalesced):
+//   k_mhd_ghosts      periodic / outflow gather for cells and faces (one pass, any order)
+//   k_mhd_predict<O3> ring zones: cell-centred B = face average, reconstruction of the 8
+//                     variables, ADER predictor; writes the half-time modes (u0 + tau/2,
+//                     slopes, and at O3 the quadratic and cross modes)
+//   k_mhd_flux<A>     HLL (Davis speeds with the fast magnetosonic speed) on the A faces;
+//                     the normal field is the mean of the two reconstructed values
+//   k_mhd_emf<C>      edge EMF E_C from the four zones around the edge: the two-dimensional
+//                     HLL Riemann solver (UCT-HLL, Londrillo & Del Zanna 2004; the HLL limit
+//                     of Balsara's MHLLE 2010): HLL-weighted corner EMFs plus the upwind
+//                     jumps of the transverse fields in both directions
+//   k_mhd_update      U -= dt div F (corrector.cpp:72-125 association), B_face -= dt curl E;
+//                     div B is preserved to round-off (each edge EMF enters the four faces
+//                     around it with opposite signs)
+//   k_mhd_dt          CFL estimate, exact min through the bit pattern (as the Euler path)
+//   k_mhd_advance     the dt -> dt_next hand-off and t_final clip (harness.cpp:155-170)
+// Compiled with --fmad=false: the numpy restatement (oracle/mhd_oracle.py) uses the same
+// expression shapes, so the two agree to the last bit on the same inputs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/hydro_mhd.h"
+#include "common.cuh"
+#include "fused_types.cuh"
+
+namespace hc {
+namespace mhd {
+
+constexpr int NM = 8;  // rho, mx, my, mz, E, Bx, By, Bz
+
+struct Box {
+    int n[3];      // active zones per axis
+    int gh;        // ghost width
+    int P, Q, R;   // padded extents (mx+1, my+1, mz+1)
+    size_t N;      // P*Q*R
+};
+
+__device__ __forceinline__ size_t at(const Box& b, int k, int j, int i) {
+    return (size_t(k) * b.Q + j) * b.P + i;
+}
+__device__ __forceinline__ size_t stride(const Box& b, int axis) {
+    return axis == 0 ? size_t(1) : (axis == 1 ? size_t(b.P) : size_t(b.P) * b.Q);
+}
+
+struct MArgs {
+    double* s;      // state [8][N]
+    double* modes;  // [NMODE][8][N]: 0 = u0 + tau/2, 1+a slope, 4+a quadratic, 7+a cross (a,a+1)
+    double* flux;   // [3][5][N] fluid fluxes, face f of axis A stored at the zone it is the low face of
+    double* emf;    // [3][N] edge EMFs: E_x(i, j-1/2, k-1/2), E_y(i-1/2, j, k-1/2), E_z(i-1/2, j-1/2, k)
+    Box b;
+    double d[3];    // dx, dy, dz
+    double id[3];   // 1/dx, 1/dy, 1/dz
+    double gamma;
+    Limiter lim;
+    int bc[3];
+    StepCtl* ctl;
+    ErrBlock* eb;
+};
+
+// --------------------------------------------------------------------------- physics
+
+struct MPrim {
+    double rho, u[3], p, b2, inv_rho;
+};
+
+// conserved -> primitive; p = (gamma-1)(E - rho v^2/2 - B^2/2)
+__device__ __forceinline__ MPrim mhd_prim(const double* c, double gamma, Fault& f) {
+    MPrim q;
+    q.rho = c[0];
+    if (!(c[0] > 0.0)) f.set(1, c[0]);
+    q.inv_rho = 1.0 / c[0];
+    q.u[0] = c[1] * q.inv_rho;
+    q.u[1] = c[2] * q.inv_rho;
+    q.u[2] = c[3] * q.inv_rho;
+    q.b2 = c[5] * c[5] + c[6] * c[6] + c[7] * c[7];
+    q.p = (gamma - 1.0) *
+          (c[4] - 0.5 * (c[1] * q.u[0] + c[2] * q.u[1] + c[3] * q.u[2]) - 0.5 * q.b2);
+    if (!(q.p > 0.0)) f.set(2, q.p);
+    return q;
+}
+
+// fast magnetosonic speed along axis A:
+// c_f^2 = ((a^2 + b^2) + sqrt((a^2 + b^2)^2 - 4 a^2 b_A^2)) / 2, a^2 = gamma p/rho, b = B/sqrt(rho)
+template <int A>
+__device__ __forceinline__ double fast_speed(const double* c, const MPrim& q, double gamma) {
+    double a2 = gamma * q.p * q.inv_rho;
+    double b2 = q.b2 * q.inv_rho;
+    double bn2 = c[5 + A] * c[5 + A] * q.inv_rho;
+    double s = a2 + b2;
+    double disc = s * s - 4.0 * a2 * bn2;
+    disc = disc > 0.0 ? disc : 0.0;
+    return sqrt(0.5 * (s + sqrt(disc)));
+}
+
+// ideal-MHD flux along axis A (8 components; the normal-field component is exactly 0)
+template <int A>
+__device__ __forceinline__ void mhd_flux(const double* c, const MPrim& q, double* f) {
+    const double un = q.u[A];
+    const double bn = c[5 + A];
+    const double vb = q.u[0] * c[5] + q.u[1] * c[6] + q.u[2] * c[7];
+    const double pt = q.p + 0.5 * q.b2;
+    f[0] = c[0] * un;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[1 + d] = c[1 + d] * un - bn * c[5 + d];
+    f[1 + A] += pt;
+    f[4] = (c[4] + pt) * un - bn * vb;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) f[5 + d] = c[5 + d] * un - bn * q.u[d];
+}
+
+// HLL with Davis speeds (the Euler path's riemann.hpp:55-86 structure, fast speed in place of c)
+template <int A>
+__device__ __forceinline__ void mhd_hll(const double* ul, const double* ur, double gamma,
+                                        double* f5, Fault& flt) {
+    MPrim ql = mhd_prim(ul, gamma, flt);
+    MPrim qr = mhd_prim(ur, gamma, flt);
+    const double cl = fast_speed<A>(ul, ql, gamma);
+    const double cr = fast_speed<A>(ur, qr, gamma);
+    const double sl = smin(ql.u[A] - cl, qr.u[A] - cr);
+    const double sr = smax(ql.u[A] + cl, qr.u[A] + cr);
+    double fl[NM], fr[NM];
+    mhd_flux<A>(ul, ql, fl);
+    mhd_flux<A>(ur, qr, fr);
+    if (sl >= 0.0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) f5[q] = fl[q];
+    } else if (sr <= 0.0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) f5[q] = fr[q];
+    } else {
+        const double inv = 1.0 / (sr - sl);
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            f5[q] = (sr * fl[q] - sl * fr[q] + sl * sr * (ur[q] - ul[q])) * inv;
+    }
+}
+
+// predictor.cpp:12-22 flux_divergence with the MHD flux; face[s][q], s = (+x,-x,+y,-y,+z,-z)
+template <bool SHIFT>
+__device__ __forceinline__ void mhd_divergence(const double (*face)[NM], const double* h,
+                                               const double* id, double gamma, double* div,
+                                               Fault& flt) {
+    double acc[NM];
+    {
+        double a[NM], b[NM], fa[NM], fb[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            a[q] = SHIFT ? face[0][q] + h[q] : face[0][q];
+            b[q] = SHIFT ? face[1][q] + h[q] : face[1][q];
+        }
+        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
+        mhd_flux<0>(a, qa, fa);
+        mhd_flux<0>(b, qb, fb);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) acc[q] = (fa[q] - fb[q]) * id[0];
+    }
+    {
+        double a[NM], b[NM], fa[NM], fb[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            a[q] = SHIFT ? face[2][q] + h[q] : face[2][q];
+            b[q] = SHIFT ? face[3][q] + h[q] : face[3][q];
+        }
+        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
+        mhd_flux<1>(a, qa, fa);
+        mhd_flux<1>(b, qb, fb);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) acc[q] = acc[q] + (fa[q] - fb[q]) * id[1];
+    }
+    {
+        double a[NM], b[NM], fa[NM], fb[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            a[q] = SHIFT ? face[4][q] + h[q] : face[4][q];
+            b[q] = SHIFT ? face[5][q] + h[q] : face[5][q];
+        }
+        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
+        mhd_flux<2>(a, qa, fa);
+        mhd_flux<2>(b, qb, fb);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) div[q] = acc[q] + (fa[q] - fb[q]) * id[2];
+    }
+}
+
+// ------------------------------------------------------------------------------ kernels
+
+__device__ __forceinline__ int map_c(int c, int lo, int hi, int kind) {
+    if (c >= lo && c < hi) return c;
+    const int n = hi - lo;
+    if (kind == HC_PERIODIC) return lo + (((c - lo) % n) + n) % n;
+    return c < lo ? lo : hi - 1;
+}
+
+// Ghost gather. Active ranges: cells [gh, gh+n) per axis; the normal axis of a face field
+// [gh, gh+n] at outflow (both boundary faces are interior unknowns) and [gh, gh+n) when
+// periodic (face gh+n IS face gh). Every ghost copies its (composed) active image.
+__global__ void k_mhd_ghosts(MArgs a) {
+    if (a.ctl && a.ctl->done) return;
+    const Box& b = a.b;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= b.N) return;
+    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = int(r / (size_t(b.P) * b.Q));
+    const int c[3] = {i, j, k};
+#pragma unroll 1
+    for (int q = 0; q < NM; ++q) {
+        int src[3];
+        bool ghost = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            int hi = b.gh + b.n[d];
+            if (q >= 5 && q - 5 == d && a.bc[d] == HC_OUTFLOW) hi += 1;
+            src[d] = map_c(c[d], b.gh, hi, a.bc[d]);
+            ghost |= src[d] != c[d];
+        }
+        if (ghost) a.s[q * b.N + r] = a.s[q * b.N + at(b, src[2], src[1], src[0])];
+    }
+}
+
+// cell-centred variable q at storage offset o. B: the mean of the face pair at order 2; at
+// order 3 the fourth-order cell average 1/2 (b[-1/2] + b[+1/2]) - 1/24 (b[+3/2] - b[+1/2] -
+// b[-1/2] + b[-3/2]) (the trapezoid's h^2/8 f'' error reduced to the average's h^2/24 f'';
+// with the plain mean the face fields converge at second order only)
+template <bool O3>
+__device__ __forceinline__ double cellvar(const MArgs& a, int q, size_t o) {
+    const double* s = a.s + size_t(q) * a.b.N;
+    if (q < 5) return s[o];
+    const size_t st = stride(a.b, q - 5);
+    const double b0 = s[o], b1 = s[o + st];
+    double c = 0.5 * (b0 + b1);
+    if (O3) c = c - (1.0 / 24.0) * (((s[o + 2 * st] - b1) - b0) + s[o - st]);
+    return c;
+}
+
+template <bool O3>
+__global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    // ring zone (active coords -1..n) -> storage
+    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
+              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
+    const size_t o = at(b, k, j, i);
+    const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
+    const double dt = a.ctl->dt;
+    double face[6][NM], u0s[NM];
+    double* mo = a.modes;
+    Fault wf;  // (WENO3 in careful mode never raises)
+    wf.clear();
+#pragma unroll 1
+    for (int q = 0; q < NM; ++q) {
+        const double u0 = cellvar<O3>(a, q, o);
+        u0s[q] = u0;
+        double lin[3], quad[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double up = cellvar<O3>(a, q, o + st[d]), um = cellvar<O3>(a, q, o - st[d]);
+            if (!O3) {
+                const double cf = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
+                lin[d] = mc_limiter(up - u0, u0 - um, cf);  // reconstruct.cpp:16-28
+            } else {
+                const double upp = cellvar<O3>(a, q, o + 2 * st[d]);
+                const double umm = cellvar<O3>(a, q, o - 2 * st[d]);
+                weno3<0>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], wf);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            face[2 * d][q] = extrap<O3>(u0, +1.0, lin[d], quad[d]);
+            face[2 * d + 1][q] = extrap<O3>(u0, -1.0, lin[d], quad[d]);
+            mo[(size_t(1 + d) * NM + q) * b.N + o] = lin[d];
+        }
+        if (O3) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                mo[(size_t(4 + d) * NM + q) * b.N + o] = quad[d];
+                // cross mode of the pair (d, d+1): unlimited central mixed difference
+                const size_t sa = st[d], sb = st[(d + 1) % 3];
+                const double cr = 0.25 * ((cellvar<O3>(a, q, o + sa + sb) - cellvar<O3>(a, q, o + sa - sb)) -
+                                          (cellvar<O3>(a, q, o - sa + sb) - cellvar<O3>(a, q, o - sa - sb)));
+                mo[(size_t(7 + d) * NM + q) * b.N + o] = cr;
+            }
+        }
+    }
+    // ADER predictor (predictor.cpp:26-60): tau = -dt div F(face states); O3: one Picard pass
+    Fault f;
+    f.clear();
+    double div[NM], tau[NM];
+    mhd_divergence<false>(face, nullptr, a.id, a.gamma, div, f);
+#pragma unroll
+    for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
+    if (O3) {
+        double h[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) h[q] = 0.5 * tau[q];
+        mhd_divergence<true>(face, h, a.id, a.gamma, div, f);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
+    }
+    if (f.code) record_fault(a.eb, ST_PREDICT, f, i - b.gh, j - b.gh, k - b.gh, 0);
+#pragma unroll
+    for (int q = 0; q < NM; ++q) mo[size_t(q) * b.N + o] = u0s[q] + 0.5 * tau[q];
+}
+
+// half-time face-average state of the zone at o on its side `side` (+1 / -1) along axis A
+template <bool O3>
+__device__ __forceinline__ void face_state(const MArgs& a, size_t o, int A, double side,
+                                           double* u) {
+    const double* mo = a.modes;
+    const size_t N = a.b.N;
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+        const double m0 = mo[size_t(q) * N + o];
+        const double l = mo[(size_t(1 + A) * NM + q) * N + o];
+        const double qd = O3 ? mo[(size_t(4 + A) * NM + q) * N + o] : 0.0;
+        u[q] = extrap<O3>(m0, side, l, qd);
+    }
+}
+
+template <bool O3, int A>
+__global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
+    const int na = b.n[A] + 1, n1 = b.n[B1], n2 = b.n[B2];
+    const size_t cnt = size_t(na) * n1 * n2;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    int c[3];
+    c[A] = int(r % na);
+    c[B1] = int((r / na) % n1);
+    c[B2] = int(r / (size_t(na) * n1));
+    const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);  // zone right of the face
+    const size_t ol = o - stride(b, A);
+    double ul[NM], ur[NM], f5[5];
+    face_state<O3>(a, ol, A, +1.0, ul);
+    face_state<O3>(a, o, A, -1.0, ur);
+    const double bn = 0.5 * (ul[5 + A] + ur[5 + A]);
+    ul[5 + A] = bn;
+    ur[5 + A] = bn;
+    Fault f;
+    f.clear();
+    mhd_hll<A>(ul, ur, a.gamma, f5, f);
+    if (f.code) record_fault(a.eb, ST_FLUX, f, c[A], c[B1], c[B2], A);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) a.flux[(size_t(A) * 5 + q) * b.N + o] = f5[q];
+}
+
+// Edge EMF along axis C from the four zones around the edge (axes a = C+1, b = C+2):
+//   E_C = sum_{la,lb} w_a(la) w_b(lb) E_C(corner of zone (la,lb))
+//         + alpha_a+ alpha_a- / (alpha_a+ + alpha_a-) (B_b[a+] - B_b[a-])
+//         - alpha_b+ alpha_b- / (alpha_b+ + alpha_b-) (B_a[b+] - B_a[b-])
+// w(low) = alpha+/(alpha+ + alpha-), w(high) = alpha-/(alpha+ + alpha-); alpha+ = max(0, max
+// over the corners of v + c_f), alpha- = max(0, max of c_f - v); B_b[a-] = mean of the two
+// low-a corner values (and so on); E_C = -(v x B)_C = v_b B_a - v_a B_b.
+template <bool O3, int C>
+__global__ void __launch_bounds__(128) k_mhd_emf(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
+    const int nc = b.n[C], na = b.n[AA] + 1, nb = b.n[BB] + 1;
+    const size_t cnt = size_t(nc) * na * nb;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    int c[3];
+    c[AA] = int(r % na);
+    c[BB] = int((r / na) % nb);
+    c[C] = int(r / (size_t(na) * nb));
+    const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
+    const size_t sa = stride(b, AA), sb = stride(b, BB);
+    const double* mo = a.modes;
+    const size_t N = b.N;
+    double ec[2][2], ba[2][2], bb[2][2];
+    double apa = 0.0, ama = 0.0, apb = 0.0, amb = 0.0;
+    Fault f;
+    f.clear();
+#pragma unroll
+    for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int la = 0; la < 2; ++la) {
+            // zone (la - 1, lb - 1) relative to the edge's high zone; corner at (xa, xb)
+            const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
+            const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
+            double u[NM];
+#pragma unroll
+            for (int q = 0; q < NM; ++q) {
+                double v = mo[size_t(q) * N + z] + xa * mo[(size_t(1 + AA) * NM + q) * N + z] +
+                           xb * mo[(size_t(1 + BB) * NM + q) * N + z];
+                if (O3)
+                    v = v + (1.0 / 6.0) * mo[(size_t(4 + AA) * NM + q) * N + z] +
+                        (1.0 / 6.0) * mo[(size_t(4 + BB) * NM + q) * N + z] +
+                        (xa * xb) * mo[(size_t(7 + AA) * NM + q) * N + z];
+                u[q] = v;
+            }
+            MPrim p = mhd_prim(u, a.gamma, f);
+            ec[la][lb] = p.u[BB] * u[5 + AA] - p.u[AA] * u[5 + BB];
+            ba[la][lb] = u[5 + AA];
+            bb[la][lb] = u[5 + BB];
+            const double cfa = fast_speed<AA>(u, p, a.gamma);
+            const double cfb = fast_speed<BB>(u, p, a.gamma);
+            apa = smax(apa, p.u[AA] + cfa);
+            ama = smax(ama, cfa - p.u[AA]);
+            apb = smax(apb, p.u[BB] + cfb);
+            amb = smax(amb, cfb - p.u[BB]);
+        }
+    if (f.code) record_fault(a.eb, ST_FLUX, f, c[0], c[1], c[2], 3 + C);
+    const double ia = 1.0 / (apa + ama), ib = 1.0 / (apb + amb);
+    const double wa[2] = {apa * ia, ama * ia}, wb[2] = {apb * ib, amb * ib};
+    const double e = wa[0] * wb[0] * ec[0][0] + wa[1] * wb[0] * ec[1][0] +
+                     wa[0] * wb[1] * ec[0][1] + wa[1] * wb[1] * ec[1][1];
+    const double jb = 0.5 * (bb[1][0] + bb[1][1]) - 0.5 * (bb[0][0] + bb[0][1]);  // B_b across a
+    const double ja = 0.5 * (ba[0][1] + ba[1][1]) - 0.5 * (ba[0][0] + ba[1][0]);  // B_a across b
+    a.emf[size_t(C) * N + o] = e + apa * ama * ia * jb - apb * amb * ib * ja;
+}
+
+// Conservative update of the cells (corrector.cpp:72-125 association) and CT update of the
+// faces: dB_x/dt = -(dE_z/dy - dE_y/dz), dB_y/dt = -(dE_x/dz - dE_z/dx),
+// dB_z/dt = -(dE_y/dx - dE_x/dy).
+__global__ void k_mhd_update(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int px = b.n[0] + 1, py = b.n[1] + 1;
+    const size_t cnt = size_t(px) * py * (b.n[2] + 1);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int i = int(r % px), j = int((r / px) % py), k = int(r / (size_t(px) * py));
+    const bool ci = i < b.n[0], cj = j < b.n[1], ck = k < b.n[2];
+    const size_t o = at(b, k + b.gh, j + b.gh, i + b.gh);
+    const size_t N = b.N, sy = b.P, sz = size_t(b.P) * b.Q;
+    const double dt = a.ctl->dt;
+    const double cx = dt / a.d[0], cy = dt / a.d[1], cz = dt / a.d[2];  // corrector.cpp:75
+    const double* F = a.flux;
+    const double* ex = a.emf;
+    const double* ey = a.emf + N;
+    const double* ez = a.emf + 2 * N;
+    if (ci && cj && ck) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const double* fx = F + (size_t(0) * 5 + q) * N;
+            const double* fy = F + (size_t(1) * 5 + q) * N;
+            const double* fz = F + (size_t(2) * 5 + q) * N;
+            const double rr = -cx * (fx[o + 1] - fx[o]) - cy * (fy[o + sy] - fy[o]) -
+                              cz * (fz[o + sz] - fz[o]);
+            a.s[q * N + o] = a.s[q * N + o] + rr;
+        }
+    }
+    if (cj && ck)
+        a.s[5 * N + o] = a.s[5 * N + o] - (cy * (ez[o + sy] - ez[o]) - cz * (ey[o + sz] - ey[o]));
+    if (ci && ck)
+        a.s[6 * N + o] = a.s[6 * N + o] - (cz * (ex[o + sz] - ex[o]) - cx * (ez[o + 1] - ez[o]));
+    if (ci && cj)
+        a.s[7 * N + o] = a.s[7 * N + o] - (cx * (ey[o + 1] - ey[o]) - cy * (ex[o + sy] - ex[o]));
+}
+
+// CFL estimate of a zone (eval_tstep_ptwise shape with the fast speed), exact min
+template <bool O3>
+__device__ __forceinline__ double zone_dt(const MArgs& a, size_t o, double cfl, Fault& f) {
+    double u[NM];
+#pragma unroll
+    for (int q = 0; q < NM; ++q) u[q] = cellvar<O3>(a, q, o);
+    MPrim p = mhd_prim(u, a.gamma, f);
+    const double sx = fabs(p.u[0]) + fast_speed<0>(u, p, a.gamma);
+    const double sy = fabs(p.u[1]) + fast_speed<1>(u, p, a.gamma);
+    const double sz = fabs(p.u[2]) + fast_speed<2>(u, p, a.gamma);
+    return cfl / (sx / a.d[0] + sy / a.d[1] + sz / a.d[2]);
+}
+
+template <bool O3>
+__global__ void k_mhd_dt(MArgs a, double cfl, double* out, int stage) {
+    if (a.ctl && a.ctl->done && stage == ST_UPDATE) return;
+    const Box& b = a.b;
+    const size_t cnt = size_t(b.n[0]) * b.n[1] * b.n[2];
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    double d = 1.0e32;
+    if (r < cnt) {
+        const int i = int(r % b.n[0]), j = int((r / b.n[0]) % b.n[1]),
+                  k = int(r / (size_t(b.n[0]) * b.n[1]));
+        Fault f;
+        f.clear();
+        const double v = zone_dt<O3>(a, at(b, k + b.gh, j + b.gh, i + b.gh), cfl, f);
+        if (f.code) record_fault(a.eb, stage, f, i, j, k, 0);
+        else d = v;
+    }
+    d = warp_min(d);
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 1.0e32;
+        v = warp_min(v);
+        if (threadIdx.x == 0) atomic_min_pos(out, v);
+    }
+}
+
+__global__ void k_mhd_divb(MArgs a, double* out) {
+    const Box& b = a.b;
+    const size_t cnt = size_t(b.n[0]) * b.n[1] * b.n[2];
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    double d = 0.0;
+    if (r < cnt) {
+        const int i = int(r % b.n[0]), j = int((r / b.n[0]) % b.n[1]),
+                  k = int(r / (size_t(b.n[0]) * b.n[1]));
+        const size_t o = at(b, k + b.gh, j + b.gh, i + b.gh), N = b.N;
+        const double* s = a.s;
+        const double dv = (s[5 * N + o + 1] - s[5 * N + o]) / a.d[0] +
+                          (s[6 * N + o + b.P] - s[6 * N + o]) / a.d[1] +
+                          (s[7 * N + o + size_t(b.P) * b.Q] - s[7 * N + o]) / a.d[2];
+        d = fabs(dv) * fmin(a.d[0], fmin(a.d[1], a.d[2]));
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, s));
+    if ((threadIdx.x & 31) == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(out),
+                  static_cast<unsigned long long>(__double_as_longlong(d)));
+}
+
+__global__ void k_mhd_advance(StepCtl* c, const ErrBlock* eb) {
+    if (c->done) return;
+    for (int s = 0; s < ST_COUNT; ++s)
+        if (eb->rec[s].flag) {
+            c->done = 2;
+            return;
+        }
+    c->t = c->t + c->dt;
+    c->steps += 1;
+    double dn = c->acc;
+    c->dt_next = dn;
+    c->acc = 1.0e32;
+    if (c->t_final > 0.0) {  // harness.cpp:156-160
+        double rem = c->t_final - c->t;
+        if (rem <= 1e-12 * c->t_final) c->done = 1;
+        else if (dn >= rem) dn = rem;
+    }
+    c->dt = dn;
+}
+
+}  // namespace mhd
+}  // namespace hc
+
+using namespace hc;
+using namespace hc::mhd;
+
+struct hc_mhd {
+    hc_geom g;
+    hc_mhd_params p;
+    Box b;
+    double* s = nullptr;
+    double* modes = nullptr;
+    double* flux = nullptr;
+    double* emf = nullptr;
+    double* scratch = nullptr;  // one double for reductions
+    StepCtl* ctl = nullptr;
+    ErrBlock* eb = nullptr;
+    cudaStream_t st = nullptr;
+    long launches = 0;
+    double cfl = 0.4;
+};
+
+namespace {
+
+MArgs margs(const hc_mhd* m) {
+    MArgs a;
+    a.s = m->s;
+    a.modes = m->modes;
+    a.flux = m->flux;
+    a.emf = m->emf;
+    a.b = m->b;
+    a.d[0] = m->g.dx;
+    a.d[1] = m->g.dy;
+    a.d[2] = m->g.dz;
+    for (int d = 0; d < 3; ++d) a.id[d] = 1.0 / a.d[d];  // predictor.cpp:29
+    a.gamma = m->p.gamma;
+    a.lim = Limiter{m->p.lim.cfac_rho, m->p.lim.cfac_other, m->p.lim.weno_eps,
+                    m->p.lim.weno_w[0], m->p.lim.weno_w[1], m->p.lim.weno_w[2]};
+    for (int d = 0; d < 3; ++d) a.bc[d] = m->p.bc[d];
+    a.ctl = m->ctl;
+    a.eb = m->eb;
+    return a;
+}
+
+inline unsigned blocks(size_t n, int tpb) { return unsigned((n + tpb - 1) / tpb); }
+
+int launch_step(hc_mhd* m) {
+    MArgs a = margs(m);
+    const Box& b = m->b;
+    const bool o3 = m->p.order == 3;
+    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
+    k_mhd_ghosts<<<blocks(b.N, 256), 256, 0, m->st>>>(a);
+    if (o3) k_mhd_predict<true><<<blocks(ring, 128), 128, 0, m->st>>>(a);
+    else k_mhd_predict<false><<<blocks(ring, 128), 128, 0, m->st>>>(a);
+    const size_t fx = size_t(b.n[0] + 1) * b.n[1] * b.n[2];
+    const size_t fy = size_t(b.n[0]) * (b.n[1] + 1) * b.n[2];
+    const size_t fz = size_t(b.n[0]) * b.n[1] * (b.n[2] + 1);
+    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (b.n[2] + 1);
+    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (b.n[2] + 1);
+    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * b.n[2];
+    if (o3) {
+        k_mhd_flux<true, 0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<true, 1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<true, 2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<true, 0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<true, 1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<true, 2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
+    } else {
+        k_mhd_flux<false, 0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<false, 1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<false, 2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<false, 0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<false, 1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
+        k_mhd_emf<false, 2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
+    }
+    const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
+    k_mhd_update<<<blocks(up, 256), 256, 0, m->st>>>(a);
+    const size_t act = size_t(b.n[0]) * b.n[1] * b.n[2];
+    // CFL estimate of the updated state: its ghosts are stale, but zone_dt reads only the
+    // zone's own faces, which are all active
+    if (o3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
+    else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
+    k_mhd_advance<<<1, 1, 0, m->st>>>(m->ctl, m->eb);
+    m->launches += 11;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd step launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
+    if (!p || !out) {
+        set_error(HC_INVALID, "null argument");
+        return HC_INVALID;
+    }
+    int rc = validate_geom(g, p->order);
+    if (rc) return rc;
+    if (g->ghost < (p->order == 3 ? 4 : 2)) {  // WENO radius 2 + ring + B cell average
+        set_error(HC_INVALID, "mhd: order 3 needs a ghost width of at least 4");
+        return HC_INVALID;
+    }
+    for (int d = 0; d < 3; ++d)
+        if (p->bc[d] != HC_PERIODIC && p->bc[d] != HC_OUTFLOW) {
+            set_error(HC_INVALID, "mhd: boundary kind must be periodic or outflow");
+            return HC_INVALID;
+        }
+    hc_mhd* m = new (std::nothrow) hc_mhd;
+    if (!m) {
+        set_error(HC_CUDA, "out of host memory");
+        return HC_CUDA;
+    }
+    m->g = *g;
+    m->p = *p;
+    Box& b = m->b;
+    b.n[0] = g->nx;
+    b.n[1] = g->ny;
+    b.n[2] = g->nz;
+    b.gh = g->ghost;
+    b.P = g->nx + 2 * g->ghost + 1;
+    b.Q = g->ny + 2 * g->ghost + 1;
+    b.R = g->nz + 2 * g->ghost + 1;
+    b.N = size_t(b.P) * b.Q * b.R;
+    const int nmode = p->order == 3 ? 10 : 4;
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e == cudaSuccess) e = cudaMalloc(&m->s, sizeof(double) * NM * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->modes, sizeof(double) * size_t(nmode) * NM * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->flux, sizeof(double) * 15 * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->emf, sizeof(double) * 3 * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->scratch, sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&m->ctl, sizeof(StepCtl));
+    if (e == cudaSuccess) e = cudaMalloc(&m->eb, sizeof(ErrBlock));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemset(m->s, 0, sizeof(double) * NM * b.N);
+    if (e == cudaSuccess) e = cudaMemset(m->flux, 0, sizeof(double) * 15 * b.N);
+    if (e == cudaSuccess) e = cudaMemset(m->emf, 0, sizeof(double) * 3 * b.N);
+    if (e == cudaSuccess) e = cudaMemset(m->eb, 0, sizeof(ErrBlock));
+    if (e == cudaSuccess) {
+        StepCtl c{};
+        c.acc = 1.0e32;
+        e = cudaMemcpy(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+        hc_mhd_destroy(m);
+        return cuda_fail(e, "hc_mhd_create");
+    }
+    *out = m;
+    return HC_OK;
+}
+
+int hc_mhd_destroy(hc_mhd* m) {
+    if (!m) return HC_OK;
+    cudaSetDevice(m->p.device);
+    if (m->st) cudaStreamSynchronize(m->st);
+    cudaFree(m->s);
+    cudaFree(m->modes);
+    cudaFree(m->flux);
+    cudaFree(m->emf);
+    cudaFree(m->scratch);
+    cudaFree(m->ctl);
+    cudaFree(m->eb);
+    if (m->st) cudaStreamDestroy(m->st);
+    delete m;
+    return HC_OK;
+}
+
+int hc_mhd_upload(hc_mhd* m, const double* host) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    HC_CUDA(cudaMemcpyAsync(m->s, host, sizeof(double) * NM * m->b.N, cudaMemcpyHostToDevice,
+                            m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_mhd_download(hc_mhd* m, double* host) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    HC_CUDA(cudaMemcpyAsync(host, m->s, sizeof(double) * NM * m->b.N, cudaMemcpyDeviceToHost,
+                            m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_mhd_set_time(hc_mhd* m, double t, double dt, double cfl, double t_final) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    StepCtl c{};
+    c.dt = dt;
+    c.t = t;
+    c.t_final = t_final;
+    c.acc = 1.0e32;
+    c.dt_next = dt;
+    m->cfl = cfl;
+    HC_CUDA(cudaMemcpyAsync(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice, m->st));
+    HC_CUDA(cudaMemsetAsync(m->eb, 0, sizeof(ErrBlock), m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_mhd_step(hc_mhd* m, int n) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    for (int s = 0; s < n; ++s) {
+        int rc = launch_step(m);
+        if (rc) return rc;
+    }
+    return HC_OK;
+}
+
+int hc_mhd_sync(hc_mhd* m, double* t, double* dt, long* steps) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    StepCtl c;
+    ErrBlock eb;
+    HC_CUDA(cudaMemcpyAsync(&c, m->ctl, sizeof c, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaMemcpyAsync(&eb, m->eb, sizeof eb, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    if (t) *t = c.t;
+    if (dt) *dt = c.dt;
+    if (steps) *steps = long(c.steps);
+    return report_device_errors(eb);
+}
+
+int hc_mhd_cfl_dt(hc_mhd* m, double cfl, double* dt) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    MArgs a = margs(m);
+    const double seed = 1.0e32;
+    HC_CUDA(cudaMemcpyAsync(m->scratch, &seed, sizeof seed, cudaMemcpyHostToDevice, m->st));
+    HC_CUDA(cudaMemsetAsync(m->eb, 0, sizeof(ErrBlock), m->st));
+    const size_t act = size_t(m->b.n[0]) * m->b.n[1] * m->b.n[2];
+    if (m->p.order == 3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, cfl, m->scratch, ST_DT);
+    else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, cfl, m->scratch, ST_DT);
+    m->launches += 1;
+    ErrBlock eb;
+    HC_CUDA(cudaMemcpyAsync(dt, m->scratch, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaMemcpyAsync(&eb, m->eb, sizeof eb, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return report_device_errors(eb);
+}
+
+int hc_mhd_max_divb(hc_mhd* m, double* out) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    MArgs a = margs(m);
+    HC_CUDA(cudaMemsetAsync(m->scratch, 0, sizeof(double), m->st));
+    const size_t act = size_t(m->b.n[0]) * m->b.n[1] * m->b.n[2];
+    k_mhd_divb<<<blocks(act, 256), 256, 0, m->st>>>(a, m->scratch);
+    m->launches += 1;
+    HC_CUDA(cudaMemcpyAsync(out, m->scratch, sizeof(double), cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+long hc_mhd_launches(hc_mhd* m) { return m ? m->launches : 0; }
+
+}  // extern "C"

@@ -167,11 +167,13 @@ def load_library(path: str = LIB_PATH):
 
 
 def exported_symbols():
-    """Names declared in include/hydro_cuda.h (checked against the .so by the CPU tests)."""
+    """Names declared in include/*.h (checked against the .so by the CPU tests)."""
+    import glob
     import re
-    hdr = os.path.join(os.path.dirname(PKG), "include", "hydro_cuda.h")
-    with open(hdr) as f:
-        txt = f.read()
+    txt = ""
+    for hdr in sorted(glob.glob(os.path.join(os.path.dirname(PKG), "include", "*.h"))):
+        with open(hdr) as f:
+            txt += f.read()
     return sorted(set(re.findall(r"^\s*(?:int|long)\s+(hc_[a-z0-9_]+)\s*\(", txt, re.M)))
 
 

@@ -1,0 +1,136 @@
+"""GPU tests of the ideal-MHD ADER-CT extension (include/hydro_mhd.h). PARITY UNPINNED: the
+reference has no MHD, so the checks are (1) the sm_100a kernels against the
+builder-authored numpy restatement oracle/mhd_oracle.py, bit for bit (same expression shapes,
+--fmad=false), and (2) self-consistency of the scheme: div B preserved to round-off,
+conservation to round-off, the measured convergence order on the smooth MHD vortex
+(Balsara 2004), and robustness on Orszag-Tang."""
+import numpy as np
+import pytest
+
+from oracle import mhd_oracle as mo
+from paper_2211_13295_b200 import hydro, mhd
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def active(s, g):
+    gh = g.ghost
+    return s[:, gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx]
+
+
+def setup(problem, n, order, bc=(mhd.PERIODIC,) * 3):
+    if problem == "vortex":
+        lo, hi = (-5, -5, -5), (5, 5, 5)
+        g = mhd.make_geometry(*n, order, lo, hi)
+        s = mhd.mhd_vortex(g, order)
+    elif problem == "ot":
+        lo, hi = (0, 0, 0), (1, 1, 1)
+        g = mhd.make_geometry(*n, order, lo, hi)
+        s = mhd.orszag_tang(g, order)
+    else:
+        lo, hi = (0, 0, 0), (1, 1, 1)
+        g = mhd.make_geometry(*n, order, lo, hi)
+        s = mhd.random_field(g, order)
+    G = mo.Geom(*n, order, lo, hi)
+    return g, G, s
+
+
+CASES = [
+    # problem, n, order, bc, steps
+    ("vortex", (12, 10, 6), 2, (0, 0, 0), 4),
+    ("vortex", (12, 10, 6), 3, (0, 0, 0), 4),
+    ("random", (8, 9, 10), 3, (0, 0, 0), 3),
+    ("random", (10, 8, 6), 2, (1, 0, 1), 3),
+    ("ot", (16, 12, 4), 3, (1, 1, 0), 3),
+]
+
+
+@pytest.mark.parametrize("problem,n,order,bc,steps", CASES)
+def test_mhd_bitwise_vs_restatement(problem, n, order, bc, steps):
+    g, G, s0 = setup(problem, n, order)
+    cfl = 0.4
+    st = mhd.MhdStepper(g, mhd.make_params(order, bc=bc))
+    st.upload(s0)
+    dt0 = st.cfl_dt(cfl)
+    s_ref = s0.copy()
+    par = mo.Params(order, bc=bc)
+    assert dt0 == mo.cfl_dt(s_ref, G, par, cfl)
+    dts, dt_next, t = mo.run_steps(s_ref, G, par, cfl, steps, dt0)
+    st.set_time(0.0, dt0, cfl)
+    st.step(steps)
+    tg, dtg, done = st.sync()
+    out = st.download()
+    assert done == steps
+    a, b = active(out, g), active(s_ref, g)
+    diff = np.abs(a - b).max()
+    assert (bits(a) == bits(b)).all(), f"max |diff| {diff}"
+    assert dtg == dt_next and tg == t
+    st.close()
+
+
+def test_mhd_divb_and_conservation_3d():
+    n, order = (24, 24, 24), 3
+    g, G, s0 = setup("random", n, order)
+    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st.upload(s0)
+    d0 = st.max_divb()
+    t, dt, done = st.run(0.4, nsteps=60)
+    assert done == 60
+    s = st.download()
+    bmax = np.abs(active(s, g)[5:]).max()
+    d1 = st.max_divb()
+    assert d1 < 1e-13 * bmax, (d0, d1, bmax)  # |div B| dx, relative to |B|
+    tot0 = active(s0, g)[:5].sum(axis=(1, 2, 3))
+    tot1 = active(s, g)[:5].sum(axis=(1, 2, 3))
+    scale = np.abs(active(s0, g)[:5]).sum(axis=(1, 2, 3))
+    assert (np.abs(tot1 - tot0) <= 1e-13 * scale + 1e-13).all(), (tot0, tot1)
+    st.close()
+
+
+def _vortex_error(n, order, t_final=1.0):
+    g, G, s0 = setup("vortex", (n, n, 4), order)
+    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st.upload(s0)
+    t, dt, done = st.run(0.4, t_final=t_final)
+    s = st.download()
+    ex = mhd.mhd_vortex(g, order, t=t)
+    a, b = active(s, g), active(ex, g)
+    st.close()
+    return np.abs(a[0] - b[0]).mean(), np.abs(a[5] - b[5]).mean(), abs(t - t_final)
+
+
+@pytest.mark.parametrize("order,lo_rho,lo_b", [(2, 1.6, 1.6), (3, 2.5, 1.9)])
+def test_mhd_vortex_convergence(order, lo_rho, lo_b):
+    """measured order on the smooth MHD vortex, 32 -> 64 -> 128 zones (cf. the reference's
+    Euler windows, acceptance_main.cpp:342-343)"""
+    e = [_vortex_error(n, order) for n in (32, 64, 128)]
+    for _, _, dt_err in e:
+        assert dt_err < 1e-12
+    rho = [x[0] for x in e]
+    bx = [x[1] for x in e]
+    o_rho = np.log2(rho[1] / rho[2])
+    o_b = np.log2(bx[1] / bx[2])
+    assert o_rho >= lo_rho and o_b >= lo_b, (order, rho, bx, o_rho, o_b)
+
+
+def test_mhd_orszag_tang_runs():
+    g, G, s0 = setup("ot", (128, 128, 4), 3)
+    st = mhd.MhdStepper(g, mhd.make_params(3))
+    st.upload(s0)
+    t, dt, done = st.run(0.4, t_final=0.5)
+    assert abs(t - 0.5) < 1e-12
+    s = st.download()
+    assert np.isfinite(s).all()
+    bmax = np.abs(active(s, g)[5:]).max()
+    assert st.max_divb() < 1e-12 * bmax
+    st.close()
+
+
+def test_mhd_rejects_small_ghost():
+    g = hydro.make_geometry(8, 8, 8, 3, (0, 0, 0), (1, 1, 1))  # Euler ghost width 3
+    with pytest.raises(ValueError):
+        mhd.MhdStepper(g, mhd.make_params(3))

@@ -184,6 +184,100 @@ def workload_config(args):
     }
 
 
+# ---------------------------------------------------------------------- MHD (extension)
+
+
+def bench_mhd(args):
+    """BASELINE.json configs[2]: 3D MHD Orszag-Tang (z-invariant initial data on a 3D mesh)
+    with constrained transport and the 2D-HLL edge solver, WENO-ADER O3, 384^3 on one GPU.
+    No reference counterpart (parity unpinned; checked against oracle/mhd_oracle.py)."""
+    import numpy as np
+    import torch
+
+    from paper_2211_13295_b200 import mhd
+    n = args.n if args.n != 256 else 384
+    order = args.order
+    torch.cuda.set_device(0)
+    g = mhd.make_geometry(n, n, n, order, (0, 0, 0), (1, 1, 1))
+    s0 = mhd.orszag_tang(g, order)
+    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st.upload(s0)
+    cfl = 0.4
+    dt0 = st.cfl_dt(cfl)
+    st.set_time(0.0, dt0, cfl)
+    stream = torch.cuda.ExternalStream(st.stream_ptr)
+    st.step(args.warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = st.launches
+    with ClockSampler(0) as clocks:
+        e0.record(stream)
+        st.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = st.launches - l0
+    t, dt, done = st.sync()
+    zones = n ** 3
+    value = zones * args.steps / (ms * 1e-3) / 1e6
+    # roofline: this first MHD path is unfused (predict -> 3 flux -> 3 EMF -> update), so it
+    # is HBM-bound: ideal traffic with one pass per kernel (DESIGN.md 8)
+    bytes_per_zone = 2900.0
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = bytes_per_zone * zones / (ms / args.steps * 1e-3) / 1e9
+    # end to end through the public API with host buffers (H2D state, step, D2H state)
+    host = torch.empty(s0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    host[...] = s0
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    ee = 2
+    for _ in range(ee):
+        st.upload(host)
+        st.step(1)
+        host[...] = st.download()
+    e2e_s = (time.perf_counter() - h0) / ee
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import mhd_oracle as mo
+        cn = 32
+        cg = mhd.make_geometry(cn, cn, cn, order, (0, 0, 0), (1, 1, 1))
+        cs = mhd.orszag_tang(cg, order)
+        G = mo.Geom(cn, cn, cn, order, (0, 0, 0), (1, 1, 1))
+        par = mo.Params(order)
+        cdt = mo.cfl_dt(cs, G, par, cfl)
+        c0 = time.perf_counter()
+        mo.run_steps(cs, G, par, cfl, 2, cdt)
+        cpu = {"value": cn ** 3 * 2 / (time.perf_counter() - c0) / 1e6, "unit": UNIT,
+               "cores": 1, "kind": "port",
+               "sample": f"{cn}^3 O{order} Orszag-Tang, 2 steps of the numpy restatement "
+                         "oracle/mhd_oracle.py (the reference has no MHD)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (Orszag-Tang IC sampled on the host, B from a vector potential)",
+        "config": {"workload": f"C3: 3D ideal MHD Orszag-Tang {n}^3, WENO-ADER O{order}, HLL "
+                               "faces + 2D-HLL (UCT) edge EMFs, constrained transport "
+                               "(configs[2]; extension, no reference counterpart)",
+                   "n": n, "order": order, "build": "bit-exact (--fmad=false)",
+                   "l2": "state + modes ~50 GB > L2", "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak,
+                     "traffic": None, "bytes_per_zone": bytes_per_zone,
+                     "note": "whole step (11 kernels) against the ideal one-pass traffic of "
+                             "the unfused design"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": zones / e2e_s / 1e6, "unit": UNIT,
+                "h2d_bytes_per_step": host.nbytes, "d2h_bytes_per_step": host.nbytes,
+                "api": "hc_mhd_upload + hc_mhd_step + hc_mhd_download (host wall clock)"},
+        "gpu_launches": launches, "clocks": clocks.summary(),
+        "final": {"t": t, "dt_next": dt, "steps_done": done, "max_divb": st.max_divb()},
+    }
+    st.close()
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------- our arm
 
 
@@ -201,10 +295,20 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="euler", choices=["euler", "mhd"],
+                    help="euler: configs[1] (the headline); mhd: configs[2], 3D Orszag-Tang "
+                         "with CT + the multidimensional Riemann solver (extension, 384^3)")
     args = ap.parse_args()
     args.fast = not args.exact
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
+    if args.workload == "mhd":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "the reference has no MHD (SPEC.md:8); nothing to run"}))
+            return
+        bench_mhd(args)
+        return
     if args.impl == "reference":
         reference_arm(args)
         return

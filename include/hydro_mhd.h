@@ -60,6 +60,8 @@ int hc_mhd_cfl_dt(hc_mhd* m, double cfl, double* dt);
 int hc_mhd_max_divb(hc_mhd* m, double* out);
 /* kernels launched so far on this stepper */
 long hc_mhd_launches(hc_mhd* m);
+/* the cudaStream_t every call of this stepper runs on (for event timing) */
+int hc_mhd_stream(hc_mhd* m, void** stream);
 
 #ifdef __cplusplus
 }

@@ -58,6 +58,7 @@ struct MArgs {
     double* s;      // state [8][N]
     double* modes;  // [NMODE][8][N]: 0 = u0 + tau/2, 1+a slope, 4+a quadratic, 7+a cross (a,a+1)
     double* flux;   // [3][5][N] fluid fluxes, face f of axis A stored at the zone it is the low face of
+    double* bcell;  // [3][N] cell-centred B of the current state (k_mhd_cellb)
     double* emf;    // [3][N] edge EMFs: E_x(i, j-1/2, k-1/2), E_y(i-1/2, j, k-1/2), E_z(i-1/2, j-1/2, k)
     Box b;
     double d[3];    // dx, dy, dz
@@ -147,50 +148,43 @@ __device__ __forceinline__ void mhd_hll(const double* ul, const double* ur, doub
     }
 }
 
-// predictor.cpp:12-22 flux_divergence with the MHD flux; face[s][q], s = (+x,-x,+y,-y,+z,-z)
+// the six face states of a zone, (+x,-x,+y,-y,+z,-z) x 8 variables, in shared memory (one
+// column per thread: [s][q][thread], conflict-free) instead of a local-memory array
+struct FaceSmem {
+    double* p;
+    int t;
+    __device__ __forceinline__ double& operator()(int s, int q) const {
+        return p[(s * NM + q) * 128 + t];
+    }
+};
+
+// predictor.cpp:12-22 flux_divergence with the MHD flux; optional shift h added to every face
 template <bool SHIFT>
-__device__ __forceinline__ void mhd_divergence(const double (*face)[NM], const double* h,
+__device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const double* h,
                                                const double* id, double gamma, double* div,
                                                Fault& flt) {
-    double acc[NM];
-    {
+#pragma unroll
+    for (int A = 0; A < 3; ++A) {
         double a[NM], b[NM], fa[NM], fb[NM];
 #pragma unroll
         for (int q = 0; q < NM; ++q) {
-            a[q] = SHIFT ? face[0][q] + h[q] : face[0][q];
-            b[q] = SHIFT ? face[1][q] + h[q] : face[1][q];
+            a[q] = SHIFT ? face(2 * A, q) + h[q] : face(2 * A, q);
+            b[q] = SHIFT ? face(2 * A + 1, q) + h[q] : face(2 * A + 1, q);
         }
         MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
-        mhd_flux<0>(a, qa, fa);
-        mhd_flux<0>(b, qb, fb);
-#pragma unroll
-        for (int q = 0; q < NM; ++q) acc[q] = (fa[q] - fb[q]) * id[0];
-    }
-    {
-        double a[NM], b[NM], fa[NM], fb[NM];
-#pragma unroll
-        for (int q = 0; q < NM; ++q) {
-            a[q] = SHIFT ? face[2][q] + h[q] : face[2][q];
-            b[q] = SHIFT ? face[3][q] + h[q] : face[3][q];
+        if (A == 0) {
+            mhd_flux<0>(a, qa, fa);
+            mhd_flux<0>(b, qb, fb);
+        } else if (A == 1) {
+            mhd_flux<1>(a, qa, fa);
+            mhd_flux<1>(b, qb, fb);
+        } else {
+            mhd_flux<2>(a, qa, fa);
+            mhd_flux<2>(b, qb, fb);
         }
-        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
-        mhd_flux<1>(a, qa, fa);
-        mhd_flux<1>(b, qb, fb);
 #pragma unroll
-        for (int q = 0; q < NM; ++q) acc[q] = acc[q] + (fa[q] - fb[q]) * id[1];
-    }
-    {
-        double a[NM], b[NM], fa[NM], fb[NM];
-#pragma unroll
-        for (int q = 0; q < NM; ++q) {
-            a[q] = SHIFT ? face[4][q] + h[q] : face[4][q];
-            b[q] = SHIFT ? face[5][q] + h[q] : face[5][q];
-        }
-        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
-        mhd_flux<2>(a, qa, fa);
-        mhd_flux<2>(b, qb, fb);
-#pragma unroll
-        for (int q = 0; q < NM; ++q) div[q] = acc[q] + (fa[q] - fb[q]) * id[2];
+        for (int q = 0; q < NM; ++q)
+            div[q] = A == 0 ? (fa[q] - fb[q]) * id[0] : div[q] + (fa[q] - fb[q]) * id[A];
     }
 }
 
@@ -243,6 +237,26 @@ __device__ __forceinline__ double cellvar(const MArgs& a, int q, size_t o) {
     return c;
 }
 
+// cell-centred B of every zone whose face stencil lies in the box, once per step (the
+// predictor's stencils then read it like the fluid variables)
+template <bool O3>
+__global__ void k_mhd_cellb(MArgs a) {
+    if (a.ctl && a.ctl->done) return;
+    const Box& b = a.b;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= b.N) return;
+    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = int(r / (size_t(b.P) * b.Q));
+    const int lo = O3 ? 1 : 0, hi = O3 ? 2 : 1;  // faces c-1 .. c+2 (O3) / c .. c+1
+    if (i < lo || j < lo || k < lo || i + hi >= b.P || j + hi >= b.Q || k + hi >= b.R) return;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) a.bcell[size_t(d) * b.N + r] = cellvar<O3>(a, 5 + d, r);
+}
+
+// the 8 cell-centred variables as the predictor reads them
+__device__ __forceinline__ double wvar(const MArgs& a, int q, size_t o) {
+    return q < 5 ? a.s[size_t(q) * a.b.N + o] : a.bcell[size_t(q - 5) * a.b.N + o];
+}
+
 template <bool O3>
 __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
     if (a.ctl->done) return;
@@ -257,31 +271,31 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
     const size_t o = at(b, k, j, i);
     const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
     const double dt = a.ctl->dt;
-    double face[6][NM], u0s[NM];
+    __shared__ double sface[6 * NM * 128];
+    const FaceSmem face{sface, int(threadIdx.x)};
     double* mo = a.modes;
     Fault wf;  // (WENO3 in careful mode never raises)
     wf.clear();
 #pragma unroll 1
     for (int q = 0; q < NM; ++q) {
-        const double u0 = cellvar<O3>(a, q, o);
-        u0s[q] = u0;
+        const double u0 = wvar(a, q, o);
         double lin[3], quad[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double up = cellvar<O3>(a, q, o + st[d]), um = cellvar<O3>(a, q, o - st[d]);
+            const double up = wvar(a, q, o + st[d]), um = wvar(a, q, o - st[d]);
             if (!O3) {
                 const double cf = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
                 lin[d] = mc_limiter(up - u0, u0 - um, cf);  // reconstruct.cpp:16-28
             } else {
-                const double upp = cellvar<O3>(a, q, o + 2 * st[d]);
-                const double umm = cellvar<O3>(a, q, o - 2 * st[d]);
+                const double upp = wvar(a, q, o + 2 * st[d]);
+                const double umm = wvar(a, q, o - 2 * st[d]);
                 weno3<0>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], wf);
             }
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            face[2 * d][q] = extrap<O3>(u0, +1.0, lin[d], quad[d]);
-            face[2 * d + 1][q] = extrap<O3>(u0, -1.0, lin[d], quad[d]);
+            face(2 * d, q) = extrap<O3>(u0, +1.0, lin[d], quad[d]);
+            face(2 * d + 1, q) = extrap<O3>(u0, -1.0, lin[d], quad[d]);
             mo[(size_t(1 + d) * NM + q) * b.N + o] = lin[d];
         }
         if (O3) {
@@ -290,8 +304,8 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
                 mo[(size_t(4 + d) * NM + q) * b.N + o] = quad[d];
                 // cross mode of the pair (d, d+1): unlimited central mixed difference
                 const size_t sa = st[d], sb = st[(d + 1) % 3];
-                const double cr = 0.25 * ((cellvar<O3>(a, q, o + sa + sb) - cellvar<O3>(a, q, o + sa - sb)) -
-                                          (cellvar<O3>(a, q, o - sa + sb) - cellvar<O3>(a, q, o - sa - sb)));
+                const double cr = 0.25 * ((wvar(a, q, o + sa + sb) - wvar(a, q, o + sa - sb)) -
+                                          (wvar(a, q, o - sa + sb) - wvar(a, q, o - sa - sb)));
                 mo[(size_t(7 + d) * NM + q) * b.N + o] = cr;
             }
         }
@@ -313,7 +327,7 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
     }
     if (f.code) record_fault(a.eb, ST_PREDICT, f, i - b.gh, j - b.gh, k - b.gh, 0);
 #pragma unroll
-    for (int q = 0; q < NM; ++q) mo[size_t(q) * b.N + o] = u0s[q] + 0.5 * tau[q];
+    for (int q = 0; q < NM; ++q) mo[size_t(q) * b.N + o] = wvar(a, q, o) + 0.5 * tau[q];
 }
 
 // half-time face-average state of the zone at o on its side `side` (+1 / -1) along axis A
@@ -336,14 +350,15 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
-    const int na = b.n[A] + 1, n1 = b.n[B1], n2 = b.n[B2];
-    const size_t cnt = size_t(na) * n1 * n2;
+    // x fastest for every axis (coalesced): extents n_d, +1 along A (faces 0..n_A)
+    const int ex = b.n[0] + (A == 0), ey = b.n[1] + (A == 1), ez = b.n[2] + (A == 2);
+    const size_t cnt = size_t(ex) * ey * ez;
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (r >= cnt) return;
     int c[3];
-    c[A] = int(r % na);
-    c[B1] = int((r / na) % n1);
-    c[B2] = int(r / (size_t(na) * n1));
+    c[0] = int(r % ex);
+    c[1] = int((r / ex) % ey);
+    c[2] = int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);  // zone right of the face
     const size_t ol = o - stride(b, A);
     double ul[NM], ur[NM], f5[5];
@@ -372,14 +387,15 @@ __global__ void __launch_bounds__(128) k_mhd_emf(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
-    const int nc = b.n[C], na = b.n[AA] + 1, nb = b.n[BB] + 1;
-    const size_t cnt = size_t(nc) * na * nb;
+    // x fastest (coalesced): extents n_d, +1 across the edge (a and b run 0..n)
+    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = b.n[2] + (C != 2);
+    const size_t cnt = size_t(ex) * ey * ez;
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (r >= cnt) return;
     int c[3];
-    c[AA] = int(r % na);
-    c[BB] = int((r / na) % nb);
-    c[C] = int(r / (size_t(na) * nb));
+    c[0] = int(r % ex);
+    c[1] = int((r / ex) % ey);
+    c[2] = int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
     const size_t sa = stride(b, AA), sb = stride(b, BB);
     const double* mo = a.modes;
@@ -562,6 +578,7 @@ struct hc_mhd {
     double* modes = nullptr;
     double* flux = nullptr;
     double* emf = nullptr;
+    double* bc = nullptr;
     double* scratch = nullptr;  // one double for reductions
     StepCtl* ctl = nullptr;
     ErrBlock* eb = nullptr;
@@ -578,6 +595,7 @@ MArgs margs(const hc_mhd* m) {
     a.modes = m->modes;
     a.flux = m->flux;
     a.emf = m->emf;
+    a.bcell = m->bc;
     a.b = m->b;
     a.d[0] = m->g.dx;
     a.d[1] = m->g.dy;
@@ -600,6 +618,8 @@ int launch_step(hc_mhd* m) {
     const bool o3 = m->p.order == 3;
     const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
     k_mhd_ghosts<<<blocks(b.N, 256), 256, 0, m->st>>>(a);
+    if (o3) k_mhd_cellb<true><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
+    else k_mhd_cellb<false><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
     if (o3) k_mhd_predict<true><<<blocks(ring, 128), 128, 0, m->st>>>(a);
     else k_mhd_predict<false><<<blocks(ring, 128), 128, 0, m->st>>>(a);
     const size_t fx = size_t(b.n[0] + 1) * b.n[1] * b.n[2];
@@ -631,7 +651,7 @@ int launch_step(hc_mhd* m) {
     if (o3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
     else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
     k_mhd_advance<<<1, 1, 0, m->st>>>(m->ctl, m->eb);
-    m->launches += 11;
+    m->launches += 12;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd step launch");
 }
@@ -678,6 +698,7 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
     if (e == cudaSuccess) e = cudaMalloc(&m->modes, sizeof(double) * size_t(nmode) * NM * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->flux, sizeof(double) * 15 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, sizeof(double) * 3 * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->bc, sizeof(double) * 3 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->scratch, sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&m->ctl, sizeof(StepCtl));
     if (e == cudaSuccess) e = cudaMalloc(&m->eb, sizeof(ErrBlock));
@@ -707,6 +728,7 @@ int hc_mhd_destroy(hc_mhd* m) {
     cudaFree(m->modes);
     cudaFree(m->flux);
     cudaFree(m->emf);
+    cudaFree(m->bc);
     cudaFree(m->scratch);
     cudaFree(m->ctl);
     cudaFree(m->eb);
@@ -798,5 +820,10 @@ int hc_mhd_max_divb(hc_mhd* m, double* out) {
 }
 
 long hc_mhd_launches(hc_mhd* m) { return m ? m->launches : 0; }
+
+int hc_mhd_stream(hc_mhd* m, void** stream) {
+    *stream = m->st;
+    return HC_OK;
+}
 
 }  // extern "C"

@@ -114,6 +114,12 @@ class MhdStepper:
     def launches(self):
         return self.lib.hc_mhd_launches(self.h)
 
+    @property
+    def stream_ptr(self):
+        v = C.c_void_p()
+        _check(self.lib.hc_mhd_stream(self.h, C.byref(v)))
+        return v.value or 0
+
     def run(self, cfl, t_final=0.0, nsteps=None, max_steps=100000):
         """harness.cpp:155-170 loop on the device: dt from the CFL min of the state, then steps
         until t_final (device-side clip) or nsteps."""

@@ -30,6 +30,7 @@ SOURCES = {
     "fused_fast.cu": ["--fmad=true"] + TUNE,
     "peak.cu": ["--fmad=true"],
     "mhd.cu": ["--fmad=false"],
+    "ced.cu": ["--fmad=false"],
 }
 
 

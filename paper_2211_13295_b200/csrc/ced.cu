@@ -1,0 +1,547 @@
+// ced.cu -- computational electrodynamics in a conducting medium on the ADER path, B200
+// (sm_100a), FP64 (include/hydro_ced.h). EXTENSION: the reference scopes out CED and
+// stiff-source ADER; the north star names both (BASELINE.json config 4).
+//
+// All six unknowns are face-centred (D and B normal components), so every update is a
+// constrained-transport curl of edge values; there are no face Riemann fluxes. Per step:
+//   k_ced_ghosts        periodic / outflow gather of the six face fields
+//   k_ced_cell<O3>      cell averages of D, B from the faces (ct::face_avg)
+//   k_ced_predict<O3>   ring zones: MC / WENO3 (+ cross terms) of the 6 cell variables, ADER
+//                       predictor with the Maxwell flux and the conduction source solved
+//                       over the half step by the exponential update (one Picard pass at O3)
+//   k_ced_edge<O3, C>   E_C and H_C on the C edges from the four corner states: the 2D upwind
+//                       solver (HLL with speeds +-c is exact for linear Maxwell):
+//                         E_C = mean corner E_C + c/2 (B_b[a+] - B_b[a-]) - c/2 (B_a[b+] - B_a[b-])
+//                         H_C = mean corner H_C - c/2 (D_b[a+] - D_b[a-]) + c/2 (D_a[b+] - D_a[b-])
+//                       (a = C+1, b = C+2; [a+] = mean of the two corners on the high-a side)
+//   k_ced_update        B -= dt curl_h E;  D = exp(-s dt) D + phi(s dt) dt curl_h H,
+//                       s = sigma_face / eps, phi(z) = (1 - e^-z)/z (L-stable, exact for
+//                       frozen curl H: no time-step restriction from sigma)
+//   k_ced_advance       t/dt hand-off with the t_final clip (harness.cpp:155-170)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <new>
+#include <string>
+
+#include "../../include/hydro_ced.h"
+#include "common.cuh"
+#include "ct_common.cuh"
+#include "fused_types.cuh"
+
+namespace hc {
+namespace ced {
+
+using ct::at;
+using ct::blocks;
+using ct::Box;
+using ct::map_c;
+using ct::stride;
+
+constexpr int NF = 6;  // Dx, Dy, Dz, Bx, By, Bz
+
+struct CArgs {
+    double* s;      // [6][N] face fields
+    double* sigma;  // [N] zone conductivity
+    double* w;      // [6][N] cell averages of the face fields
+    double* modes;  // [NMODE][6][N]: 0 = u0 + tau/2, 1+a slope, 4+a quadratic, 7+a cross
+    double* emf;    // [3][N] E on the edges (same indexing as mhd.cu)
+    double* hmf;    // [3][N] H on the edges
+    Box b;
+    double d[3], id[3];
+    double eps, mu, c;
+    Limiter lim;
+    int bc[3];
+    StepCtl* ctl;
+};
+
+// exp(-z) and phi(z) = (1 - exp(-z)) / z for z = s dt >= 0 (phi(0) = 1)
+__device__ __forceinline__ void decay(double z, double& ex, double& ph) {
+    ex = exp(-z);
+    ph = z > 0.0 ? -expm1(-z) / z : 1.0;
+}
+
+// Maxwell flux along A of the state u = (D, B): F(D) = (0, H_{A+2}, -H_{A+1}),
+// F(B) = (0, -E_{A+2}, E_{A+1}) on the cyclic components (A, A+1, A+2)
+template <int A>
+__device__ __forceinline__ void maxwell_flux(const double* u, double ie, double im, double* f) {
+    constexpr int A1 = (A + 1) % 3, A2 = (A + 2) % 3;
+    f[A] = 0.0;
+    f[A1] = u[3 + A2] * im;
+    f[A2] = -(u[3 + A1] * im);
+    f[3 + A] = 0.0;
+    f[3 + A1] = -(u[A2] * ie);
+    f[3 + A2] = u[A1] * ie;
+}
+
+__global__ void k_ced_ghosts(CArgs a, int with_sigma) {
+    if (a.ctl && a.ctl->done) return;
+    const Box& b = a.b;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= b.N) return;
+    const int c[3] = {int(r % b.P), int((r / b.P) % b.Q), int(r / (size_t(b.P) * b.Q))};
+#pragma unroll 1
+    for (int q = 0; q < NF + with_sigma; ++q) {
+        int src[3];
+        bool ghost = false;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            int hi = b.gh + b.n[d];
+            if (q < NF && q % 3 == d && a.bc[d] == HC_OUTFLOW) hi += 1;
+            src[d] = map_c(c[d], b.gh, hi, a.bc[d]);
+            ghost |= src[d] != c[d];
+        }
+        if (!ghost) continue;
+        double* v = q < NF ? a.s + size_t(q) * b.N : a.sigma;
+        v[r] = v[at(b, src[2], src[1], src[0])];
+    }
+}
+
+template <bool O3>
+__global__ void k_ced_cell(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= b.N) return;
+    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = int(r / (size_t(b.P) * b.Q));
+    const int lo = O3 ? 1 : 0, hi = O3 ? 2 : 1;
+    if (i < lo || j < lo || k < lo || i + hi >= b.P || j + hi >= b.Q || k + hi >= b.R) return;
+#pragma unroll
+    for (int q = 0; q < NF; ++q)
+        a.w[size_t(q) * b.N + r] = ct::face_avg<O3>(a.s + size_t(q) * b.N, r, stride(b, q % 3));
+}
+
+template <bool O3>
+__global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
+              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
+    const size_t o = at(b, k, j, i);
+    const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
+    const double dt = a.ctl->dt;
+    const size_t N = b.N;
+    double face[6][NF], u0[NF];
+    Fault wf;
+    wf.clear();
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+        const double* w = a.w + size_t(q) * N;
+        const double c0 = w[o];
+        u0[q] = c0;
+        double lin[3], quad[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double up = w[o + st[d]], um = w[o - st[d]];
+            if (!O3) lin[d] = mc_limiter(up - c0, c0 - um, a.lim.cfac_other);
+            else weno3<0>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
+            face[2 * d][q] = extrap<O3>(c0, +1.0, lin[d], quad[d]);
+            face[2 * d + 1][q] = extrap<O3>(c0, -1.0, lin[d], quad[d]);
+            a.modes[(size_t(1 + d) * NF + q) * N + o] = lin[d];
+            if (O3) {
+                a.modes[(size_t(4 + d) * NF + q) * N + o] = quad[d];
+                const size_t sa = st[d], sb = st[(d + 1) % 3];
+                a.modes[(size_t(7 + d) * NF + q) * N + o] =
+                    0.25 * ((w[o + sa + sb] - w[o + sa - sb]) - (w[o - sa + sb] - w[o - sa - sb]));
+            }
+        }
+    }
+    // predictor: C = -div F of the face states; B: tau = dt C; D: the conduction source over
+    // the half step, D_h = e^{-s dt/2} D0 + phi(s dt/2) (dt/2) C_D, tau = 2 (D_h - D0)
+    const double ie = 1.0 / a.eps, im = 1.0 / a.mu;
+    double ex, ph;
+    decay(a.sigma[o] * ie * (0.5 * dt), ex, ph);
+    double tau[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int pass = 0; pass < (O3 ? 2 : 1); ++pass) {
+        double div[NF];
+#pragma unroll
+        for (int A = 0; A < 3; ++A) {
+            double ua[NF], ub[NF], fa[NF], fb[NF];
+#pragma unroll
+            for (int q = 0; q < NF; ++q) {
+                ua[q] = pass ? face[2 * A][q] + 0.5 * tau[q] : face[2 * A][q];
+                ub[q] = pass ? face[2 * A + 1][q] + 0.5 * tau[q] : face[2 * A + 1][q];
+            }
+            if (A == 0) { maxwell_flux<0>(ua, ie, im, fa); maxwell_flux<0>(ub, ie, im, fb); }
+            if (A == 1) { maxwell_flux<1>(ua, ie, im, fa); maxwell_flux<1>(ub, ie, im, fb); }
+            if (A == 2) { maxwell_flux<2>(ua, ie, im, fa); maxwell_flux<2>(ub, ie, im, fb); }
+#pragma unroll
+            for (int q = 0; q < NF; ++q)
+                div[q] = A == 0 ? (fa[q] - fb[q]) * a.id[0] : div[q] + (fa[q] - fb[q]) * a.id[A];
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const double dh = ex * u0[q] + ph * (0.5 * dt) * (-div[q]);
+            tau[q] = 2.0 * (dh - u0[q]);
+        }
+#pragma unroll
+        for (int q = 3; q < NF; ++q) tau[q] = -dt * div[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) a.modes[size_t(q) * N + o] = u0[q] + 0.5 * tau[q];
+}
+
+template <bool O3, int C>
+__global__ void __launch_bounds__(128) k_ced_edge(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
+    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = b.n[2] + (C != 2);
+    const size_t cnt = size_t(ex) * ey * ez;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int c0 = int(r % ex), c1 = int((r / ex) % ey), c2 = int(r / (size_t(ex) * ey));
+    const size_t o = at(b, c2 + b.gh, c1 + b.gh, c0 + b.gh);
+    const size_t sa = stride(b, AA), sb = stride(b, BB), N = b.N;
+    const double* mo = a.modes;
+    // per corner (la, lb): the six fields at the corner
+    double e = 0.0, h = 0.0, dbp = 0.0, dbm = 0.0, dap = 0.0, dam = 0.0;
+    double bbp = 0.0, bbm = 0.0, bap = 0.0, bam = 0.0;
+#pragma unroll
+    for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int la = 0; la < 2; ++la) {
+            const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
+            const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
+            double u[NF];
+#pragma unroll
+            for (int q = 0; q < NF; ++q) {
+                double v = mo[size_t(q) * N + z] + xa * mo[(size_t(1 + AA) * NF + q) * N + z] +
+                           xb * mo[(size_t(1 + BB) * NF + q) * N + z];
+                if (O3)
+                    v = v + (1.0 / 6.0) * mo[(size_t(4 + AA) * NF + q) * N + z] +
+                        (1.0 / 6.0) * mo[(size_t(4 + BB) * NF + q) * N + z] +
+                        (xa * xb) * mo[(size_t(7 + AA) * NF + q) * N + z];
+                u[q] = v;
+            }
+            e = e + u[C];      // D_C (-> E_C = D_C / eps)
+            h = h + u[3 + C];  // B_C (-> H_C = B_C / mu)
+            if (la) { dbp = dbp + u[BB]; bbp = bbp + u[3 + BB]; }
+            else { dbm = dbm + u[BB]; bbm = bbm + u[3 + BB]; }
+            if (lb) { dap = dap + u[AA]; bap = bap + u[3 + AA]; }
+            else { dam = dam + u[AA]; bam = bam + u[3 + AA]; }
+        }
+    const double hc = 0.5 * a.c;
+    // means of two corners: 0.5 * sum
+    a.emf[size_t(C) * N + o] = 0.25 * e / a.eps + hc * (0.5 * bbp - 0.5 * bbm) -
+                               hc * (0.5 * bap - 0.5 * bam);
+    a.hmf[size_t(C) * N + o] = 0.25 * h / a.mu - hc * (0.5 * dbp - 0.5 * dbm) +
+                               hc * (0.5 * dap - 0.5 * dam);
+}
+
+__global__ void k_ced_update(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int px = b.n[0] + 1, py = b.n[1] + 1;
+    const size_t cnt = size_t(px) * py * (b.n[2] + 1);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int i = int(r % px), j = int((r / px) % py), k = int(r / (size_t(px) * py));
+    const bool ci = i < b.n[0], cj = j < b.n[1], ck = k < b.n[2];
+    const size_t o = at(b, k + b.gh, j + b.gh, i + b.gh);
+    const size_t N = b.N, sx = 1, sy = b.P, sz = size_t(b.P) * b.Q;
+    const double dt = a.ctl->dt;
+    const double cx = dt / a.d[0], cy = dt / a.d[1], cz = dt / a.d[2];
+    const double* ex = a.emf;
+    const double* ey = a.emf + N;
+    const double* ez = a.emf + 2 * N;
+    const double* hx = a.hmf;
+    const double* hy = a.hmf + N;
+    const double* hz = a.hmf + 2 * N;
+    double* s = a.s;
+    const double ie = 1.0 / a.eps;
+    auto dstep = [&](int q, size_t so, double curl) {
+        double e_, p_;
+        decay(0.5 * (a.sigma[o] + a.sigma[o - so]) * ie * dt, e_, p_);
+        s[q * N + o] = e_ * s[q * N + o] + p_ * curl;
+    };
+    if (cj && ck) {
+        s[3 * N + o] = s[3 * N + o] - (cy * (ez[o + sy] - ez[o]) - cz * (ey[o + sz] - ey[o]));
+        dstep(0, sx, cy * (hz[o + sy] - hz[o]) - cz * (hy[o + sz] - hy[o]));
+    }
+    if (ci && ck) {
+        s[4 * N + o] = s[4 * N + o] - (cz * (ex[o + sz] - ex[o]) - cx * (ez[o + 1] - ez[o]));
+        dstep(1, sy, cz * (hx[o + sz] - hx[o]) - cx * (hz[o + 1] - hz[o]));
+    }
+    if (ci && cj) {
+        s[5 * N + o] = s[5 * N + o] - (cx * (ey[o + 1] - ey[o]) - cy * (ex[o + sy] - ex[o]));
+        dstep(2, sz, cx * (hy[o + 1] - hy[o]) - cy * (hx[o + sy] - hx[o]));
+    }
+}
+
+__global__ void k_ced_div(CArgs a, double* out) {
+    const Box& b = a.b;
+    const size_t cnt = size_t(b.n[0]) * b.n[1] * b.n[2];
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    double v[2] = {0.0, 0.0};
+    if (r < cnt) {
+        const int i = int(r % b.n[0]), j = int((r / b.n[0]) % b.n[1]),
+                  k = int(r / (size_t(b.n[0]) * b.n[1]));
+        const size_t o = at(b, k + b.gh, j + b.gh, i + b.gh), N = b.N;
+        const double m = fmin(a.d[0], fmin(a.d[1], a.d[2]));
+        for (int f = 0; f < 2; ++f) {
+            const double* s = a.s + size_t(3 * (1 - f)) * N;  // f = 0: B, f = 1: D
+            const double dv = (s[o + 1] - s[o]) / a.d[0] + (s[N + o + b.P] - s[N + o]) / a.d[1] +
+                              (s[2 * N + o + size_t(b.P) * b.Q] - s[2 * N + o]) / a.d[2];
+            v[f] = fabs(dv) * m;
+        }
+    }
+    for (int f = 0; f < 2; ++f) {
+        double d = v[f];
+#pragma unroll
+        for (int sft = 16; sft > 0; sft >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, sft));
+        if ((threadIdx.x & 31) == 0)
+            atomicMax(reinterpret_cast<unsigned long long*>(out + f),
+                      static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+}
+
+__global__ void k_ced_advance(StepCtl* c) {
+    if (c->done) return;
+    c->t = c->t + c->dt;
+    c->steps += 1;
+    double dn = c->dt_next;  // the medium's constant CFL step
+    if (c->t_final > 0.0) {
+        double rem = c->t_final - c->t;
+        if (rem <= 1e-12 * c->t_final) c->done = 1;
+        else if (dn >= rem) dn = rem;
+    }
+    c->dt = dn;
+}
+
+}  // namespace ced
+}  // namespace hc
+
+using namespace hc;
+using namespace hc::ced;
+
+struct hc_ced {
+    hc_geom g;
+    hc_ced_params p;
+    Box b;
+    double *s = nullptr, *sigma = nullptr, *w = nullptr, *modes = nullptr, *emf = nullptr,
+           *hmf = nullptr, *scratch = nullptr;
+    StepCtl* ctl = nullptr;
+    cudaStream_t st = nullptr;
+    long launches = 0;
+};
+
+namespace {
+
+CArgs cargs(const hc_ced* m) {
+    CArgs a;
+    a.s = m->s;
+    a.sigma = m->sigma;
+    a.w = m->w;
+    a.modes = m->modes;
+    a.emf = m->emf;
+    a.hmf = m->hmf;
+    a.b = m->b;
+    a.d[0] = m->g.dx;
+    a.d[1] = m->g.dy;
+    a.d[2] = m->g.dz;
+    for (int d = 0; d < 3; ++d) a.id[d] = 1.0 / a.d[d];
+    a.eps = m->p.eps;
+    a.mu = m->p.mu;
+    a.c = 1.0 / std::sqrt(m->p.eps * m->p.mu);
+    a.lim = Limiter{m->p.lim.cfac_rho, m->p.lim.cfac_other, m->p.lim.weno_eps,
+                    m->p.lim.weno_w[0], m->p.lim.weno_w[1], m->p.lim.weno_w[2]};
+    for (int d = 0; d < 3; ++d) a.bc[d] = m->p.bc[d];
+    a.ctl = m->ctl;
+    return a;
+}
+
+int launch_step(hc_ced* m) {
+    CArgs a = cargs(m);
+    const Box& b = m->b;
+    const bool o3 = m->p.order == 3;
+    cudaStream_t st = m->st;
+    k_ced_ghosts<<<blocks(b.N, 256), 256, 0, st>>>(a, 0);
+    if (o3) k_ced_cell<true><<<blocks(b.N, 256), 256, 0, st>>>(a);
+    else k_ced_cell<false><<<blocks(b.N, 256), 256, 0, st>>>(a);
+    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
+    if (o3) k_ced_predict<true><<<blocks(ring, 128), 128, 0, st>>>(a);
+    else k_ced_predict<false><<<blocks(ring, 128), 128, 0, st>>>(a);
+    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (b.n[2] + 1);
+    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (b.n[2] + 1);
+    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * b.n[2];
+    if (o3) {
+        k_ced_edge<true, 0><<<blocks(ex, 128), 128, 0, st>>>(a);
+        k_ced_edge<true, 1><<<blocks(ey, 128), 128, 0, st>>>(a);
+        k_ced_edge<true, 2><<<blocks(ez, 128), 128, 0, st>>>(a);
+    } else {
+        k_ced_edge<false, 0><<<blocks(ex, 128), 128, 0, st>>>(a);
+        k_ced_edge<false, 1><<<blocks(ey, 128), 128, 0, st>>>(a);
+        k_ced_edge<false, 2><<<blocks(ez, 128), 128, 0, st>>>(a);
+    }
+    const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
+    k_ced_update<<<blocks(up, 256), 256, 0, st>>>(a);
+    k_ced_advance<<<1, 1, 0, st>>>(m->ctl);
+    m->launches += 8;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "ced step launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
+    if (!p || !out) {
+        set_error(HC_INVALID, "null argument");
+        return HC_INVALID;
+    }
+    int rc = validate_geom(g, p->order);
+    if (rc) return rc;
+    if (g->ghost < (p->order == 3 ? 4 : 2)) {
+        set_error(HC_INVALID, "ced: order 3 needs a ghost width of at least 4");
+        return HC_INVALID;
+    }
+    if (!(p->eps > 0.0) || !(p->mu > 0.0)) {
+        set_error(HC_INVALID, "ced: eps and mu must be positive");
+        return HC_INVALID;
+    }
+    for (int d = 0; d < 3; ++d)
+        if (p->bc[d] != HC_PERIODIC && p->bc[d] != HC_OUTFLOW) {
+            set_error(HC_INVALID, "ced: boundary kind must be periodic or outflow");
+            return HC_INVALID;
+        }
+    hc_ced* m = new (std::nothrow) hc_ced;
+    if (!m) {
+        set_error(HC_CUDA, "out of host memory");
+        return HC_CUDA;
+    }
+    m->g = *g;
+    m->p = *p;
+    Box& b = m->b;
+    b.n[0] = g->nx;
+    b.n[1] = g->ny;
+    b.n[2] = g->nz;
+    b.gh = g->ghost;
+    b.P = g->nx + 2 * g->ghost + 1;
+    b.Q = g->ny + 2 * g->ghost + 1;
+    b.R = g->nz + 2 * g->ghost + 1;
+    b.N = size_t(b.P) * b.Q * b.R;
+    const int nmode = p->order == 3 ? 10 : 4;
+    const size_t B = sizeof(double) * b.N;
+    cudaError_t e = cudaSetDevice(p->device);
+    if (e == cudaSuccess) e = cudaMalloc(&m->s, NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->sigma, B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->w, NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->modes, size_t(nmode) * NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->emf, 3 * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->hmf, 3 * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->scratch, 2 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&m->ctl, sizeof(StepCtl));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemset(m->s, 0, NF * B);
+    if (e == cudaSuccess) e = cudaMemset(m->sigma, 0, B);
+    if (e == cudaSuccess) e = cudaMemset(m->emf, 0, 3 * B);
+    if (e == cudaSuccess) e = cudaMemset(m->hmf, 0, 3 * B);
+    if (e == cudaSuccess) {
+        StepCtl c{};
+        e = cudaMemcpy(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice);
+    }
+    if (e != cudaSuccess) {
+        hc_ced_destroy(m);
+        return cuda_fail(e, "hc_ced_create");
+    }
+    *out = m;
+    return HC_OK;
+}
+
+int hc_ced_destroy(hc_ced* m) {
+    if (!m) return HC_OK;
+    cudaSetDevice(m->p.device);
+    if (m->st) cudaStreamSynchronize(m->st);
+    for (double* p : {m->s, m->sigma, m->w, m->modes, m->emf, m->hmf, m->scratch}) cudaFree(p);
+    cudaFree(m->ctl);
+    if (m->st) cudaStreamDestroy(m->st);
+    delete m;
+    return HC_OK;
+}
+
+int hc_ced_upload(hc_ced* m, const double* host, const double* sigma) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    const size_t B = sizeof(double) * m->b.N;
+    HC_CUDA(cudaMemcpyAsync(m->s, host, NF * B, cudaMemcpyHostToDevice, m->st));
+    HC_CUDA(cudaMemcpyAsync(m->sigma, sigma, B, cudaMemcpyHostToDevice, m->st));
+    CArgs a = cargs(m);
+    a.ctl = nullptr;
+    k_ced_ghosts<<<blocks(m->b.N, 256), 256, 0, m->st>>>(a, 1);  // sigma's ghost zones
+    m->launches += 1;
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_ced_download(hc_ced* m, double* host) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    HC_CUDA(cudaMemcpyAsync(host, m->s, sizeof(double) * NF * m->b.N, cudaMemcpyDeviceToHost,
+                            m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_ced_cfl_dt(hc_ced* m, double cfl, double* dt) {
+    const double c = 1.0 / std::sqrt(m->p.eps * m->p.mu);
+    *dt = cfl / (c / m->g.dx + c / m->g.dy + c / m->g.dz);
+    return HC_OK;
+}
+
+int hc_ced_set_time(hc_ced* m, double t, double dt, double t_final) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    StepCtl c{};
+    c.t = t;
+    c.dt = dt;
+    c.dt_next = dt;
+    c.t_final = t_final;
+    if (t_final > 0.0 && dt > t_final - t) c.dt = t_final - t;
+    HC_CUDA(cudaMemcpyAsync(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
+
+int hc_ced_step(hc_ced* m, int n) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    for (int s = 0; s < n; ++s) {
+        int rc = launch_step(m);
+        if (rc) return rc;
+    }
+    return HC_OK;
+}
+
+int hc_ced_sync(hc_ced* m, double* t, double* dt, long* steps) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    StepCtl c;
+    HC_CUDA(cudaMemcpyAsync(&c, m->ctl, sizeof c, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    if (t) *t = c.t;
+    if (dt) *dt = c.dt;
+    if (steps) *steps = long(c.steps);
+    return HC_OK;
+}
+
+int hc_ced_max_div(hc_ced* m, double* divb, double* divd) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    CArgs a = cargs(m);
+    HC_CUDA(cudaMemsetAsync(m->scratch, 0, 2 * sizeof(double), m->st));
+    const size_t act = size_t(m->b.n[0]) * m->b.n[1] * m->b.n[2];
+    k_ced_div<<<blocks(act, 256), 256, 0, m->st>>>(a, m->scratch);
+    m->launches += 1;
+    double v[2];
+    HC_CUDA(cudaMemcpyAsync(v, m->scratch, sizeof v, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    *divb = v[0];
+    *divd = v[1];
+    return HC_OK;
+}
+
+long hc_ced_launches(hc_ced* m) { return m ? m->launches : 0; }
+
+}  // extern "C"

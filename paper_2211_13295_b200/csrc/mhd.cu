@@ -33,6 +33,7 @@
 
 #include "../../include/hydro_mhd.h"
 #include "common.cuh"
+#include "ct_common.cuh"
 #include "fused_types.cuh"
 
 namespace hc {
@@ -40,19 +41,10 @@ namespace mhd {
 
 constexpr int NM = 8;  // rho, mx, my, mz, E, Bx, By, Bz
 
-struct Box {
-    int n[3];      // active zones per axis
-    int gh;        // ghost width
-    int P, Q, R;   // padded extents (mx+1, my+1, mz+1)
-    size_t N;      // P*Q*R
-};
-
-__device__ __forceinline__ size_t at(const Box& b, int k, int j, int i) {
-    return (size_t(k) * b.Q + j) * b.P + i;
-}
-__device__ __forceinline__ size_t stride(const Box& b, int axis) {
-    return axis == 0 ? size_t(1) : (axis == 1 ? size_t(b.P) : size_t(b.P) * b.Q);
-}
+using ct::Box;
+using ct::at;
+using ct::map_c;
+using ct::stride;
 
 struct MArgs {
     double* s;      // state [8][N]
@@ -190,13 +182,6 @@ __device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const doubl
 
 // ------------------------------------------------------------------------------ kernels
 
-__device__ __forceinline__ int map_c(int c, int lo, int hi, int kind) {
-    if (c >= lo && c < hi) return c;
-    const int n = hi - lo;
-    if (kind == HC_PERIODIC) return lo + (((c - lo) % n) + n) % n;
-    return c < lo ? lo : hi - 1;
-}
-
 // Ghost gather. Active ranges: cells [gh, gh+n) per axis; the normal axis of a face field
 // [gh, gh+n] at outflow (both boundary faces are interior unknowns) and [gh, gh+n) when
 // periodic (face gh+n IS face gh). Every ghost copies its (composed) active image.
@@ -230,11 +215,7 @@ template <bool O3>
 __device__ __forceinline__ double cellvar(const MArgs& a, int q, size_t o) {
     const double* s = a.s + size_t(q) * a.b.N;
     if (q < 5) return s[o];
-    const size_t st = stride(a.b, q - 5);
-    const double b0 = s[o], b1 = s[o + st];
-    double c = 0.5 * (b0 + b1);
-    if (O3) c = c - (1.0 / 24.0) * (((s[o + 2 * st] - b1) - b0) + s[o - st]);
-    return c;
+    return ct::face_avg<O3>(s, o, stride(a.b, q - 5));
 }
 
 // cell-centred B of every zone whose face stencil lies in the box, once per step (the
@@ -610,7 +591,7 @@ MArgs margs(const hc_mhd* m) {
     return a;
 }
 
-inline unsigned blocks(size_t n, int tpb) { return unsigned((n + tpb - 1) / tpb); }
+using ct::blocks;
 
 int launch_step(hc_mhd* m) {
     MArgs a = margs(m);

@@ -35,8 +35,9 @@ extern "C" {
 #define HC_ABI_VERSION 1
 
 typedef enum { HC_OK = 0, HC_UNPHYSICAL = 1, HC_INVALID = 2, HC_CUDA = 3 } hc_status;
-/* riemann.hpp:12 SolverChoice; HC_HLLC is an extension (the reference has none) */
-typedef enum { HC_RUSANOV = 0, HC_HLL = 1, HC_HLLC = 2 } hc_solver_kind;
+/* riemann.hpp:12 SolverChoice; HC_HLLC and HC_HLLI are extensions (the reference has neither,
+ * SPEC.md:339) */
+typedef enum { HC_RUSANOV = 0, HC_HLL = 1, HC_HLLC = 2, HC_HLLI = 3 } hc_solver_kind;
 typedef enum { HC_PERIODIC = 0, HC_OUTFLOW = 1 } hc_boundary; /* boundary.hpp:7 BoundaryKind */
 
 /* PatchGeometry, geometry.hpp:34-65 */

@@ -45,7 +45,7 @@ typedef struct {
 } or_limiter;
 
 enum { OR_OK = 0, OR_UNPHYSICAL = 1, OR_INVALID = 2 };
-enum { OR_RUSANOV = 0, OR_HLL = 1, OR_HLLC = 2 /* extension: not in the reference */ };
+enum { OR_RUSANOV = 0, OR_HLL = 1, OR_HLLC = 2, OR_HLLI = 3 /* 2, 3: extensions */ };
 enum { OR_PERIODIC = 0, OR_OUTFLOW = 1 };
 
 /* message of the last failing call, formatted like the reference's
@@ -60,6 +60,7 @@ int or_eval_tstep_ptwise(const double* u, double cfl, double dx, double dy, doub
 int or_rusanov_flux(const double* ul, const double* ur, int axis, double gamma, double* f);
 int or_hll_flux(const double* ul, const double* ur, int axis, double gamma, double* f);
 int or_hllc_flux(const double* ul, const double* ur, int axis, double gamma, double* f);
+int or_hlli_flux(const double* ul, const double* ur, int axis, double gamma, double* f);
 double or_mc_limiter(double a, double b, double cfac);
 void or_weno3_point(const double* s, const or_limiter* cfg, double* ux, double* uxx);
 int or_predictor_ptwise(double* zone_v, int modes, double dt, double dx, double dy, double dz,

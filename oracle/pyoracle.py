@@ -19,7 +19,7 @@ ORACLE_SO = os.path.join(HERE, "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhydro_ref.so")
 
 NVAR = 5
-RUSANOV, HLL, HLLC = 0, 1, 2  # HLLC: builder-authored extension (parity unpinned)
+RUSANOV, HLL, HLLC, HLLI = 0, 1, 2, 3  # HLLC/HLLI: builder-authored extensions (parity unpinned)
 PERIODIC, OUTFLOW = 0, 1
 
 
@@ -145,6 +145,14 @@ class CpuLib:
         """Builder-authored HLLC restatement (no reference counterpart; parity unpinned)."""
         f = np.zeros(5)
         self._rc(self._fn("hllc_flux")(_p(np.ascontiguousarray(ul, float)),
+                                       _p(np.ascontiguousarray(ur, float)), axis,
+                                       C.c_double(gamma), _p(f)))
+        return f
+
+    def hlli_flux(self, ul, ur, axis, gamma=1.4):
+        """Builder-authored HLLI restatement (no reference counterpart; parity unpinned)."""
+        f = np.zeros(5)
+        self._rc(self._fn("hlli_flux")(_p(np.ascontiguousarray(ul, float)),
                                        _p(np.ascontiguousarray(ur, float)), axis,
                                        C.c_double(gamma), _p(f)))
         return f

@@ -62,7 +62,8 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
     switch (solver) {
         case 0: return launch_one<O3, 0, RK>(a, st);
         case 1: return launch_one<O3, 1, RK>(a, st);
-        default: return launch_one<O3, 2, RK>(a, st);  // HLLC (extension)
+        case 2: return launch_one<O3, 2, RK>(a, st);  // HLLC (extension)
+        default: return launch_one<O3, 3, RK>(a, st);  // HLLI (extension)
     }
 }
 

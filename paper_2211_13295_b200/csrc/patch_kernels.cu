@@ -461,6 +461,8 @@ int d_flux(const hc_geom& g, int modes, const double* m, int axis, double gamma,
     HC_FLUX_CASE(0, 1, true) HC_FLUX_CASE(1, 1, true) HC_FLUX_CASE(2, 1, true)
     HC_FLUX_CASE(0, 2, false) HC_FLUX_CASE(1, 2, false) HC_FLUX_CASE(2, 2, false)
     HC_FLUX_CASE(0, 2, true) HC_FLUX_CASE(1, 2, true) HC_FLUX_CASE(2, 2, true)
+    HC_FLUX_CASE(0, 3, false) HC_FLUX_CASE(1, 3, false) HC_FLUX_CASE(2, 3, false)
+    HC_FLUX_CASE(0, 3, true) HC_FLUX_CASE(1, 3, true) HC_FLUX_CASE(2, 3, true)
 #undef HC_FLUX_CASE
     set_error(HC_INVALID, "bad axis/solver/modes");
     return HC_INVALID;

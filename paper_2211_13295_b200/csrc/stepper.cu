@@ -220,7 +220,7 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     }
     int rc = validate_geom(g, p->order);
     if (rc) return rc;
-    if (p->solver != HC_RUSANOV && p->solver != HC_HLL && p->solver != HC_HLLC) {
+    if (p->solver < HC_RUSANOV || p->solver > HC_HLLI) {
         set_error(HC_INVALID, "unknown riemann solver");
         return HC_INVALID;
     }

@@ -23,7 +23,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libhydro_cuda.so")
 
 NVAR = 5
-RUSANOV, HLL, HLLC = 0, 1, 2  # HLLC: extension (no reference counterpart)
+RUSANOV, HLL, HLLC, HLLI = 0, 1, 2, 3  # HLLC, HLLI: extensions (no reference counterpart)
 PERIODIC, OUTFLOW = 0, 1
 HC_OK, HC_UNPHYSICAL, HC_INVALID, HC_CUDA = 0, 1, 2, 3
 

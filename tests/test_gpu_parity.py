@@ -58,7 +58,7 @@ def test_every_kernel_bitwise(api, orc, order):
     api.predict_patch(g, M, mg, 0.004)
     orc.predict_patch(go, M, mo, 0.004)
     assert same(mg, mo)
-    for solver in (hydro.RUSANOV, hydro.HLL, hydro.HLLC):
+    for solver in (hydro.RUSANOV, hydro.HLL, hydro.HLLC, hydro.HLLI):
         fg, fo = hydro.zeros_faces(g), po.zeros_faces(go)
         for ax in range(3):
             api.make_flux_axis(g, M, mg, ax, solver, fg[ax])
@@ -136,6 +136,8 @@ STEPPER_CASES = [
     # HLLC: extension without a reference counterpart, pinned to the C restatement
     (3, hydro.HLLC, hydro.PERIODIC, (20, 18, 16), "vortex", 4),
     (2, hydro.HLLC, hydro.OUTFLOW, (40, 12, 9), "sod", 8),
+    (3, hydro.HLLI, hydro.PERIODIC, (20, 18, 16), "vortex", 4),
+    (2, hydro.HLLI, hydro.OUTFLOW, (40, 12, 9), "sod", 8),
 ]
 
 

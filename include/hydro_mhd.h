@@ -37,7 +37,7 @@ typedef struct {
     int order;      /* 2 (MC slopes) or 3 (WENO3 + cross terms) */
     double gamma;
     hc_limiter lim; /* as the Euler path: MC factors, WENO3 eps and linear weights */
-    int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis */
+    int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis; bc[2] = -1: z ghosts caller-filled */
     int device;
 } hc_mhd_params;
 
@@ -62,6 +62,20 @@ int hc_mhd_max_divb(hc_mhd* m, double* out);
 long hc_mhd_launches(hc_mhd* m);
 /* the cudaStream_t every call of this stepper runs on (for event timing) */
 int hc_mhd_stream(hc_mhd* m, void** stream);
+/* run every later call on `stream` (a cudaStream_t owned by the caller) */
+int hc_mhd_set_stream(hc_mhd* m, void* stream);
+
+/* Multi-GPU z-slab step (params.bc[2] = -1: the caller fills the z-ghost planes):
+ * (1) fill_ghosts (x/y), caller exchanges z halos, (2) compute (predictor .. update and the
+ * CFL estimate into the dt accumulator), caller all-reduces (MIN) the accumulator,
+ * (3) advance. */
+int hc_mhd_fill_ghosts(hc_mhd* m);
+int hc_mhd_compute(hc_mhd* m);
+int hc_mhd_advance(hc_mhd* m);
+/* device state pointer, doubles per variable array, doubles per z plane */
+int hc_mhd_state(hc_mhd* m, double** dptr, size_t* var_stride, size_t* plane_elems);
+/* device address of the step's dt_next accumulator (1 double) */
+int hc_mhd_dt_acc(hc_mhd* m, double** acc);
 
 #ifdef __cplusplus
 }

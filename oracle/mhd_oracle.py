@@ -79,6 +79,9 @@ def fill_ghosts(s, g: Geom, bc):
     for q in range(NM):
         idx = []
         for d in range(3):
+            if bc[d] is None or bc[d] < 0:  # caller-filled (z halos of a slab)
+                idx.append(np.arange(ext[d]))
+                continue
             lo, hi = g.gh, g.gh + g.n[d]
             if q >= 5 and q - 5 == d and bc[d] == OUTFLOW:
                 hi += 1
@@ -398,7 +401,9 @@ def update(s, F, E, g: Geom, dt):
 
 
 def cfl_dt(s, g: Geom, par: Params, cfl):
-    w = cell_vars(s, par.order == 3)
+    # each zone's own two faces (mean): no ghost face enters, so the estimate is the same
+    # under any domain decomposition
+    w = cell_vars(s, False)
     gh = g.gh
     act = (slice(gh, gh + g.n[2]), slice(gh, gh + g.n[1]), slice(gh, gh + g.n[0]))
     u = [x[act] for x in w]
@@ -422,6 +427,11 @@ def max_divb(s, g: Geom):
 def step(s, g: Geom, par: Params, dt, cfl):
     """one ADER-CT step in place; returns dt_next (the CFL min of the new state)"""
     fill_ghosts(s, g, par.bc)
+    return compute(s, g, par, dt, cfl)
+
+
+def compute(s, g: Geom, par: Params, dt, cfl):
+    """the step after the ghost fill (hc_mhd_compute): returns this domain's CFL min"""
     m = predict(s, g, par, dt)
     F = [face_fluxes(m, g, par, A) for A in range(3)]
     E = [edge_emf(m, g, par, C) for C in range(3)]

@@ -200,7 +200,7 @@ __global__ void k_mhd_ghosts(MArgs a) {
         for (int d = 0; d < 3; ++d) {
             int hi = b.gh + b.n[d];
             if (q >= 5 && q - 5 == d && a.bc[d] == HC_OUTFLOW) hi += 1;
-            src[d] = map_c(c[d], b.gh, hi, a.bc[d]);
+            src[d] = a.bc[d] < 0 ? c[d] : map_c(c[d], b.gh, hi, a.bc[d]);  // <0: caller fills
             ghost |= src[d] != c[d];
         }
         if (ghost) a.s[q * b.N + r] = a.s[q * b.N + at(b, src[2], src[1], src[0])];
@@ -466,9 +466,11 @@ __global__ void k_mhd_update(MArgs a) {
 // CFL estimate of a zone (eval_tstep_ptwise shape with the fast speed), exact min
 template <bool O3>
 __device__ __forceinline__ double zone_dt(const MArgs& a, size_t o, double cfl, Fault& f) {
+    // the zone's own two faces only (mean): the estimate must not read ghost faces, which
+    // are stale after the update, so it is identical under any domain decomposition
     double u[NM];
 #pragma unroll
-    for (int q = 0; q < NM; ++q) u[q] = cellvar<O3>(a, q, o);
+    for (int q = 0; q < NM; ++q) u[q] = cellvar<false>(a, q, o);
     MPrim p = mhd_prim(u, a.gamma, f);
     const double sx = fabs(p.u[0]) + fast_speed<0>(u, p, a.gamma);
     const double sy = fabs(p.u[1]) + fast_speed<1>(u, p, a.gamma);
@@ -564,6 +566,7 @@ struct hc_mhd {
     StepCtl* ctl = nullptr;
     ErrBlock* eb = nullptr;
     cudaStream_t st = nullptr;
+    bool own_stream = true;
     long launches = 0;
     double cfl = 0.4;
 };
@@ -593,12 +596,19 @@ MArgs margs(const hc_mhd* m) {
 
 using ct::blocks;
 
-int launch_step(hc_mhd* m) {
+int launch_ghosts(hc_mhd* m) {
+    MArgs a = margs(m);
+    k_mhd_ghosts<<<blocks(m->b.N, 256), 256, 0, m->st>>>(a);
+    m->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd ghost launch");
+}
+
+int launch_compute(hc_mhd* m) {
     MArgs a = margs(m);
     const Box& b = m->b;
     const bool o3 = m->p.order == 3;
     const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
-    k_mhd_ghosts<<<blocks(b.N, 256), 256, 0, m->st>>>(a);
     if (o3) k_mhd_cellb<true><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
     else k_mhd_cellb<false><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
     if (o3) k_mhd_predict<true><<<blocks(ring, 128), 128, 0, m->st>>>(a);
@@ -627,14 +637,26 @@ int launch_step(hc_mhd* m) {
     const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
     k_mhd_update<<<blocks(up, 256), 256, 0, m->st>>>(a);
     const size_t act = size_t(b.n[0]) * b.n[1] * b.n[2];
-    // CFL estimate of the updated state: its ghosts are stale, but zone_dt reads only the
-    // zone's own faces, which are all active
+    // CFL estimate of the updated state from each zone's own faces (ghosts are stale)
     if (o3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
     else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
-    k_mhd_advance<<<1, 1, 0, m->st>>>(m->ctl, m->eb);
-    m->launches += 12;
+    m->launches += 10;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd step launch");
+}
+
+int launch_advance(hc_mhd* m) {
+    k_mhd_advance<<<1, 1, 0, m->st>>>(m->ctl, m->eb);
+    m->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd advance launch");
+}
+
+int launch_step(hc_mhd* m) {
+    int rc = launch_ghosts(m);
+    if (!rc) rc = launch_compute(m);
+    if (!rc) rc = launch_advance(m);
+    return rc;
 }
 
 }  // namespace
@@ -653,8 +675,8 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
         return HC_INVALID;
     }
     for (int d = 0; d < 3; ++d)
-        if (p->bc[d] != HC_PERIODIC && p->bc[d] != HC_OUTFLOW) {
-            set_error(HC_INVALID, "mhd: boundary kind must be periodic or outflow");
+        if (p->bc[d] != HC_PERIODIC && p->bc[d] != HC_OUTFLOW && !(d == 2 && p->bc[d] == -1)) {
+            set_error(HC_INVALID, "mhd: boundary kind must be periodic or outflow (z: or -1)");
             return HC_INVALID;
         }
     hc_mhd* m = new (std::nothrow) hc_mhd;
@@ -713,7 +735,7 @@ int hc_mhd_destroy(hc_mhd* m) {
     cudaFree(m->scratch);
     cudaFree(m->ctl);
     cudaFree(m->eb);
-    if (m->st) cudaStreamDestroy(m->st);
+    if (m->st && m->own_stream) cudaStreamDestroy(m->st);
     delete m;
     return HC_OK;
 }
@@ -804,6 +826,42 @@ long hc_mhd_launches(hc_mhd* m) { return m ? m->launches : 0; }
 
 int hc_mhd_stream(hc_mhd* m, void** stream) {
     *stream = m->st;
+    return HC_OK;
+}
+
+int hc_mhd_set_stream(hc_mhd* m, void* stream) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    if (m->own_stream) HC_CUDA(cudaStreamDestroy(m->st));
+    m->own_stream = false;
+    m->st = static_cast<cudaStream_t>(stream);
+    return HC_OK;
+}
+
+int hc_mhd_fill_ghosts(hc_mhd* m) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    return launch_ghosts(m);
+}
+
+int hc_mhd_compute(hc_mhd* m) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    return launch_compute(m);
+}
+
+int hc_mhd_advance(hc_mhd* m) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    return launch_advance(m);
+}
+
+int hc_mhd_state(hc_mhd* m, double** dptr, size_t* var_stride, size_t* plane_elems) {
+    *dptr = m->s;
+    *var_stride = m->b.N;
+    *plane_elems = size_t(m->b.P) * m->b.Q;
+    return HC_OK;
+}
+
+int hc_mhd_dt_acc(hc_mhd* m, double** acc) {
+    *acc = &m->ctl->acc;
     return HC_OK;
 }
 

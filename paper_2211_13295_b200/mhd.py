@@ -50,7 +50,7 @@ def _lib():
     if not getattr(lib, "_mhd_typed", False):
         lib.hc_mhd_launches.restype = C.c_long
         lib.hc_mhd_launches.argtypes = [C.c_void_p]
-        for n in ("hc_mhd_destroy",):
+        for n in ("hc_mhd_destroy", "hc_mhd_fill_ghosts", "hc_mhd_compute", "hc_mhd_advance"):
             getattr(lib, n).argtypes = [C.c_void_p]
         lib.hc_mhd_step.argtypes = [C.c_void_p, C.c_int]
         lib._mhd_typed = True
@@ -113,6 +113,28 @@ class MhdStepper:
     @property
     def launches(self):
         return self.lib.hc_mhd_launches(self.h)
+
+    def set_stream(self, ptr):
+        _check(self.lib.hc_mhd_set_stream(self.h, C.c_void_p(ptr)))
+
+    def fill_ghosts(self):
+        _check(self.lib.hc_mhd_fill_ghosts(self.h))
+
+    def compute(self):
+        _check(self.lib.hc_mhd_compute(self.h))
+
+    def advance(self):
+        _check(self.lib.hc_mhd_advance(self.h))
+
+    def state_ptr(self):
+        p, vs, pe = C.c_void_p(), C.c_size_t(), C.c_size_t()
+        _check(self.lib.hc_mhd_state(self.h, C.byref(p), C.byref(vs), C.byref(pe)))
+        return p.value, vs.value, pe.value
+
+    def dt_acc_ptr(self):
+        p = C.c_void_p()
+        _check(self.lib.hc_mhd_dt_acc(self.h, C.byref(p)))
+        return p.value
 
     @property
     def stream_ptr(self):

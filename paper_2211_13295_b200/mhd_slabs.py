@@ -1,0 +1,116 @@
+"""mhd_slabs -- z-slab decomposition of the MHD (CT) step over the GPUs of a node, one process
+per GPU (BASELINE.json config 5: 512^3 MHD on 2/4/8 B200s).
+
+Every rank owns nz_global / world contiguous z planes of a periodic nx x ny x nz_global mesh
+in one ``mhd.MhdStepper`` with caller-filled z ghosts (params.bc[2] = -1). Per step:
+
+  1. x/y ghosts of the slab on the device (hc_mhd_fill_ghosts),
+  2. z halo exchange with the two neighbours: each of the 8 variable arrays (5 cell averages,
+     3 face fields) sends its planes [gh, 2gh+1) down -- they are the lower rank's top ghost
+     planes, the +1 being the shared z-face plane on top of that slab -- and its planes
+     [nloc, nloc+gh) up -- the upper rank's bottom ghosts; whole padded planes (x/y ghosts
+     included), one grouped NCCL send/recv per side,
+  3. the step (hc_mhd_compute), the all-reduce (MIN) of the dt_next accumulator (exact), then
+     the device t/dt hand-off (hc_mhd_advance).
+
+The z-face plane shared by two slabs is updated by both ranks from identical inputs, so the
+decomposed run is bit-identical to the single-domain run (tests/test_mhd_slabs_gloo.py runs
+the exchange over gloo with the numpy restatement as the per-slab compute). Periodic z only.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import mhd
+
+
+def slab_range(nz_global: int, rank: int, world: int):
+    if nz_global % world:
+        raise ValueError("patch split must divide the mesh evenly")
+    nloc = nz_global // world
+    if nloc < 4:
+        raise ValueError("patch must have at least 4 zones per axis")
+    return rank * nloc, (rank + 1) * nloc
+
+
+def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=None):
+    """planes: torch tensor [NVAR, nloc + 2 gh + 1, plane_elems] viewing the slab's state
+    (CPU or CUDA). Fills the z ghosts of every variable from the periodic z neighbours."""
+    import torch
+    import torch.distributed as dist
+
+    lo_send = planes[:, gh:2 * gh + 1]            # -> lower rank's [gh+nloc, 2gh+nloc+1)
+    hi_send = planes[:, nloc:nloc + gh]           # -> upper rank's [0, gh)
+    lo_ghost = planes[:, 0:gh]
+    hi_ghost = planes[:, gh + nloc:2 * gh + nloc + 1]
+    if world == 1:
+        lo_ghost.copy_(hi_send.clone())
+        hi_ghost.copy_(lo_send.clone())
+        return
+    below, above = (rank - 1) % world, (rank + 1) % world
+    rb = torch.empty_like(lo_ghost)
+    ra = torch.empty_like(hi_ghost)
+    ops = [dist.P2POp(dist.isend, lo_send.contiguous(), below, group),
+           dist.P2POp(dist.irecv, ra, above, group),
+           dist.P2POp(dist.isend, hi_send.contiguous(), above, group),
+           dist.P2POp(dist.irecv, rb, below, group)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    lo_ghost.copy_(rb)
+    hi_ghost.copy_(ra)
+
+
+class MhdSlabDomain:
+    """One rank's slab of a periodic nx x ny x nz_global MHD mesh on [0,1]^2 x [0, nz dz]."""
+
+    def __init__(self, nx, ny, nz_global, order, rank=0, world=1, device=0):
+        import torch
+        self.rank, self.world, self.order = rank, world, order
+        self.z0, self.z1 = slab_range(nz_global, rank, world)
+        self.nloc = self.z1 - self.z0
+        d = 1.0 / nx
+        g = mhd.make_geometry(nx, ny, self.nloc, order, (0.0, 0.0, self.z0 * d),
+                              (1.0, ny * d, self.z1 * d))
+        self.geom = g
+        self.st = mhd.MhdStepper(g, mhd.make_params(order, bc=(0, 0, -1), device=device))
+        self.stream = torch.cuda.Stream(device=device)
+        self.st.set_stream(self.stream.cuda_stream)
+
+    def initial_state(self):
+        return mhd.orszag_tang(self.geom, self.order)
+
+    def _planes(self):
+        import torch
+        from .slabs import _CudaArray
+        ptr, vs, pe = self.st.state_ptr()
+        g = self.geom
+        return torch.as_tensor(_CudaArray(ptr, (mhd.NM, g.mz + 1, pe)), device="cuda")
+
+    def _acc(self):
+        import torch
+        from .slabs import _CudaArray
+        return torch.as_tensor(_CudaArray(self.st.dt_acc_ptr(), (1,)), device="cuda")
+
+    def initial_dt(self, cfl):
+        dt = self.st.cfl_dt(cfl)
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            dt = float(t.item())
+        return dt
+
+    def step(self):
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.st.fill_ghosts()
+            exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank, self.world)
+            self.st.compute()
+            if self.world > 1:
+                import torch.distributed as dist
+                dist.all_reduce(self._acc(), op=dist.ReduceOp.MIN)
+            self.st.advance()
+
+    def close(self):
+        self.st.close()

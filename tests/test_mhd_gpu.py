@@ -134,3 +134,32 @@ def test_mhd_rejects_small_ghost():
     g = hydro.make_geometry(8, 8, 8, 3, (0, 0, 0), (1, 1, 1))  # Euler ghost width 3
     with pytest.raises(ValueError):
         mhd.MhdStepper(g, mhd.make_params(3))
+
+
+def test_mhd_slab_path_single_rank_matches_stepper():
+    """the multi-GPU step split (fill_ghosts -> z exchange -> compute -> advance) with one
+    rank equals the periodic single-domain stepper bit for bit"""
+    import torch
+    from paper_2211_13295_b200 import mhd_slabs
+    n, order = 16, 3
+    dom = mhd_slabs.MhdSlabDomain(n, n, n, order)
+    s0 = dom.initial_state()
+    dom.st.upload(s0)
+    dt0 = dom.initial_dt(0.4)
+    dom.st.set_time(0.0, dt0, 0.4)
+    for _ in range(3):
+        dom.step()
+    torch.cuda.synchronize()
+    a = active(dom.st.download(), dom.geom)
+    t1 = dom.st.sync()
+    dom.close()
+    g = mhd.make_geometry(n, n, n, order, (0, 0, 0), (1, 1, 1))
+    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st.upload(mhd.orszag_tang(g, order))
+    assert st.cfl_dt(0.4) == dt0
+    st.set_time(0.0, dt0, 0.4)
+    st.step(3)
+    b = active(st.download(), g)
+    assert (bits(a) == bits(b)).all()
+    assert st.sync() == t1
+    st.close()

@@ -313,6 +313,70 @@ def bench_mhd(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------- CED (extension)
+
+
+def bench_ced(args):
+    """BASELINE.json configs[3]: 3D CED with stiff conductivity, WENO-ADER O3, 256^3: a plane
+    wave crossing a conducting slab with sigma dt = 1e3 (stiff; the exponential step has no
+    dt restriction). Extension without a reference counterpart (parity unpinned; checked
+    against oracle/ced_oracle.py)."""
+    import numpy as np
+    import torch
+
+    from paper_2211_13295_b200 import ced
+    n, order = args.n, args.order
+    torch.cuda.set_device(0)
+    g = ced.make_geometry(n, n, n, order, (0, 0, 0), (1, 1, 1))
+    st = ced.CedStepper(g, ced.make_params(order))
+    s0 = ced.plane_wave(g)
+    dt = st.cfl_dt(0.4)
+    x = (np.arange(g.mx + 1) - g.ghost + 0.5) * g.dx
+    sigma = np.zeros((g.mz + 1, g.my + 1, g.mx + 1))
+    sigma[:, :, (x > 0.4) & (x < 0.6)] = 1e3 / dt
+    st.upload(s0, sigma)
+    st.set_time(0.0, dt)
+    stream = torch.cuda.ExternalStream(st.stream_ptr)
+    st.step(args.warmup)
+    torch.cuda.synchronize()
+    l0 = st.launches
+    with ClockSampler(0) as clocks:
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = st.launches - l0
+    t, _, done = st.sync()
+    zones = n ** 3
+    divb, divd = st.max_div()
+    bytes_per_zone = 1650.0  # ideal one-pass traffic of the unfused O3 design (DESIGN.md 8)
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = bytes_per_zone * zones / (ms / args.steps * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": zones * args.steps / (ms * 1e-3) / 1e6, "unit": UNIT,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (plane wave, conducting slab sigma dt = 1e3)",
+        "config": {"workload": f"C4: 3D CED with stiff conductivity {n}^3, WENO-ADER O{order}, "
+                               "CT for D and B, 2D upwind edge solver, exponential conduction "
+                               "step (configs[3]; extension, no reference counterpart)",
+                   "n": n, "order": order, "build": "bit-exact (--fmad=false)",
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "bytes_per_zone": bytes_per_zone,
+                     "note": "whole step (8 kernels) against the ideal one-pass traffic"},
+        "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks.summary(),
+        "final": {"t": t, "steps_done": done, "max_divb": divb, "max_divd": divd},
+    }
+    st.close()
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------- our arm
 
 
@@ -330,13 +394,20 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="euler", choices=["euler", "mhd"],
+    ap.add_argument("--workload", default="euler", choices=["euler", "mhd", "ced"],
                     help="euler: configs[1] (the headline); mhd: configs[2], 3D Orszag-Tang "
                          "with CT + the multidimensional Riemann solver (extension, 384^3)")
     args = ap.parse_args()
     args.fast = not args.exact
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
+    if args.workload == "ced":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "the reference has no CED (SPEC.md:8); nothing to run"}))
+            return
+        bench_ced(args)
+        return
     if args.workload == "mhd":
         if args.impl == "reference":
             print(json.dumps({"impl": "reference", "unavailable":

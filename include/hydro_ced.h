@@ -59,6 +59,8 @@ int hc_ced_sync(hc_ced* m, double* t, double* dt, long* steps_done);
 /* max over active zones of |div B| * min(d) and |div D| * min(d) */
 int hc_ced_max_div(hc_ced* m, double* divb, double* divd);
 long hc_ced_launches(hc_ced* m);
+/* the cudaStream_t every call of this stepper runs on (for event timing) */
+int hc_ced_stream(hc_ced* m, void** stream);
 
 #ifdef __cplusplus
 }

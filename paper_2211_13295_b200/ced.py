@@ -123,6 +123,12 @@ class CedStepper:
     def launches(self):
         return self.lib.hc_ced_launches(self.h)
 
+    @property
+    def stream_ptr(self):
+        v = C.c_void_p()
+        _check(self.lib.hc_ced_stream(self.h, C.byref(v)))
+        return v.value or 0
+
     def run(self, cfl, t_final, chunk=64):
         dt = self.cfl_dt(cfl)
         self.set_time(0.0, dt, t_final)

@@ -544,4 +544,9 @@ int hc_ced_max_div(hc_ced* m, double* divb, double* divd) {
 
 long hc_ced_launches(hc_ced* m) { return m ? m->launches : 0; }
 
+int hc_ced_stream(hc_ced* m, void** stream) {
+    *stream = m->st;
+    return HC_OK;
+}
+
 }  // extern "C"

@@ -68,19 +68,24 @@ struct MPrim {
     double rho, u[3], p, b2, inv_rho;
 };
 
-// conserved -> primitive; p = (gamma-1)(E - rho v^2/2 - B^2/2)
+// conserved -> primitive; p = (gamma-1)(E - rho v^2/2 - B^2/2). FAST = 1: the branch-free
+// bit-exact division of pointwise.cuh (flags instead of branches; callers re-run in careful
+// mode when f.redo()), FAST = 0: IEEE division and first-fault capture.
+template <int FAST = 0>
 __device__ __forceinline__ MPrim mhd_prim(const double* c, double gamma, Fault& f) {
     MPrim q;
     q.rho = c[0];
-    if (!(c[0] > 0.0)) f.set(1, c[0]);
-    q.inv_rho = 1.0 / c[0];
+    if (FAST) f.bad |= !(c[0] > 0.0);
+    else if (!(c[0] > 0.0)) f.set(1, c[0]);
+    q.inv_rho = ddiv<FAST>(1.0, c[0], f);
     q.u[0] = c[1] * q.inv_rho;
     q.u[1] = c[2] * q.inv_rho;
     q.u[2] = c[3] * q.inv_rho;
     q.b2 = c[5] * c[5] + c[6] * c[6] + c[7] * c[7];
     q.p = (gamma - 1.0) *
           (c[4] - 0.5 * (c[1] * q.u[0] + c[2] * q.u[1] + c[3] * q.u[2]) - 0.5 * q.b2);
-    if (!(q.p > 0.0)) f.set(2, q.p);
+    if (FAST) f.bad |= !(q.p > 0.0);
+    else if (!(q.p > 0.0)) f.set(2, q.p);
     return q;
 }
 
@@ -151,7 +156,7 @@ struct FaceSmem {
 };
 
 // predictor.cpp:12-22 flux_divergence with the MHD flux; optional shift h added to every face
-template <bool SHIFT>
+template <bool SHIFT, int FAST>
 __device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const double* h,
                                                const double* id, double gamma, double* div,
                                                Fault& flt) {
@@ -163,7 +168,7 @@ __device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const doubl
             a[q] = SHIFT ? face(2 * A, q) + h[q] : face(2 * A, q);
             b[q] = SHIFT ? face(2 * A + 1, q) + h[q] : face(2 * A + 1, q);
         }
-        MPrim qa = mhd_prim(a, gamma, flt), qb = mhd_prim(b, gamma, flt);
+        MPrim qa = mhd_prim<FAST>(a, gamma, flt), qb = mhd_prim<FAST>(b, gamma, flt);
         if (A == 0) {
             mhd_flux<0>(a, qa, fa);
             mhd_flux<0>(b, qb, fb);
@@ -235,28 +240,18 @@ __global__ void k_mhd_cellb(MArgs a) {
 
 // the 8 cell-centred variables as the predictor reads them
 __device__ __forceinline__ double wvar(const MArgs& a, int q, size_t o) {
-    return q < 5 ? a.s[size_t(q) * a.b.N + o] : a.bcell[size_t(q - 5) * a.b.N + o];
+    return q < 5 ? __ldg(a.s + size_t(q) * a.b.N + o) : __ldg(a.bcell + size_t(q - 5) * a.b.N + o);
 }
 
-template <bool O3>
-__global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
-    if (a.ctl->done) return;
+// One ring zone: reconstruction of the 8 cell variables (modes written), ADER predictor,
+// half-time mean written. FAST = 1 is the branch-free bit-exact division; the caller re-runs
+// the zone with FAST = 0 when a fast-path flag is raised (identical bits either way).
+template <bool O3, int FAST>
+__device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const FaceSmem& face,
+                                             double dt, Fault& f) {
     const Box& b = a.b;
-    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
-    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
-    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (r >= cnt) return;
-    // ring zone (active coords -1..n) -> storage
-    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
-              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
-    const size_t o = at(b, k, j, i);
     const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
-    const double dt = a.ctl->dt;
-    __shared__ double sface[6 * NM * 128];
-    const FaceSmem face{sface, int(threadIdx.x)};
     double* mo = a.modes;
-    Fault wf;  // (WENO3 in careful mode never raises)
-    wf.clear();
 #pragma unroll 1
     for (int q = 0; q < NM; ++q) {
         const double u0 = wvar(a, q, o);
@@ -270,7 +265,7 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
             } else {
                 const double upp = wvar(a, q, o + 2 * st[d]);
                 const double umm = wvar(a, q, o - 2 * st[d]);
-                weno3<0>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], wf);
+                weno3<FAST>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], f);
             }
         }
 #pragma unroll
@@ -292,23 +287,53 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
         }
     }
     // ADER predictor (predictor.cpp:26-60): tau = -dt div F(face states); O3: one Picard pass
-    Fault f;
-    f.clear();
     double div[NM], tau[NM];
-    mhd_divergence<false>(face, nullptr, a.id, a.gamma, div, f);
+    mhd_divergence<false, FAST>(face, nullptr, a.id, a.gamma, div, f);
 #pragma unroll
     for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
     if (O3) {
         double h[NM];
 #pragma unroll
         for (int q = 0; q < NM; ++q) h[q] = 0.5 * tau[q];
-        mhd_divergence<true>(face, h, a.id, a.gamma, div, f);
+        mhd_divergence<true, FAST>(face, h, a.id, a.gamma, div, f);
 #pragma unroll
         for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
     }
-    if (f.code) record_fault(a.eb, ST_PREDICT, f, i - b.gh, j - b.gh, k - b.gh, 0);
 #pragma unroll
     for (int q = 0; q < NM; ++q) mo[size_t(q) * b.N + o] = wvar(a, q, o) + 0.5 * tau[q];
+}
+
+template <bool O3>
+__device__ __noinline__ Fault predict_zone_careful(const MArgs& a, size_t o, FaceSmem face,
+                                                   double dt) {
+    Fault f;
+    f.clear();
+    predict_zone<O3, 0>(a, o, face, dt, f);
+    return f;
+}
+
+template <bool O3>
+__global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    // ring zone (active coords -1..n) -> storage
+    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
+              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
+    const size_t o = at(b, k, j, i);
+    const double dt = a.ctl->dt;
+    __shared__ double sface[6 * NM * 128];
+    const FaceSmem face{sface, int(threadIdx.x)};
+    Fault f;
+    f.clear();
+    predict_zone<O3, 1>(a, o, face, dt, f);
+    if (f.redo()) {
+        Fault c = predict_zone_careful<O3>(a, o, face, dt);
+        if (c.code) record_fault(a.eb, ST_PREDICT, c, i - b.gh, j - b.gh, k - b.gh, 0);
+    }
 }
 
 // half-time face-average state of the zone at o on its side `side` (+1 / -1) along axis A

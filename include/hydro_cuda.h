@@ -216,6 +216,11 @@ int hc_stepper_dt_ptrs(hc_stepper* s, double** dt_next_dev, double** dt_dev);
  * halos; (2) run the fused kernel; caller then all-reduces dt_next; (3) advance t/dt. */
 int hc_stepper_fill_ghosts(hc_stepper* s);
 int hc_stepper_compute(hc_stepper* s);
+/* The fused launch over active z planes [kz_first, kz_last) only (last = 1 closes the step or
+ * RK stage). Lets a z-slab driver compute the interior planes [G, nz-G) -- whose stencils
+ * never touch the z-ghost planes, G = order - 1 + 1 -- while the halo exchange is in flight,
+ * then the two boundary ranges. */
+int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last);
 int hc_stepper_advance(hc_stepper* s);
 /* fused launches per step: 1 (ADER), 2 or 3 (RK); a multi-GPU step repeats fill_ghosts +
  * halo exchange + compute per stage, then all-reduce + advance */

@@ -419,11 +419,23 @@ static const double kSsp3[3][2] = {{0.0, 1.0}, {0.75, 0.25}, {1.0 / 3.0, 2.0 / 3
 int hc_stepper_stages(hc_stepper* s) { return s->o.integrator == 0 ? 1 : s->o.integrator; }
 
 // One fused launch: the ADER step, or the next Runge-Kutta stage.
-int hc_stepper_compute(hc_stepper* s) {
+int hc_stepper_compute(hc_stepper* s) { return hc_stepper_compute_range(s, 0, s->g.nz, 1); }
+
+// The fused launch over active planes [kz_first, kz_last) only; `last` = 1 closes the step /
+// stage (buffer and stage bookkeeping). Ranges of one step may run in any order: each reads
+// the input buffer, writes its own planes of the output buffer and min-reduces into the
+// same dt accumulator.
+int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last) {
     int rc = set_dev(s);
     if (rc) return rc;
+    if (kz_first < 0 || kz_last > s->g.nz || kz_first > kz_last) {
+        set_error(HC_INVALID, "compute range outside the active planes");
+        return HC_INVALID;
+    }
     FusedArgs a = fused_args(s);
     a.cfl = s->cfl;
+    a.kz_first = kz_first;
+    a.kz_last = kz_last;
     const bool rk = s->o.integrator != 0;
     if (rk) {
         const int ns = s->o.integrator, k = s->stage;
@@ -435,10 +447,13 @@ int hc_stepper_compute(hc_stepper* s) {
         a.rk_b = ab[1];
         a.want_dt = k == ns - 1;
     }
-    rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st)
-                    : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st);
-    if (rc) return rc;
-    s->launches++;
+    if (kz_last > kz_first) {
+        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st)
+                        : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st);
+        if (rc) return rc;
+        s->launches++;
+    }
+    if (!last) return HC_OK;
     if (rk)
         s->stage = (s->stage + 1) % s->o.integrator;
     else

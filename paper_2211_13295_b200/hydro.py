@@ -367,6 +367,11 @@ class Stepper:
     def compute(self):
         _check(self.lib.hc_stepper_compute(self.h))
 
+    def compute_range(self, kz_first, kz_last, last):
+        """fused launch over active planes [kz_first, kz_last); last closes the step/stage"""
+        _check(self.lib.hc_stepper_compute_range(self.h, int(kz_first), int(kz_last),
+                                                 int(bool(last))))
+
     def advance(self):
         _check(self.lib.hc_stepper_advance(self.h))
 

@@ -100,8 +100,11 @@ class SlabDomain:
     """One rank's slab of an ``nx x ny x nz_global`` mesh on [-5,5]^2 x [-5, -5 + nz*dz]."""
 
     def __init__(self, nx, ny, nz_global, order, rank=0, world=1, device=0, exact=True,
-                 solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER):
+                 solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER, overlap=None):
         self.rank, self.world, self.order = rank, world, order
+        # overlap: z halos by the (local, at N=1) exchange, interior planes computed meanwhile
+        overlap = world > 1 if overlap is None else overlap
+        self.overlap = overlap
         self.periodic = bc == PERIODIC
         self.z0, self.z1 = slab_range(nz_global, rank, world)
         self.nloc = self.z1 - self.z0
@@ -115,11 +118,13 @@ class SlabDomain:
         self.geom = g
         self.params = hydro.make_params(order, solver)
         self.api = hydro.HostApi()
-        self.st = hydro.Stepper(g, self.params, bc=(bc, bc, bc if world == 1 else None),
+        self.st = hydro.Stepper(g, self.params, bc=(bc, bc, bc if world == 1 and not overlap
+                                                     else None),
                                 exact=exact, device=device, integrator=integrator)
         # every device op of the step (our kernels, NCCL, events) is ordered on one stream
         import torch
         self.stream = torch.cuda.Stream(device=device)
+        self.comm = torch.cuda.Stream(device=device)  # halo exchange, overlapped
         self.st.set_stream(self.stream.cuda_stream)
 
     # ---- host side
@@ -182,22 +187,43 @@ class SlabDomain:
         return torch.as_tensor(_CudaArray(acc, (1,)), device="cuda")
 
     # ---- one step
-    def step(self, kernel_events=None):
-        """One ADER step; kernel_events=(start, end) bracket the fused kernel."""
+    def step(self, kernel_events=None, overlap=None):  # noqa: C901
+        """One ADER step; kernel_events=(start, end) bracket the fused kernel.
+
+        overlap (default: on for N>1): the interior planes [G, nloc-G), whose stencils never
+        reach the z-ghost planes, are computed while the halo exchange runs on a second
+        stream; the two boundary ranges follow once the halos have landed."""
         import torch
         s = self.stream
-        if self.world == 1 and kernel_events is None:
+        if overlap is None:
+            overlap = self.overlap
+        if self.world == 1 and kernel_events is None and not overlap:
             self.st.step(1)
             return
+        G = self.order  # stencil halo R + 1 (R = 1 at order 2, 2 at order 3)
         with torch.cuda.stream(s):
             for k in range(self.st.stages):  # 1 (ADER) or 2/3 RK stages
                 self.st.fill_ghosts()
-                if self.world > 1:
-                    exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank,
-                                     self.world, self.periodic)
                 if kernel_events is not None and k == 0:
                     kernel_events[0].record(s)
-                self.st.compute()
+                if overlap and self.nloc > 2 * G:
+                    ready = torch.cuda.Event()
+                    ready.record(s)
+                    self.comm.wait_event(ready)
+                    with torch.cuda.stream(self.comm):
+                        exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank,
+                                         self.world, self.periodic)
+                        halos = torch.cuda.Event()
+                        halos.record(self.comm)
+                    self.st.compute_range(G, self.nloc - G, False)  # overlaps the exchange
+                    s.wait_event(halos)
+                    self.st.compute_range(0, G, False)
+                    self.st.compute_range(self.nloc - G, self.nloc, True)
+                else:
+                    if self.world > 1:
+                        exchange_z_halos(self._planes(), self.geom.ghost, self.nloc,
+                                         self.rank, self.world, self.periodic)
+                    self.st.compute()
             if kernel_events is not None:
                 kernel_events[1].record(s)
             if self.world > 1:

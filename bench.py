@@ -517,11 +517,13 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     e_ms = dom.max_over_ranks(e0.elapsed_time(e1))
-    nbytes = host.nbytes
+    # world 1: step_host moves only the active zones (40 B each) both ways; N>1: whole slabs
+    nbytes = zones_local * 40 if world == 1 else host.nbytes
     e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": (nbytes + 16) * world,
            "steps": args.e2e_steps,
-           "api": ("hc_stepper_step_host (H2D of U_skinny, fused step, D2H, pipelined in "
+           "api": ("hc_stepper_step_host (H2D of the active U_skinny zones, fused step, D2H, "
+                   "pipelined in "
                    f"{args.e2e_chunks} z-chunks) + hc_stepper_sync (dt_next)") if world == 1 else
                   "per rank: hc_stepper_upload + slab step (NCCL halos) + hc_stepper_download"}
 

@@ -199,8 +199,9 @@ int hc_stepper_download(hc_stepper* s, double* host_skinny);
 int hc_stepper_set_time(hc_stepper* s, double t, double dt, double cfl, double t_final);
 /* Enqueue n fused steps (no host sync). */
 int hc_stepper_step(hc_stepper* s, int n);
-/* One step end to end from HOST memory: H2D of host_in (U_skinny, ghosts included), the
- * fused step, D2H of the updated active planes into host_out (may equal host_in),
+/* One step end to end from HOST memory: H2D of the active zones of host_in (U_skinny
+ * layout; ghosts are filled on the device, never transferred), the fused step, D2H of the
+ * updated active zones into host_out (may equal host_in; its ghosts are left untouched),
  * pipelined over nchunks z-chunks on three streams so both PCIe directions overlap the
  * kernel. Returns after host_out is complete. */
 int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out, int nchunks);

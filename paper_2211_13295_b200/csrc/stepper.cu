@@ -498,6 +498,36 @@ static int copy_planes(hc_stepper* s, double* dev, double* host, int k_lo, int k
     return HC_OK;
 }
 
+// Copies the ACTIVE zones of storage planes [k_lo, k_hi) (clamped to the active planes)
+// between the host SkinnyState and the device state: one strided 3D copy, rows of nx zones.
+// Ghost zones are never transferred -- the device fills them (fill_planes).
+static int copy_active(hc_stepper* s, double* dev, double* host, int k_lo, int k_hi, bool up,
+                       cudaStream_t st) {
+    const SG& g = s->sg;
+    k_lo = std::max(k_lo, g.gh);
+    k_hi = std::min(k_hi, g.gh + g.nz);
+    if (k_hi <= k_lo) return HC_OK;
+    cudaMemcpy3DParms p = {};
+    const size_t row = size_t(g.mx) * NV * sizeof(double);
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, row, row, g.my);
+    cudaPitchedPtr dp = make_cudaPitchedPtr(dev, size_t(g.pitch) * sizeof(double), row, g.my_pad);
+    const cudaPos pos = make_cudaPos(size_t(g.gh) * NV * sizeof(double), g.gh, k_lo);
+    p.extent = make_cudaExtent(size_t(g.nx) * NV * sizeof(double), g.ny, k_hi - k_lo);
+    if (up) {
+        p.srcPtr = hp;
+        p.dstPtr = dp;
+        p.kind = cudaMemcpyHostToDevice;
+    } else {
+        p.srcPtr = dp;
+        p.dstPtr = hp;
+        p.kind = cudaMemcpyDeviceToHost;
+    }
+    p.srcPos = pos;
+    p.dstPos = pos;
+    HC_CUDA(cudaMemcpy3DAsync(&p, st));
+    return HC_OK;
+}
+
 // One ADER step end to end from host memory: H2D of U_skinny, ghost fill, fused update, D2H
 // of the updated active planes, pipelined over z-chunks on three streams so the two PCIe
 // directions and the kernel overlap (chunk c computes while c+1 uploads and c-1 downloads).
@@ -539,14 +569,17 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
     HC_CUDA(cudaEventRecord(ev_start, s->st));
     HC_CUDA(cudaStreamWaitEvent(s->s_h2d, ev_start, 0));
     HC_CUDA(cudaStreamWaitEvent(s->s_d2h, ev_start, 0));
-    // the top active planes first: they feed the periodic bottom ghosts of chunk 0
-    if ((rc = copy_planes(s, in, hin, g.gh + g.nz - G, g.gh + g.nz, true, s->s_h2d))) return rc;
+    // Only active zones cross PCIe (ghosts are filled on the device): the top G active planes
+    // first -- they feed the periodic bottom ghosts of chunk 0 -- then chunk by chunk.
+    const int wrap_lo = g.gh + g.nz - G;
+    if ((rc = copy_active(s, in, hin, wrap_lo, g.gh + g.nz, true, s->s_h2d))) return rc;
     HC_CUDA(cudaEventRecord(ev_wrap, s->s_h2d));
-    int uploaded = 0;  // storage planes [0, uploaded) are on the device
+    int uploaded = 0;  // storage planes [0, uploaded) are on the device (ghosts once filled)
     for (int c = 0; c < nchunks; ++c) {
         const int c0 = int((long(g.nz) * c) / nchunks), c1 = int((long(g.nz) * (c + 1)) / nchunks);
         const int hi = (c == nchunks - 1) ? g.mz : std::min(g.mz, g.gh + c1 + G);
-        if ((rc = copy_planes(s, in, hin, uploaded, hi, true, s->s_h2d))) return rc;
+        if ((rc = copy_active(s, in, hin, uploaded, std::min(hi, wrap_lo), true, s->s_h2d)))
+            return rc;
         HC_CUDA(cudaEventRecord(ev_up[c], s->s_h2d));
         HC_CUDA(cudaStreamWaitEvent(s->st, ev_up[c], 0));
         if (c == 0) HC_CUDA(cudaStreamWaitEvent(s->st, ev_wrap, 0));
@@ -562,7 +595,7 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
         s->launches++;
         HC_CUDA(cudaEventRecord(ev_comp[c], s->st));
         HC_CUDA(cudaStreamWaitEvent(s->s_d2h, ev_comp[c], 0));
-        if ((rc = copy_planes(s, out, host_out, g.gh + c0, g.gh + c1, false, s->s_d2h))) return rc;
+        if ((rc = copy_active(s, out, host_out, g.gh + c0, g.gh + c1, false, s->s_d2h))) return rc;
     }
     s->cur = 1 - s->cur;
     if ((rc = hc_stepper_advance(s))) return rc;

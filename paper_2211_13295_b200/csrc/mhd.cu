@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
 // over the corners of v + c_f), alpha- = max(0, max of c_f - v); B_b[a-] = mean of the two
 // low-a corner values (and so on); E_C = -(v x B)_C = v_b B_a - v_a B_b.
 template <bool O3, int C>
-__global__ void __launch_bounds__(128) k_mhd_emf(MArgs a) {
+__global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(128) k_mhd_emf(MArgs a) {
     c[2] = int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
     const size_t sa = stride(b, AA), sb = stride(b, BB);
-    const double* mo = a.modes;
+    const double* __restrict__ mo = a.modes;
     const size_t N = b.N;
     double ec[2][2], ba[2][2], bb[2][2];
     double apa = 0.0, ama = 0.0, apb = 0.0, amb = 0.0;
@@ -420,12 +420,12 @@ __global__ void __launch_bounds__(128) k_mhd_emf(MArgs a) {
             double u[NM];
 #pragma unroll
             for (int q = 0; q < NM; ++q) {
-                double v = mo[size_t(q) * N + z] + xa * mo[(size_t(1 + AA) * NM + q) * N + z] +
-                           xb * mo[(size_t(1 + BB) * NM + q) * N + z];
+                double v = __ldg(mo + size_t(q) * N + z) + xa * __ldg(mo + (size_t(1 + AA) * NM + q) * N + z) +
+                           xb * __ldg(mo + (size_t(1 + BB) * NM + q) * N + z);
                 if (O3)
-                    v = v + (1.0 / 6.0) * mo[(size_t(4 + AA) * NM + q) * N + z] +
-                        (1.0 / 6.0) * mo[(size_t(4 + BB) * NM + q) * N + z] +
-                        (xa * xb) * mo[(size_t(7 + AA) * NM + q) * N + z];
+                    v = v + (1.0 / 6.0) * __ldg(mo + (size_t(4 + AA) * NM + q) * N + z) +
+                        (1.0 / 6.0) * __ldg(mo + (size_t(4 + BB) * NM + q) * N + z) +
+                        (xa * xb) * __ldg(mo + (size_t(7 + AA) * NM + q) * N + z);
                 u[q] = v;
             }
             MPrim p = mhd_prim(u, a.gamma, f);

@@ -82,3 +82,36 @@ def test_host_initial_conditions_match_the_oracle():
     go = po.make_geometry(8, 4, 4, 2, (0, 0, 0), (1, 1, 1))
     assert (api.init_sod(g) == orc.init_sod(go)).all()
     assert (api.init_constant(g) == orc.init_constant(go)).all()
+
+
+def test_extension_struct_layouts_match_the_headers(tmp_path):
+    """ctypes mirrors of hc_mhd_params / hc_ced_params against include/hydro_{mhd,ced}.h"""
+    import os
+    import subprocess
+
+    from paper_2211_13295_b200 import ced, mhd
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "sizes_ext.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "hydro_mhd.h"\n#include "hydro_ced.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(hc_mhd_params),'
+        " offsetof(hc_mhd_params, bc), offsetof(hc_mhd_params, device), sizeof(hc_ced_params),"
+        " offsetof(hc_ced_params, bc), offsetof(hc_ced_params, device)); return 0;}\n")
+    exe = tmp_path / "sizes_ext"
+    subprocess.run(["/usr/bin/gcc", "-I" + os.path.join(root, "include"), str(src), "-o",
+                    str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [C.sizeof(mhd.MhdParams), mhd.MhdParams.bc.offset, mhd.MhdParams.device.offset,
+            C.sizeof(ced.CedParams), ced.CedParams.bc.offset, ced.CedParams.device.offset]
+    assert got == want
+
+
+@pytest.mark.skipif(hydro.device_count() > 0, reason="checks the no-GPU behaviour")
+def test_extensions_have_no_cpu_fallback():
+    from paper_2211_13295_b200 import ced, mhd
+    g = mhd.make_geometry(8, 8, 8, 3, (0, 0, 0), (1, 1, 1))
+    with pytest.raises(hydro.HydroCudaError):
+        mhd.MhdStepper(g, mhd.make_params(3))
+    with pytest.raises(hydro.HydroCudaError):
+        ced.CedStepper(g, ced.make_params(3))

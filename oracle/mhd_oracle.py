@@ -275,23 +275,35 @@ def predict(s, g: Geom, par: Params, dt):
         out[ring] = v
         return out
 
+    # the 18 solver states of mhd.cu (spatial part; the half-time state adds ht = tau/2):
+    # faces s = 2A (+A), 2A+1 (-A); edge midpoints s = 6 + 4C + 2 lb + la at
+    # (xa, xb) = (la ? -1/2 : +1/2, lb ? -1/2 : +1/2) in the (C+1, C+2) plane
     m = Modes()
-    m.m0 = [box(u0[q] + 0.5 * tau[q]) for q in range(NM)]
-    m.lin = [[box(lin[d][q]) for q in range(NM)] for d in range(3)]
-    if o3:
-        m.quad = [[box(quad[d][q]) for q in range(NM)] for d in range(3)]
-        m.cross = [[box(cross[d][q]) for q in range(NM)] for d in range(3)]
+    m.ht = [box(0.5 * tau[q]) for q in range(NM)]
+    m.st = [[None] * NM for _ in range(18)]
+    for q in range(NM):
+        for d in range(3):
+            m.st[2 * d][q] = box(face[2 * d][q])
+            m.st[2 * d + 1][q] = box(face[2 * d + 1][q])
+        for C in range(3):
+            AA, BB = (C + 1) % 3, (C + 2) % 3
+            for lb in range(2):
+                for la in range(2):
+                    xa = 0.5 if la == 0 else -0.5
+                    xb = 0.5 if lb == 0 else -0.5
+                    v = u0[q] + xa * lin[AA][q] + xb * lin[BB][q]
+                    if o3:
+                        v = (v + (1.0 / 6.0) * quad[AA][q] + (1.0 / 6.0) * quad[BB][q] +
+                             (xa * xb) * cross[AA][q])
+                    m.st[6 + 4 * C + 2 * lb + la][q] = box(v)
     return m
 
 
 def face_fluxes(m, g: Geom, par: Params, A):
     """k_mhd_flux<A>: fluid fluxes of the A faces, stored at the zone right of the face;
     valid at faces 0..n_A, active transverse."""
-    o3 = par.order == 3
-    ul = [extrap(_shift(m.m0[q], A, -1), +1.0, _shift(m.lin[A][q], A, -1),
-                 _shift(m.quad[A][q], A, -1) if o3 else 0.0, o3) for q in range(NM)]
-    ur = [extrap(m.m0[q], -1.0, m.lin[A][q], m.quad[A][q] if o3 else 0.0, o3)
-          for q in range(NM)]
+    ul = [_shift(m.st[2 * A][q], A, -1) + _shift(m.ht[q], A, -1) for q in range(NM)]
+    ur = [m.st[2 * A + 1][q] + m.ht[q] for q in range(NM)]
     bn = 0.5 * (ul[5 + A] + ur[5 + A])
     ul[5 + A] = bn
     ur[5 + A] = bn
@@ -319,7 +331,6 @@ def face_fluxes(m, g: Geom, par: Params, A):
 def edge_emf(m, g: Geom, par: Params, C):
     """k_mhd_emf<C>: E_C on the C edges (a, b = C+1, C+2), stored at the zone whose low a and
     low b sides meet there; valid for a in 0..n_a, b in 0..n_b, C in 0..n_C-1."""
-    o3 = par.order == 3
     AA, BB = (C + 1) % 3, (C + 2) % 3
     sel = [slice(None)] * 3
     for d in range(3):
@@ -336,15 +347,7 @@ def edge_emf(m, g: Geom, par: Params, C):
                 if lb == 0:
                     out = _shift(out, BB, -1)
                 return out[sel]
-            xa = 0.5 if la == 0 else -0.5
-            xb = 0.5 if lb == 0 else -0.5
-            u = []
-            for q in range(NM):
-                v = z(m.m0[q]) + xa * z(m.lin[AA][q]) + xb * z(m.lin[BB][q])
-                if o3:
-                    v = (v + (1.0 / 6.0) * z(m.quad[AA][q]) + (1.0 / 6.0) * z(m.quad[BB][q]) +
-                         (xa * xb) * z(m.cross[AA][q]))
-                u.append(v)
+            u = [z(m.st[6 + 4 * C + 2 * lb + la][q]) + z(m.ht[q]) for q in range(NM)]
             pr = prim(u, par.gamma)
             vel = pr[1]
             ec[la, lb] = vel[BB] * u[5 + AA] - vel[AA] * u[5 + BB]

@@ -8,9 +8,9 @@
 //
 // Kernels (one thread per zone / face / edge, SoA state so every warp access is coalesced):
 //   k_mhd_ghosts      periodic / outflow gather for cells and faces (one pass, any order)
-//   k_mhd_predict<O3> ring zones: cell-centred B = face average, reconstruction of the 8
-//                     variables, ADER predictor; writes the half-time modes (u0 + tau/2,
-//                     slopes, and at O3 the quadratic and cross modes)
+//   k_mhd_predict<O3> ring zones: reconstruction of the 8 variables, the 18 states the
+//                     face and edge solvers read (6 face averages, 12 edge midpoints, without
+//                     the temporal part), ADER predictor; writes those states and tau/2
 //   k_mhd_flux<A>     HLL (Davis speeds with the fast magnetosonic speed) on the A faces;
 //                     the normal field is the mean of the two reconstructed values
 //   k_mhd_emf<C>      edge EMF E_C from the four zones around the edge: the two-dimensional
@@ -48,7 +48,8 @@ using ct::stride;
 
 struct MArgs {
     double* s;      // state [8][N]
-    double* modes;  // [NMODE][8][N]: 0 = u0 + tau/2, 1+a slope, 4+a quadratic, 7+a cross (a,a+1)
+    double* states; // [18][8][N] spatial part of the predictor's states (see NST below)
+    double* ht;     // [8][N] tau/2 of every ring zone (states at half time = states + ht)
     double* flux;   // [3][5][N] fluid fluxes, face f of axis A stored at the zone it is the low face of
     double* bcell;  // [3][N] cell-centred B of the current state (k_mhd_cellb)
     double* emf;    // [3][N] edge EMFs: E_x(i, j-1/2, k-1/2), E_y(i-1/2, j, k-1/2), E_z(i-1/2, j-1/2, k)
@@ -243,19 +244,31 @@ __device__ __forceinline__ double wvar(const MArgs& a, int q, size_t o) {
     return q < 5 ? __ldg(a.s + size_t(q) * a.b.N + o) : __ldg(a.bcell + size_t(q - 5) * a.b.N + o);
 }
 
-// One ring zone: reconstruction of the 8 cell variables (modes written), ADER predictor,
-// half-time mean written. FAST = 1 is the branch-free bit-exact division; the caller re-runs
-// the zone with FAST = 0 when a fast-path flag is raised (identical bits either way).
+// States a zone hands to the face and edge solvers, evaluated from its reconstruction (u0,
+// slopes, quadratic and cross modes) at the points the solvers need, WITHOUT the temporal
+// part: the half-time state is states[s] + ht (tau/2 of the zone), added by the consumer.
+//   s = 2A (+A face average), 2A+1 (-A face average)            for A = 0, 1, 2
+//   s = 6 + 4C + 2 lb + la: the midpoint of an edge along C, in the (a, b) = (C+1, C+2)
+//       plane at (xa, xb) = (la ? -1/2 : +1/2, lb ? -1/2 : +1/2) -- the corner the zone
+//       presents to the edge when it is the (la, lb) zone of the four around it
+// Materialising these 18 states (instead of the 10 modes) turns the face and edge kernels into
+// plain loads: 16 / 32 values per face / edge instead of 48 / 192 mode loads.
+constexpr int NST = 18;
+
+// One ring zone: reconstruction of the 8 cell variables, its 18 solver states, ADER predictor,
+// tau/2. FAST = 1 is the branch-free bit-exact division; the caller re-runs the zone with
+// FAST = 0 when a fast-path flag is raised (identical bits either way).
 template <bool O3, int FAST>
 __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const FaceSmem& face,
                                              double dt, Fault& f) {
     const Box& b = a.b;
     const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
-    double* mo = a.modes;
+    const size_t N = b.N;
+    double* sv = a.states;
 #pragma unroll 1
     for (int q = 0; q < NM; ++q) {
         const double u0 = wvar(a, q, o);
-        double lin[3], quad[3] = {0.0, 0.0, 0.0};
+        double lin[3], quad[3] = {0.0, 0.0, 0.0}, cross[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             const double up = wvar(a, q, o + st[d]), um = wvar(a, q, o - st[d]);
@@ -266,24 +279,35 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
                 const double upp = wvar(a, q, o + 2 * st[d]);
                 const double umm = wvar(a, q, o - 2 * st[d]);
                 weno3<FAST>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], f);
+                // cross mode of the pair (d, d+1): unlimited central mixed difference
+                const size_t sa = st[d], sb = st[(d + 1) % 3];
+                cross[d] = 0.25 * ((wvar(a, q, o + sa + sb) - wvar(a, q, o + sa - sb)) -
+                                   (wvar(a, q, o - sa + sb) - wvar(a, q, o - sa - sb)));
             }
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            face(2 * d, q) = extrap<O3>(u0, +1.0, lin[d], quad[d]);
-            face(2 * d + 1, q) = extrap<O3>(u0, -1.0, lin[d], quad[d]);
-            mo[(size_t(1 + d) * NM + q) * b.N + o] = lin[d];
+            const double fp = extrap<O3>(u0, +1.0, lin[d], quad[d]);
+            const double fm = extrap<O3>(u0, -1.0, lin[d], quad[d]);
+            face(2 * d, q) = fp;
+            face(2 * d + 1, q) = fm;
+            sv[(size_t(2 * d) * NM + q) * N + o] = fp;
+            sv[(size_t(2 * d + 1) * NM + q) * N + o] = fm;
         }
-        if (O3) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                mo[(size_t(4 + d) * NM + q) * b.N + o] = quad[d];
-                // cross mode of the pair (d, d+1): unlimited central mixed difference
-                const size_t sa = st[d], sb = st[(d + 1) % 3];
-                const double cr = 0.25 * ((wvar(a, q, o + sa + sb) - wvar(a, q, o + sa - sb)) -
-                                          (wvar(a, q, o - sa + sb) - wvar(a, q, o - sa - sb)));
-                mo[(size_t(7 + d) * NM + q) * b.N + o] = cr;
-            }
+        for (int C = 0; C < 3; ++C) {
+            const int AA = (C + 1) % 3, BB = (C + 2) % 3;
+#pragma unroll
+            for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+                for (int la = 0; la < 2; ++la) {
+                    const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
+                    double v = u0 + xa * lin[AA] + xb * lin[BB];
+                    if (O3)
+                        v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
+                            (xa * xb) * cross[AA];
+                    sv[(size_t(6 + 4 * C + 2 * lb + la) * NM + q) * N + o] = v;
+                }
         }
     }
     // ADER predictor (predictor.cpp:26-60): tau = -dt div F(face states); O3: one Picard pass
@@ -300,7 +324,7 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
         for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
     }
 #pragma unroll
-    for (int q = 0; q < NM; ++q) mo[size_t(q) * b.N + o] = wvar(a, q, o) + 0.5 * tau[q];
+    for (int q = 0; q < NM; ++q) a.ht[size_t(q) * N + o] = 0.5 * tau[q];
 }
 
 template <bool O3>
@@ -336,19 +360,12 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
     }
 }
 
-// half-time face-average state of the zone at o on its side `side` (+1 / -1) along axis A
-template <bool O3>
-__device__ __forceinline__ void face_state(const MArgs& a, size_t o, int A, double side,
-                                           double* u) {
-    const double* mo = a.modes;
+// half-time state s of the zone at o: spatial part + tau/2
+__device__ __forceinline__ void half_state(const MArgs& a, size_t o, int s, double* u) {
     const size_t N = a.b.N;
 #pragma unroll
-    for (int q = 0; q < NM; ++q) {
-        const double m0 = mo[size_t(q) * N + o];
-        const double l = mo[(size_t(1 + A) * NM + q) * N + o];
-        const double qd = O3 ? mo[(size_t(4 + A) * NM + q) * N + o] : 0.0;
-        u[q] = extrap<O3>(m0, side, l, qd);
-    }
+    for (int q = 0; q < NM; ++q)
+        u[q] = __ldg(a.states + (size_t(s) * NM + q) * N + o) + __ldg(a.ht + size_t(q) * N + o);
 }
 
 template <bool O3, int A>
@@ -368,8 +385,8 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);  // zone right of the face
     const size_t ol = o - stride(b, A);
     double ul[NM], ur[NM], f5[5];
-    face_state<O3>(a, ol, A, +1.0, ul);
-    face_state<O3>(a, o, A, -1.0, ur);
+    half_state(a, ol, 2 * A, ul);      // +A face of the left zone
+    half_state(a, o, 2 * A + 1, ur);   // -A face of the right zone
     const double bn = 0.5 * (ul[5 + A] + ur[5 + A]);
     ul[5 + A] = bn;
     ur[5 + A] = bn;
@@ -404,7 +421,6 @@ __global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
     c[2] = int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
     const size_t sa = stride(b, AA), sb = stride(b, BB);
-    const double* __restrict__ mo = a.modes;
     const size_t N = b.N;
     double ec[2][2], ba[2][2], bb[2][2];
     double apa = 0.0, ama = 0.0, apb = 0.0, amb = 0.0;
@@ -416,18 +432,8 @@ __global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
         for (int la = 0; la < 2; ++la) {
             // zone (la - 1, lb - 1) relative to the edge's high zone; corner at (xa, xb)
             const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
-            const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
             double u[NM];
-#pragma unroll
-            for (int q = 0; q < NM; ++q) {
-                double v = __ldg(mo + size_t(q) * N + z) + xa * __ldg(mo + (size_t(1 + AA) * NM + q) * N + z) +
-                           xb * __ldg(mo + (size_t(1 + BB) * NM + q) * N + z);
-                if (O3)
-                    v = v + (1.0 / 6.0) * __ldg(mo + (size_t(4 + AA) * NM + q) * N + z) +
-                        (1.0 / 6.0) * __ldg(mo + (size_t(4 + BB) * NM + q) * N + z) +
-                        (xa * xb) * __ldg(mo + (size_t(7 + AA) * NM + q) * N + z);
-                u[q] = v;
-            }
+            half_state(a, z, 6 + 4 * C + 2 * lb + la, u);
             MPrim p = mhd_prim(u, a.gamma, f);
             ec[la][lb] = p.u[BB] * u[5 + AA] - p.u[AA] * u[5 + BB];
             ba[la][lb] = u[5 + AA];
@@ -583,7 +589,8 @@ struct hc_mhd {
     hc_mhd_params p;
     Box b;
     double* s = nullptr;
-    double* modes = nullptr;
+    double* states = nullptr;
+    double* ht = nullptr;
     double* flux = nullptr;
     double* emf = nullptr;
     double* bc = nullptr;
@@ -601,7 +608,8 @@ namespace {
 MArgs margs(const hc_mhd* m) {
     MArgs a;
     a.s = m->s;
-    a.modes = m->modes;
+    a.states = m->states;
+    a.ht = m->ht;
     a.flux = m->flux;
     a.emf = m->emf;
     a.bcell = m->bc;
@@ -720,10 +728,10 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
     b.Q = g->ny + 2 * g->ghost + 1;
     b.R = g->nz + 2 * g->ghost + 1;
     b.N = size_t(b.P) * b.Q * b.R;
-    const int nmode = p->order == 3 ? 10 : 4;
     cudaError_t e = cudaSetDevice(p->device);
     if (e == cudaSuccess) e = cudaMalloc(&m->s, sizeof(double) * NM * b.N);
-    if (e == cudaSuccess) e = cudaMalloc(&m->modes, sizeof(double) * size_t(nmode) * NM * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->states, sizeof(double) * size_t(NST) * NM * b.N);
+    if (e == cudaSuccess) e = cudaMalloc(&m->ht, sizeof(double) * NM * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->flux, sizeof(double) * 15 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, sizeof(double) * 3 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->bc, sizeof(double) * 3 * b.N);
@@ -753,7 +761,8 @@ int hc_mhd_destroy(hc_mhd* m) {
     cudaSetDevice(m->p.device);
     if (m->st) cudaStreamSynchronize(m->st);
     cudaFree(m->s);
-    cudaFree(m->modes);
+    cudaFree(m->states);
+    cudaFree(m->ht);
     cudaFree(m->flux);
     cudaFree(m->emf);
     cudaFree(m->bc);

@@ -247,7 +247,7 @@ def bench_mhd(args):
     value = zones * args.steps / (ms * 1e-3) / 1e6
     # roofline: this first MHD path is unfused (predict -> 3 flux -> 3 EMF -> update), so it
     # is HBM-bound: ideal traffic with one pass per kernel
-    bytes_per_zone = 2900.0
+    bytes_per_zone = 3300.0
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = bytes_per_zone * n ** 3 / (ms / args.steps * 1e-3) / 1e9

@@ -39,6 +39,10 @@ static inline int gmx(const or_geom* g) { return g->nx + 2 * g->ghost; }
 static inline int gmy(const or_geom* g) { return g->ny + 2 * g->ghost; }
 static inline int gmz(const or_geom* g) { return g->nz + 2 * g->ghost; }
 
+/* modes per variable: geometry.hpp:23-27 (5 at O2, 11 at O3); 14 at the O4 extension
+ * (mean, 3 slopes, 3 quadratic, 3 cubic, 3 quartic, temporal) */
+static int modes_of(int order) { return order == 2 ? 5 : (order == 3 ? 11 : 14); }
+
 /* ------------------------------------------------------------------ euler.hpp */
 
 /* euler.hpp:37-50 cons_to_prim */
@@ -299,7 +303,11 @@ void or_weno3_point(const double* s, const or_limiter* cfg, double* ux, double* 
 /* reconstruct.hpp:79-83 extrapolate_to_face */
 static inline double extrap(const double* zv, int modes, int axis, double side) {
     double val = zv[0] + side * 0.5 * zv[1 + axis];
-    if (modes == 11) val += (1.0 / 6.0) * zv[4 + axis];
+    if (modes >= 11) val += (1.0 / 6.0) * zv[4 + axis];
+    if (modes == 14) {  /* O4 extension: P3(1/2) = 1/20, P4(1/2) = 1/70 */
+        val += side * (1.0 / 20.0) * zv[7 + axis];
+        val += (1.0 / 70.0) * zv[10 + axis];
+    }
     return val;
 }
 
@@ -423,6 +431,70 @@ void or_reconstruct_patch_o3(const or_geom* g, double* modal, const or_limiter* 
                 }
 }
 
+/* O4 extension (NOT in the reference: geometry.hpp:13-27 admits orders 2 and 3 only; parity
+ * unpinned): WENO-AO(5,3) (Balsara, Garain & Shu 2016) on s0..s4 = u[i-2..i+2]. The quartic
+ * of the 5-cell stencil in the basis P1 = x, P2 = x^2 - 1/12, P3 = x^3 - 3x/20,
+ * P4 = x^4 - 3x^2/14 + 3/560 (zero mean on the cell), blended with the three WENO3
+ * quadratics (weights gamma_hi = 0.85 and (1 - gamma_hi) * weno_w[k]) by Jiang-Shu weights
+ * of the smoothness indicators sum_l int (d^l P)^2:
+ *   beta_hi = (u1 + u3/10)^2 + 13/3 (u2 + 123/455 u4)^2 + 781/20 u3^2 + 1421461/2275 u4^2
+ *   P_AO = (w_hi / gamma_hi) (P_hi - sum_k gamma_k P_k) + sum_k w_k P_k. */
+void or_weno_ao_point(const double* s, const or_limiter* cfg, double* m) {
+    const double ghi = OR_AO_GAMMA_HI;
+    double o1 = 0.5 * (s[3] - s[1]), o2 = 0.5 * (s[4] - s[0]);
+    double e1 = 0.5 * (s[3] + s[1]) - s[2], e2 = 0.5 * (s[4] + s[0]) - s[2];
+    double u3 = (o2 - 2.0 * o1) * (1.0 / 6.0);
+    double u1 = o1 - (11.0 / 10.0) * u3;
+    double u4 = (e2 - 4.0 * e1) * (1.0 / 12.0);
+    double u2 = e1 - (9.0 / 7.0) * u4;
+    double d0 = s[1] - s[0], d1 = s[2] - s[1], d2 = s[3] - s[2], d3 = s[4] - s[3];
+    double ux_l = 0.5 * (3.0 * d1 - d0), uxx_l = 0.5 * (d1 - d0);
+    double ux_c = 0.5 * (d1 + d2), uxx_c = 0.5 * (d2 - d1);
+    double ux_r = 0.5 * (3.0 * d2 - d3), uxx_r = 0.5 * (d3 - d2);
+    const double k2 = 13.0 / 3.0;
+    double ta = u1 + (1.0 / 10.0) * u3, tb = u2 + (123.0 / 455.0) * u4;
+    double b_hi = ta * ta + k2 * tb * tb + (781.0 / 20.0) * u3 * u3 +
+                  (1421461.0 / 2275.0) * u4 * u4;
+    double b_l = ux_l * ux_l + k2 * uxx_l * uxx_l;
+    double b_c = ux_c * ux_c + k2 * uxx_c * uxx_c;
+    double b_r = ux_r * ux_r + k2 * uxx_r * uxx_r;
+    double gl = (1.0 - ghi) * cfg->weno_w[0], gc = (1.0 - ghi) * cfg->weno_w[1],
+           gr = (1.0 - ghi) * cfg->weno_w[2];
+    double eh = cfg->weno_eps + b_hi, el = cfg->weno_eps + b_l, ec = cfg->weno_eps + b_c,
+           er = cfg->weno_eps + b_r;
+    double ah = ghi / (eh * eh), al = gl / (el * el), ac = gc / (ec * ec), ar = gr / (er * er);
+    double inv = 1.0 / (ah + al + ac + ar);
+    double wh = ah * inv, wl = al * inv, wc = ac * inv, wr = ar * inv;
+    double ratio = wh / ghi;
+    m[0] = ratio * (u1 - (gl * ux_l + gc * ux_c + gr * ux_r)) + (wl * ux_l + wc * ux_c + wr * ux_r);
+    m[1] = ratio * (u2 - (gl * uxx_l + gc * uxx_c + gr * uxx_r)) +
+           (wl * uxx_l + wc * uxx_c + wr * uxx_r);
+    m[2] = ratio * u3;
+    m[3] = ratio * u4;
+}
+
+/* O4 extension: reconstruct_patch_o3's pattern (active + ring) with WENO-AO(5,3) per axis;
+ * modes [1+a] slope, [4+a] quadratic, [7+a] cubic, [10+a] quartic, [13] temporal. */
+void or_reconstruct_patch_o4(const or_geom* g, double* modal, const or_limiter* cfg) {
+    const int gh = g->ghost, M = 14;
+    const ptrdiff_t st[3] = {(ptrdiff_t)NV * M, (ptrdiff_t)NV * M * gmx(g),
+                             (ptrdiff_t)NV * M * gmx(g) * gmy(g)};
+    for (int k = gh - 1; k < gh + g->nz + 1; ++k)
+        for (int j = gh - 1; j < gh + g->ny + 1; ++j)
+            for (int i = gh - 1; i < gh + g->nx + 1; ++i)
+                for (int q = 0; q < NV; ++q) {
+                    double* zc = modal + zoff(g, k, j, i) * NV * M + q * M;
+                    double w[3][4];
+                    for (int a = 0; a < 3; ++a) {
+                        double s[5];
+                        for (int m = -2; m <= 2; ++m) s[m + 2] = zc[m * st[a]];
+                        or_weno_ao_point(s, cfg, w[a]);
+                    }
+                    for (int a = 0; a < 3; ++a)
+                        for (int l = 0; l < 4; ++l) zc[1 + 3 * l + a] = w[a][l];
+                }
+}
+
 /* ---------------------------------------------------------------- predictor.cpp */
 
 /* predictor.cpp:12-22 flux_divergence */
@@ -460,7 +532,7 @@ int or_predictor_ptwise(double* zv, int modes, double dt, double dx, double dy, 
     int rc = flux_divergence(face, idx, idy, idz, gamma, div);
     if (rc) return rc;
     for (int q = 0; q < NV; ++q) tau[q] = -dt * div[q];
-    if (modes == 11) {
+    if (modes >= 11) {
         for (int s = 0; s < 6; ++s)
             for (int q = 0; q < NV; ++q) face[s][q] += 0.5 * tau[q];
         if ((rc = flux_divergence(face, idx, idy, idz, gamma, div))) return rc;
@@ -476,7 +548,7 @@ int or_predict_patch(const or_geom* g, int modes, double* modal, double dt, doub
     for (int k = gh - 1; k < gh + g->nz + 1; ++k)
         for (int j = gh - 1; j < gh + g->ny + 1; ++j)
             for (int i = gh - 1; i < gh + g->nx + 1; ++i) {
-                double zone[NV * 11];
+                double zone[NV * 14];
                 double* src = modal + zoff(g, k, j, i) * NV * modes;
                 memcpy(zone, src, sizeof(double) * NV * modes);
                 if (or_predictor_ptwise(zone, modes, dt, g->dx, g->dy, g->dz, gamma)) {
@@ -622,7 +694,8 @@ int or_compute_dt_next(const or_geom* g, int modes, const double* modal, double 
 
 static void reconstruct(const or_geom* g, const or_params* par, double* modal) {
     if (par->order == 2) or_limit_patch_o2(g, modal, &par->lim);
-    else or_reconstruct_patch_o3(g, modal, &par->lim);
+    else if (par->order == 3) or_reconstruct_patch_o3(g, modal, &par->lim);
+    else or_reconstruct_patch_o4(g, modal, &par->lim);
 }
 
 static int three_sweeps(const or_geom* g, const or_params* par, int modes, const double* modal,
@@ -637,7 +710,7 @@ static int three_sweeps(const or_geom* g, const or_params* par, int modes, const
 int or_ader_step(const or_geom* g, const or_params* par, double* modal, double* skinny,
                  double* fx, double* fy, double* fz, double* rate, double dt, double cfl,
                  double* dt_next) {
-    const int modes = par->order == 2 ? 5 : 11;
+    const int modes = modes_of(par->order);
     int rc;
     or_skinny_to_modal(g, modes, skinny, modal);
     reconstruct(g, par, modal);
@@ -661,7 +734,7 @@ void or_rk_save_u0(const or_geom* g, const double* skinny, double* u0) {
 int or_rk_stage(const or_geom* g, const or_params* par, double* modal, double* skinny,
                 double* fx, double* fy, double* fz, double* rate, const double* u0, double dt,
                 double a, double b) {
-    const int modes = par->order == 2 ? 5 : 11;
+    const int modes = modes_of(par->order);
     const int gh = g->ghost;
     int rc;
     or_skinny_to_modal(g, modes, skinny, modal);
@@ -694,7 +767,7 @@ int or_rk_step(const or_geom* g, const or_params* par, int nstages, double* moda
         snprintf(g_err, sizeof g_err, "rk_stages called for a non-RK integrator");
         return OR_INVALID;
     }
-    const int modes = par->order == 2 ? 5 : 11;
+    const int modes = modes_of(par->order);
     int rc;
     or_rk_save_u0(g, skinny, stage_u0);
     for (int s = 0; s < nstages; ++s) {
@@ -826,7 +899,7 @@ double or_initial_dt(const or_geom* g, const double* s, double gamma, double cfl
  * on a 1x1x1 PatchSet is apply_boundary (test_transfer.cpp:46-68). ADER only. */
 int or_run_steps(const or_geom* g, const or_params* par, int bc, double cfl, int steps,
                  double* skinny, double* dts) {
-    const int modes = par->order == 2 ? 5 : 11;
+    const int modes = modes_of(par->order);
     size_t tot = (size_t)gmx(g) * gmy(g) * gmz(g);
     double* modal = calloc(tot * NV * modes, sizeof(double));
     double* fx = calloc((size_t)g->nz * g->ny * (g->nx + 1) * NV, sizeof(double));

@@ -73,6 +73,10 @@ void or_apply_boundary_skinny(const or_geom* g, int kind, double* skinny);
 void or_apply_boundary_modal(const or_geom* g, int modes, int kind, double* modal);
 void or_limit_patch_o2(const or_geom* g, double* modal, const or_limiter* cfg);
 void or_reconstruct_patch_o3(const or_geom* g, double* modal, const or_limiter* cfg);
+/* O4 extension (not in the reference; parity unpinned): WENO-AO(5,3), modes M = 14 */
+#define OR_AO_GAMMA_HI 0.85
+void or_weno_ao_point(const double* s, const or_limiter* cfg, double* m4);
+void or_reconstruct_patch_o4(const or_geom* g, double* modal, const or_limiter* cfg);
 int or_predict_patch(const or_geom* g, int modes, double* modal, double dt, double gamma);
 void or_zero_temporal_mode(const or_geom* g, int modes, double* modal);
 int or_make_flux_axis(const or_geom* g, int modes, const double* modal, int axis, double gamma,
@@ -86,7 +90,7 @@ int or_compute_dt_next(const or_geom* g, int modes, const double* modal, double 
 
 /* ---- stepper (stepper.cpp) ---- */
 typedef struct {
-    int order;      /* 2 or 3 */
+    int order;      /* 2 or 3 (4: the WENO-AO extension) */
     int solver;     /* OR_RUSANOV / OR_HLL */
     double gamma;
     or_limiter lim;

@@ -63,7 +63,7 @@ def make_geometry(nx, ny, nz, order, lo=(-5.0, -5.0, -5.0), hi=(5.0, 5.0, 5.0)) 
     """geometry.hpp:67-80 make_geometry."""
     g = Geom()
     g.nx, g.ny, g.nz = nx, ny, nz
-    g.ghost = {2: 2, 3: 3}[order]
+    g.ghost = {2: 2, 3: 3, 4: 3}[order]  # 4: the WENO-AO extension (radius 2, like O3)
     g.dx = (hi[0] - lo[0]) / nx
     g.dy = (hi[1] - lo[1]) / ny
     g.dz = (hi[2] - lo[2]) / nz
@@ -80,7 +80,7 @@ def make_params(order, solver=HLL, gamma=1.4) -> Params:
 
 
 def modes_for_order(order):
-    return {2: 5, 3: 11}[order]
+    return {2: 5, 3: 11, 4: 14}[order]
 
 
 def zeros_skinny(g):

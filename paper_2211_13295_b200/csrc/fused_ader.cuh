@@ -154,16 +154,30 @@ __device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double 
 // mode-0 neighbourhood: reconstruction (reconstruct.cpp:16-28 MC, :42-61 WENO3) and the
 // ADER predictor (predictor.cpp:26-60). pc: the zone in the current smem plane (rows W*NV
 // apart); zm2..zp2: the zone's column in planes p-2..p+2.
-template <bool O3, int FAST, bool RK>
+template <int ORD, int FAST, bool RK>
 __device__ __forceinline__ void zone_states(const double* pc, int row, const double* zm2,
                                             const double* zm1, const double* zp1,
                                             const double* zp2, const FusedArgs& a, double dt,
                                             double (*st)[NV], Fault& f) {
+    constexpr bool O3 = ORD >= 3;
     double face[6][NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
         const double u0 = pc[q];
-        if (!O3) {
+        if (ORD == 4) {  // WENO-AO(5,3) extension (pointwise.cuh weno_ao)
+            double mx[4], my[4], mz[4];
+            weno_ao<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
+                          mx, f);
+            weno_ao<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q],
+                          a.lim, my, f);
+            weno_ao<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, mz, f);
+            face[0][q] = extrap4(u0, +1.0, mx);
+            face[1][q] = extrap4(u0, -1.0, mx);
+            face[2][q] = extrap4(u0, +1.0, my);
+            face[3][q] = extrap4(u0, -1.0, my);
+            face[4][q] = extrap4(u0, +1.0, mz);
+            face[5][q] = extrap4(u0, -1.0, mz);
+        } else if (!O3) {
             const double cfac = q == 0 ? a.lim.cfac_rho : a.lim.cfac_other;
             const double sx = mc_limiter(pc[NV + q] - u0, u0 - pc[-NV + q], cfac);
             const double sy = mc_limiter(pc[row + q] - u0, u0 - pc[-row + q], cfac);
@@ -217,14 +231,14 @@ struct Careful {
     Fault f;
 };
 
-template <bool O3, bool RK>
+template <int ORD, bool RK>
 __device__ __noinline__ Careful zone_states_careful(const double* pc, int row, const double* zm2,
                                                     const double* zm1, const double* zp1,
                                                     const double* zp2, const FusedArgs& a,
                                                     double dt) {
     Careful c;
     c.f.clear();
-    zone_states<O3, false, RK>(pc, row, zm2, zm1, zp1, zp2, a, dt, c.st.v, c.f);
+    zone_states<ORD, 0, RK>(pc, row, zm2, zm1, zp1, zp2, a, dt, c.st.v, c.f);
     return c;
 }
 
@@ -268,9 +282,10 @@ __device__ __forceinline__ void face_flux(const double* ul, const double* ur, do
 // RK = true: one Runge-Kutta stage (temporal mode zero, U' = a*U0 + b*(U + dt*rate),
 // stepper.cpp:100-143); the CFL estimate is only taken when a.want_dt (last stage,
 // rk_step's compute_dt_next, stepper.cpp:155-156).
-template <bool O3, int SOLVER, int TX, int TY, int MINB, bool RK>
-__global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
+template <int ORD, int SOLVER, int TX, int TY, int MINB, bool RK>
+__global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     fused_ader_kernel(const FusedArgs a) {
+    constexpr bool O3 = ORD >= 3;  // radius-2 stencil (WENO3, or WENO-AO at ORD 4)
     using S = FusedShape<O3, TX, TY>;
     constexpr int R = S::R, G = S::G, NB = S::NB, W = S::W, H = S::H;
     if (a.ctl->done) return;
@@ -406,9 +421,9 @@ __global__ void __launch_bounds__(FusedShape<O3, TX, TY>::NT, MINB)
             const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
             Fault f;
             f.clear();
-            zone_states<O3, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
+            zone_states<ORD, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
             if (f.redo()) {
-                Careful c = zone_states_careful<O3, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
+                Careful c = zone_states_careful<ORD, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
 #pragma unroll
                 for (int s = 0; s < 6; ++s)
 #pragma unroll

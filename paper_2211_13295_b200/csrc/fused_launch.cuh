@@ -13,10 +13,10 @@
 namespace hc {
 namespace HC_FUSED_NS {
 
-template <bool O3, int SOLVER, int TX, int TY, int MINB, bool RK>
+template <int ORD, int SOLVER, int TX, int TY, int MINB, bool RK>
 static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
-    using S = FusedShape<O3, TX, TY>;
-    auto kern = fused_ader_kernel<O3, SOLVER, TX, TY, MINB, RK>;
+    using S = FusedShape<(ORD >= 3), TX, TY>;
+    auto kern = fused_ader_kernel<ORD, SOLVER, TX, TY, MINB, RK>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
@@ -35,9 +35,9 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "fused_ader_kernel launch");
 }
 
-template <bool O3, int SOLVER, bool RK>
+template <int ORD, int SOLVER, bool RK>
 static int launch_one(const FusedArgs& a, cudaStream_t st) {
-    using T = FusedTile<O3>;
+    using T = FusedTile<(ORD >= 3)>;
 #ifdef HC_TUNE
     static const int cfg = [] {
         const char* v = std::getenv("HC_FUSED_CFG");
@@ -45,25 +45,25 @@ static int launch_one(const FusedArgs& a, cudaStream_t st) {
     }();
     if (SOLVER == 1) {
         switch (cfg) {
-            case 1: return launch_cfg<O3, SOLVER, 16, 8, 2, RK>(a, st);
-            case 2: return launch_cfg<O3, SOLVER, 16, 12, 2, RK>(a, st);
-            case 3: return launch_cfg<O3, SOLVER, 24, 8, 2, RK>(a, st);
-            case 4: return launch_cfg<O3, SOLVER, 32, 16, 1, RK>(a, st);
-            case 5: return launch_cfg<O3, SOLVER, 16, 8, 3, RK>(a, st);
+            case 1: return launch_cfg<ORD, SOLVER, 16, 8, 2, RK>(a, st);
+            case 2: return launch_cfg<ORD, SOLVER, 16, 12, 2, RK>(a, st);
+            case 3: return launch_cfg<ORD, SOLVER, 24, 8, 2, RK>(a, st);
+            case 4: return launch_cfg<ORD, SOLVER, 32, 16, 1, RK>(a, st);
+            case 5: return launch_cfg<ORD, SOLVER, 16, 8, 3, RK>(a, st);
             default: break;
         }
     }
 #endif
-    return launch_cfg<O3, SOLVER, T::TX, T::TY, T::MINB, RK>(a, st);
+    return launch_cfg<ORD, SOLVER, T::TX, T::TY, T::MINB, RK>(a, st);
 }
 
-template <bool O3, bool RK>
+template <int ORD, bool RK>
 static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
     switch (solver) {
-        case 0: return launch_one<O3, 0, RK>(a, st);
-        case 1: return launch_one<O3, 1, RK>(a, st);
-        case 2: return launch_one<O3, 2, RK>(a, st);  // HLLC (extension)
-        default: return launch_one<O3, 3, RK>(a, st);  // HLLI (extension)
+        case 0: return launch_one<ORD, 0, RK>(a, st);
+        case 1: return launch_one<ORD, 1, RK>(a, st);
+        case 2: return launch_one<ORD, 2, RK>(a, st);  // HLLC (extension)
+        default: return launch_one<ORD, 3, RK>(a, st);  // HLLI (extension)
     }
 }
 
@@ -71,11 +71,14 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
 
 int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st) {
     using namespace HC_FUSED_NS;
-    if (rk)
-        return order == 2 ? launch_solver<false, true>(a, solver, st)
-                          : launch_solver<true, true>(a, solver, st);
-    return order == 2 ? launch_solver<false, false>(a, solver, st)
-                      : launch_solver<true, false>(a, solver, st);
+    if (rk) {
+        if (order == 2) return launch_solver<2, true>(a, solver, st);
+        return order == 3 ? launch_solver<3, true>(a, solver, st)
+                          : launch_solver<4, true>(a, solver, st);
+    }
+    if (order == 2) return launch_solver<2, false>(a, solver, st);
+    return order == 3 ? launch_solver<3, false>(a, solver, st)
+                      : launch_solver<4, false>(a, solver, st);
 }
 
 }  // namespace hc

@@ -218,7 +218,8 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         set_error(HC_INVALID, "null argument");
         return HC_INVALID;
     }
-    int rc = validate_geom(g, p->order);
+    // order 4 (the WENO-AO extension, fused stepper only) has order 3's ghost needs
+    int rc = validate_geom(g, p->order == 4 ? 3 : p->order);
     if (rc) return rc;
     if (p->solver < HC_RUSANOV || p->solver > HC_HLLI) {
         set_error(HC_INVALID, "unknown riemann solver");
@@ -246,7 +247,7 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
     s->g = *g;
     s->p = *p;
     s->o = *o;
-    const bool o3 = p->order == 3;
+    const bool o3 = p->order >= 3;
     const int TX = o3 ? FusedTile<true>::TX : FusedTile<false>::TX;
     const int TY = o3 ? FusedTile<true>::TY : FusedTile<false>::TY;
     const int G = o3 ? 3 : 2;
@@ -546,7 +547,7 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
         return hc_stepper_download(s, host_out);
     }
     const SG& g = s->sg;
-    const int G = s->p.order == 3 ? 3 : 2;
+    const int G = s->p.order >= 3 ? 3 : 2;
     nchunks = std::max(1, std::min(nchunks, g.nz / 4));
     if (!s->s_h2d) {
         HC_CUDA(cudaStreamCreateWithFlags(&s->s_h2d, cudaStreamNonBlocking));

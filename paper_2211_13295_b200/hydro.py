@@ -76,20 +76,22 @@ ADER, RK2, RK3 = 0, 2, 3  # IntegratorChoice (predictor.hpp:11)
 
 
 def ghost_for_order(order: int) -> int:
-    """geometry.hpp:13-17."""
+    """geometry.hpp:13-17 (order 4: the WENO-AO extension of the fused stepper, radius 2)."""
     if order == 2:
         return 2
-    if order == 3:
+    if order in (3, 4):
         return 3
     raise ValueError(f"unsupported order {order}")
 
 
 def modes_for_order(order: int) -> int:
-    """geometry.hpp:23-27."""
+    """geometry.hpp:23-27 (order 4: 14 modes in the C restatement, extension)."""
     if order == 2:
         return 5
     if order == 3:
         return 11
+    if order == 4:
+        return 14
     raise ValueError(f"unsupported order {order}")
 
 

@@ -356,7 +356,7 @@ def bench_ced(args):
     t, _, done = st.sync()
     zones = n ** 3
     divb, divd = st.max_div()
-    bytes_per_zone = 1650.0  # ideal one-pass traffic of the unfused O3 design
+    bytes_per_zone = 2070.0  # ideal one-pass traffic of the unfused O3 design
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = bytes_per_zone * zones / (ms / args.steps * 1e-3) / 1e9

@@ -151,17 +151,26 @@ def predict(s, sigma, g: Geom, par: Params, dt):
         out = np.zeros(g.shape)
         out[ring] = v
         return out
+    # ced.cu's 12 edge-midpoint states (spatial part) and tau/2
     m = Modes()
-    m.m0 = [box(u0[q] + 0.5 * tau[q]) for q in range(NF)]
-    m.lin = [[box(lin[d][q]) for q in range(NF)] for d in range(3)]
-    if o3:
-        m.quad = [[box(quad[d][q]) for q in range(NF)] for d in range(3)]
-        m.cross = [[box(cross[d][q]) for q in range(NF)] for d in range(3)]
+    m.ht = [box(0.5 * tau[q]) for q in range(NF)]
+    m.st = [[None] * NF for _ in range(12)]
+    for q in range(NF):
+        for C in range(3):
+            AA, BB = (C + 1) % 3, (C + 2) % 3
+            for lb in range(2):
+                for la in range(2):
+                    xa = 0.5 if la == 0 else -0.5
+                    xb = 0.5 if lb == 0 else -0.5
+                    v = u0[q] + xa * lin[AA][q] + xb * lin[BB][q]
+                    if o3:
+                        v = (v + (1.0 / 6.0) * quad[AA][q] + (1.0 / 6.0) * quad[BB][q] +
+                             (xa * xb) * cross[AA][q])
+                    m.st[4 * C + 2 * lb + la][q] = box(v)
     return m
 
 
 def edges(m, g: Geom, par: Params, C):
-    o3 = par.order == 3
     AA, BB = (C + 1) % 3, (C + 2) % 3
     sel = [slice(None)] * 3
     for d in range(3):
@@ -177,15 +186,7 @@ def edges(m, g: Geom, par: Params, C):
                 if lb == 0:
                     out = _shift(out, BB, -1)
                 return out[sel]
-            xa = 0.5 if la == 0 else -0.5
-            xb = 0.5 if lb == 0 else -0.5
-            u = []
-            for q in range(NF):
-                v = z(m.m0[q]) + xa * z(m.lin[AA][q]) + xb * z(m.lin[BB][q])
-                if o3:
-                    v = (v + (1.0 / 6.0) * z(m.quad[AA][q]) + (1.0 / 6.0) * z(m.quad[BB][q]) +
-                         (xa * xb) * z(m.cross[AA][q]))
-                u.append(v)
+            u = [z(m.st[4 * C + 2 * lb + la][q]) + z(m.ht[q]) for q in range(NF)]
             e = e + u[C]
             h = h + u[3 + C]
             if la:

@@ -44,7 +44,8 @@ struct CArgs {
     double* s;      // [6][N] face fields
     double* sigma;  // [N] zone conductivity
     double* w;      // [6][N] cell averages of the face fields
-    double* modes;  // [NMODE][6][N]: 0 = u0 + tau/2, 1+a slope, 4+a quadratic, 7+a cross
+    double* states; // [12][6][N] edge-midpoint states (spatial part), s = 4C + 2 lb + la
+    double* ht;     // [6][N] tau/2 of every ring zone (half-time state = states + ht)
     double* emf;    // [3][N] E on the edges (same indexing as mhd.cu)
     double* hmf;    // [3][N] H on the edges
     Box b;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
         const double* w = a.w + size_t(q) * N;
         const double c0 = w[o];
         u0[q] = c0;
-        double lin[3], quad[3] = {0.0, 0.0, 0.0};
+        double lin[3], quad[3] = {0.0, 0.0, 0.0}, cross[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             const double up = w[o + st[d]], um = w[o - st[d]];
@@ -141,13 +142,28 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
             else weno3<0>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
             face[2 * d][q] = extrap<O3>(c0, +1.0, lin[d], quad[d]);
             face[2 * d + 1][q] = extrap<O3>(c0, -1.0, lin[d], quad[d]);
-            a.modes[(size_t(1 + d) * NF + q) * N + o] = lin[d];
             if (O3) {
-                a.modes[(size_t(4 + d) * NF + q) * N + o] = quad[d];
                 const size_t sa = st[d], sb = st[(d + 1) % 3];
-                a.modes[(size_t(7 + d) * NF + q) * N + o] =
+                cross[d] =
                     0.25 * ((w[o + sa + sb] - w[o + sa - sb]) - (w[o - sa + sb] - w[o - sa - sb]));
             }
+        }
+        // the 12 edge-midpoint states the edge solver reads (mhd.cu's convention: the corner
+        // (xa, xb) = (la ? -1/2 : +1/2, lb ? -1/2 : +1/2) in the (C+1, C+2) plane)
+#pragma unroll
+        for (int C = 0; C < 3; ++C) {
+            const int AA = (C + 1) % 3, BB = (C + 2) % 3;
+#pragma unroll
+            for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+                for (int la = 0; la < 2; ++la) {
+                    const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
+                    double v = c0 + xa * lin[AA] + xb * lin[BB];
+                    if (O3)
+                        v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
+                            (xa * xb) * cross[AA];
+                    a.states[(size_t(4 * C + 2 * lb + la) * NF + q) * N + o] = v;
+                }
         }
     }
     // predictor: C = -div F of the face states; B: tau = dt C; D: the conduction source over
@@ -183,7 +199,7 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
         for (int q = 3; q < NF; ++q) tau[q] = -dt * div[q];
     }
 #pragma unroll
-    for (int q = 0; q < NF; ++q) a.modes[size_t(q) * N + o] = u0[q] + 0.5 * tau[q];
+    for (int q = 0; q < NF; ++q) a.ht[size_t(q) * N + o] = 0.5 * tau[q];
 }
 
 template <bool O3, int C>
@@ -198,7 +214,6 @@ __global__ void __launch_bounds__(128) k_ced_edge(CArgs a) {
     const int c0 = int(r % ex), c1 = int((r / ex) % ey), c2 = int(r / (size_t(ex) * ey));
     const size_t o = at(b, c2 + b.gh, c1 + b.gh, c0 + b.gh);
     const size_t sa = stride(b, AA), sb = stride(b, BB), N = b.N;
-    const double* mo = a.modes;
     // per corner (la, lb): the six fields at the corner
     double e = 0.0, h = 0.0, dbp = 0.0, dbm = 0.0, dap = 0.0, dam = 0.0;
     double bbp = 0.0, bbm = 0.0, bap = 0.0, bam = 0.0;
@@ -207,18 +222,11 @@ __global__ void __launch_bounds__(128) k_ced_edge(CArgs a) {
 #pragma unroll
         for (int la = 0; la < 2; ++la) {
             const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
-            const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
             double u[NF];
 #pragma unroll
-            for (int q = 0; q < NF; ++q) {
-                double v = mo[size_t(q) * N + z] + xa * mo[(size_t(1 + AA) * NF + q) * N + z] +
-                           xb * mo[(size_t(1 + BB) * NF + q) * N + z];
-                if (O3)
-                    v = v + (1.0 / 6.0) * mo[(size_t(4 + AA) * NF + q) * N + z] +
-                        (1.0 / 6.0) * mo[(size_t(4 + BB) * NF + q) * N + z] +
-                        (xa * xb) * mo[(size_t(7 + AA) * NF + q) * N + z];
-                u[q] = v;
-            }
+            for (int q = 0; q < NF; ++q)
+                u[q] = __ldg(a.states + (size_t(4 * C + 2 * lb + la) * NF + q) * N + z) +
+                       __ldg(a.ht + size_t(q) * N + z);
             e = e + u[C];      // D_C (-> E_C = D_C / eps)
             h = h + u[3 + C];  // B_C (-> H_C = B_C / mu)
             if (la) { dbp = dbp + u[BB]; bbp = bbp + u[3 + BB]; }
@@ -324,7 +332,7 @@ struct hc_ced {
     hc_geom g;
     hc_ced_params p;
     Box b;
-    double *s = nullptr, *sigma = nullptr, *w = nullptr, *modes = nullptr, *emf = nullptr,
+    double *s = nullptr, *sigma = nullptr, *w = nullptr, *states = nullptr, *ht = nullptr, *emf = nullptr,
            *hmf = nullptr, *scratch = nullptr;
     StepCtl* ctl = nullptr;
     cudaStream_t st = nullptr;
@@ -338,7 +346,8 @@ CArgs cargs(const hc_ced* m) {
     a.s = m->s;
     a.sigma = m->sigma;
     a.w = m->w;
-    a.modes = m->modes;
+    a.states = m->states;
+    a.ht = m->ht;
     a.emf = m->emf;
     a.hmf = m->hmf;
     a.b = m->b;
@@ -427,13 +436,13 @@ int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
     b.Q = g->ny + 2 * g->ghost + 1;
     b.R = g->nz + 2 * g->ghost + 1;
     b.N = size_t(b.P) * b.Q * b.R;
-    const int nmode = p->order == 3 ? 10 : 4;
     const size_t B = sizeof(double) * b.N;
     cudaError_t e = cudaSetDevice(p->device);
     if (e == cudaSuccess) e = cudaMalloc(&m->s, NF * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->sigma, B);
     if (e == cudaSuccess) e = cudaMalloc(&m->w, NF * B);
-    if (e == cudaSuccess) e = cudaMalloc(&m->modes, size_t(nmode) * NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->states, size_t(12) * NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->ht, NF * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, 3 * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->hmf, 3 * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->scratch, 2 * sizeof(double));
@@ -459,7 +468,7 @@ int hc_ced_destroy(hc_ced* m) {
     if (!m) return HC_OK;
     cudaSetDevice(m->p.device);
     if (m->st) cudaStreamSynchronize(m->st);
-    for (double* p : {m->s, m->sigma, m->w, m->modes, m->emf, m->hmf, m->scratch}) cudaFree(p);
+    for (double* p : {m->s, m->sigma, m->w, m->states, m->ht, m->emf, m->hmf, m->scratch}) cudaFree(p);
     cudaFree(m->ctl);
     if (m->st) cudaStreamDestroy(m->st);
     delete m;

@@ -11,7 +11,8 @@ PARITY UNPINNED: the reference scopes out CED and stiff-source ADER (SPEC.md:8, 
 CED code, test or fixture exists under /root/reference. Self-consistency checks live in
 tests/test_ced_oracle.py and tests/test_ced_gpu.py (exact plane waves and their convergence,
 div B = 0 and div D = 0 for uniform sigma to round-off, electromagnetic energy never
-increases, exact decay of a uniform field for any sigma dt, the magnetic-diffusion limit).
+increases, exact decay of a uniform field for any sigma dt, the magnetic-diffusion limit
+recovered by the asymptotic-preserving edge dissipation).
 
 Layout: state[6][mz+1][my+1][mx+1] = Dx, Dy, Dz, Bx, By, Bz on the low face of the zone
 with the same index; sigma[mz+1][my+1][mx+1] per zone.
@@ -170,7 +171,7 @@ def predict(s, sigma, g: Geom, par: Params, dt):
     return m
 
 
-def edges(m, g: Geom, par: Params, C):
+def edges(m, g: Geom, par: Params, C, sigma):
     AA, BB = (C + 1) % 3, (C + 2) % 3
     sel = [slice(None)] * 3
     for d in range(3):
@@ -204,8 +205,23 @@ def edges(m, g: Geom, par: Params, C):
     hc = 0.5 * par.c
     E = np.zeros(g.shape)
     H = np.zeros(g.shape)
-    E[sel] = 0.25 * e / par.eps_ + hc * (0.5 * bbp - 0.5 * bbm) - hc * (0.5 * bap - 0.5 * bam)
-    H[sel] = 0.25 * h / par.mu - hc * (0.5 * dbp - 0.5 * dbm) + hc * (0.5 * dap - 0.5 * dam)
+    # asymptotic-preserving scaling of the upwind dissipation (Jin-Levermore type): with
+    # sigma_e the mean conductivity of the four zones, theta = 1 / (1 + sigma_e h / (2 c eps))
+    # per direction; theta = 1 (plain upwind) where sigma_e = 0
+    sg = 0.0
+    for lb in range(2):
+        for la in range(2):
+            out = sigma
+            if la == 0:
+                out = _shift(out, AA, -1)
+            if lb == 0:
+                out = _shift(out, BB, -1)
+            sg = sg + out[sel]
+    sg = 0.25 * sg
+    ta = 1.0 / (1.0 + sg * g.d[AA] / (2.0 * par.c * par.eps_))
+    tb = 1.0 / (1.0 + sg * g.d[BB] / (2.0 * par.c * par.eps_))
+    E[sel] = 0.25 * e / par.eps_ + hc * ta * (0.5 * bbp - 0.5 * bbm) - hc * tb * (0.5 * bap - 0.5 * bam)
+    H[sel] = 0.25 * h / par.mu - hc * ta * (0.5 * dbp - 0.5 * dbm) + hc * tb * (0.5 * dap - 0.5 * dam)
     return E, H
 
 
@@ -270,7 +286,7 @@ def energy(s, g: Geom, par: Params):
 def step(s, sigma, g: Geom, par: Params, dt):
     fill_ghosts(s, None, g, par.bc)
     m = predict(s, sigma, g, par, dt)
-    EH = [edges(m, g, par, C) for C in range(3)]
+    EH = [edges(m, g, par, C, sigma) for C in range(3)]
     update(s, sigma, [x[0] for x in EH], [x[1] for x in EH], g, par, dt)
 
 

@@ -10,7 +10,9 @@
 //                       predictor with the Maxwell flux and the conduction source solved
 //                       over the half step by the exponential update (one Picard pass at O3)
 //   k_ced_edge<O3, C>   E_C and H_C on the C edges from the four corner states: the 2D upwind
-//                       solver (HLL with speeds +-c is exact for linear Maxwell):
+//                       solver (HLL with speeds +-c is exact for linear Maxwell), its
+//                       dissipation scaled by theta = 1/(1 + sigma h/(2 c eps)) so the
+//                       magnetic-diffusion limit is preserved in good conductors:
 //                         E_C = mean corner E_C + c/2 (B_b[a+] - B_b[a-]) - c/2 (B_a[b+] - B_a[b-])
 //                         H_C = mean corner H_C - c/2 (D_b[a+] - D_b[a-]) + c/2 (D_a[b+] - D_a[b-])
 //                       (a = C+1, b = C+2; [a+] = mean of the two corners on the high-a side)
@@ -235,11 +237,23 @@ __global__ void __launch_bounds__(128) k_ced_edge(CArgs a) {
             else { dam = dam + u[AA]; bam = bam + u[3 + AA]; }
         }
     const double hc = 0.5 * a.c;
+    // asymptotic-preserving scaling of the upwind dissipation (Jin-Levermore type): in a good
+    // conductor (sigma h / (2 c eps) >> 1) the jumps' c/2 dissipation would swamp the
+    // magnetic diffusivity 1/(mu sigma); theta = 1 / (1 + sigma_e h / (2 c eps)) per
+    // direction, sigma_e = mean of the four zones; theta = 1 exactly where sigma_e = 0
+    double sg = 0.0;
+#pragma unroll
+    for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int la = 0; la < 2; ++la) sg = sg + a.sigma[o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0)];
+    sg = 0.25 * sg;
+    const double ta = 1.0 / (1.0 + sg * a.d[AA] / (2.0 * a.c * a.eps));
+    const double tb = 1.0 / (1.0 + sg * a.d[BB] / (2.0 * a.c * a.eps));
     // means of two corners: 0.5 * sum
-    a.emf[size_t(C) * N + o] = 0.25 * e / a.eps + hc * (0.5 * bbp - 0.5 * bbm) -
-                               hc * (0.5 * bap - 0.5 * bam);
-    a.hmf[size_t(C) * N + o] = 0.25 * h / a.mu - hc * (0.5 * dbp - 0.5 * dbm) +
-                               hc * (0.5 * dap - 0.5 * dam);
+    a.emf[size_t(C) * N + o] = 0.25 * e / a.eps + hc * ta * (0.5 * bbp - 0.5 * bbm) -
+                               hc * tb * (0.5 * bap - 0.5 * bam);
+    a.hmf[size_t(C) * N + o] = 0.25 * h / a.mu - hc * ta * (0.5 * dbp - 0.5 * dbm) +
+                               hc * tb * (0.5 * dap - 0.5 * dam);
 }
 
 __global__ void k_ced_update(CArgs a) {

@@ -131,3 +131,35 @@ def test_ced_wave_absorbed_by_conductor():
     divb, _ = st.max_div()
     assert divb < 1e-12
     st.close()
+
+
+@pytest.mark.parametrize("sigma", [1e3, 5e3, 1e5])
+def test_ced_magnetic_diffusion_limit(sigma):
+    """B_z = sin(2 pi x) in a good conductor (sigma dt = 2 .. 200): after the fast transient
+    the slow mode decays at lambda = (-s + sqrt(s^2 - 4 c^2 k^2)) / 2 (~ -k^2 / (mu sigma)).
+    The asymptotic-preserving edge dissipation keeps the rate within 1 % for any sigma h."""
+    n = 64
+    L = (1.0, 4.0 / n, 4.0 / n)
+    g = ced.make_geometry(n, 4, 4, 2, (0, 0, 0), L)
+    st = ced.CedStepper(g, ced.make_params(2))
+    st.upload(ced.diffusion_mode(g), sigma)
+    gh = g.ghost
+    x = (np.arange(n) + 0.5) / n
+
+    def amp():
+        bz = st.download()[5][gh:gh + 4, gh:gh + 4, gh:gh + n].mean(axis=(0, 1))
+        return 2 * (bz * np.sin(2 * math.pi * x)).mean()
+    k = 2 * math.pi
+    lam_th = (-sigma + math.sqrt(sigma * sigma - 4 * k * k)) / 2
+    t1 = 0.2
+    t2 = min(2.0, 0.5 / abs(lam_th))  # decay of at least ~40 %
+    st.run(0.4, t1)
+    a1 = amp()
+    dt = st.cfl_dt(0.4)
+    st.set_time(t1, dt, t2)
+    while st.sync()[0] < t2 * (1 - 1e-12):
+        st.step(256)
+    a2 = amp()
+    lam = math.log(a2 / a1) / (t2 - t1)
+    assert abs(lam / lam_th - 1) < 0.01, (sigma, lam, lam_th)
+    st.close()

@@ -185,9 +185,22 @@ __global__ void k_flux(const double* __restrict__ m, G g, double gamma, double* 
     const int n2 = A == 1 ? g.nz : (A == 0 ? g.nz : g.ny);
     const int n1 = A == 0 ? g.ny : g.nx;
     const int nf = (A == 0 ? g.nx : (A == 1 ? g.ny : g.nz)) + 1;
-    size_t id = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (id >= size_t(n2) * n1 * nf) return;
-    int f = int(id % nf), c1 = int((id / nf) % n1), c2 = int(id / (size_t(nf) * n1));
+    size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (t >= size_t(n2) * n1 * nf) return;
+    // x and y sweeps: face index fastest; z sweep: the x index c1 fastest, so a warp reads
+    // adjacent zone records instead of records a plane apart (747 -> 239 us at 128^3; the face
+    // index is innermost in the OUTPUT layout only)
+    int f, c1, c2;
+    if (A != 2) {
+        f = int(t % nf);
+        c1 = int((t / nf) % n1);
+        c2 = int(t / (size_t(nf) * n1));
+    } else {
+        c1 = int(t % n1);
+        f = int((t / n1) % nf);
+        c2 = int(t / (size_t(nf) * n1));
+    }
+    const size_t id = (size_t(c2) * n1 + c1) * nf + f;  // FaceFlux layout, fields.hpp:78
     constexpr int M = O3 ? 11 : 5;
     size_t zl, zr;
     const int gh = g.gh;

@@ -107,14 +107,33 @@ __global__ void k_recon_o3(double* m, G g, Limiter L) {
     int i, j, k;
     if (!ring_index(blockIdx.x * size_t(blockDim.x) + threadIdx.x, g, i, j, k)) return;
     const ptrdiff_t sx = NV * 11, sy = sx * g.mx, sz = sy * g.my;
+    double* z0 = m + zoff(g, k, j, i) * NV * 11;
+    // all 13-point stencils of the 5 variables first (mode 0 is never written here), so the
+    // loads are not serialised behind the mode stores of the same array
+    double sv[NV][13];
+#pragma unroll
     for (int q = 0; q < NV; ++q) {
-        double* zc = m + zoff(g, k, j, i) * NV * 11 + q * 11;
+        const double* zc = z0 + q * 11;
+        sv[q][0] = zc[0];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const ptrdiff_t sd = d == 0 ? sx : (d == 1 ? sy : sz);
+            sv[q][1 + 4 * d] = zc[-2 * sd];
+            sv[q][2 + 4 * d] = zc[-sd];
+            sv[q][3 + 4 * d] = zc[sd];
+            sv[q][4 + 4 * d] = zc[2 * sd];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double* zc = z0 + q * 11;
+        const double* v = sv[q];
         double ux, uxx, uy, uyy, uz, uzz;
         Fault f;  // careful mode: IEEE division, nothing to report from a reconstruction
         f.clear();
-        weno3(zc[-2 * sx], zc[-sx], zc[0], zc[sx], zc[2 * sx], L, ux, uxx, f);
-        weno3(zc[-2 * sy], zc[-sy], zc[0], zc[sy], zc[2 * sy], L, uy, uyy, f);
-        weno3(zc[-2 * sz], zc[-sz], zc[0], zc[sz], zc[2 * sz], L, uz, uzz, f);
+        weno3(v[1], v[2], v[0], v[3], v[4], L, ux, uxx, f);
+        weno3(v[5], v[6], v[0], v[7], v[8], L, uy, uyy, f);
+        weno3(v[9], v[10], v[0], v[11], v[12], L, uz, uzz, f);
         zc[1] = ux;
         zc[2] = uy;
         zc[3] = uz;
@@ -132,12 +151,21 @@ __global__ void k_recon_o3_cross(double* m, G g) {
     int i = int(id % g.nx) + g.gh, j = int((id / g.nx) % g.ny) + g.gh,
         k = int(id / (size_t(g.nx) * g.ny)) + g.gh;
     const ptrdiff_t sx = NV * 11, sy = sx * g.mx, sz = sy * g.my;
+    double* z0 = m + zoff(g, k, j, i) * NV * 11;
+    double c[NV][3];  // all loads (slopes, modes 1-3) before the stores (modes 7-9)
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
-        double* zc = m + zoff(g, k, j, i) * NV * 11 + q * 11;
-        zc[7] = 0.25 * ((zc[sy + 1] - zc[-sy + 1]) + (zc[sx + 2] - zc[-sx + 2]));
-        zc[8] = 0.25 * ((zc[sz + 2] - zc[-sz + 2]) + (zc[sy + 3] - zc[-sy + 3]));
-        zc[9] = 0.25 * ((zc[sx + 3] - zc[-sx + 3]) + (zc[sz + 1] - zc[-sz + 1]));
+        const double* zc = z0 + q * 11;
+        c[q][0] = 0.25 * ((zc[sy + 1] - zc[-sy + 1]) + (zc[sx + 2] - zc[-sx + 2]));
+        c[q][1] = 0.25 * ((zc[sz + 2] - zc[-sz + 2]) + (zc[sy + 3] - zc[-sy + 3]));
+        c[q][2] = 0.25 * ((zc[sx + 3] - zc[-sx + 3]) + (zc[sz + 1] - zc[-sz + 1]));
+    }
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double* zc = z0 + q * 11;
+        zc[7] = c[q][0];
+        zc[8] = c[q][1];
+        zc[9] = c[q][2];
     }
 }
 

@@ -495,6 +495,15 @@ def main():
                 "frac": hbm_achieved / hbm_peak, "bytes_per_zone": BYTES_PER_ZONE,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
     }
+    # the binding unit's busy fraction from the committed ncu capture of this kernel
+    prof = os.path.join(ROOT, "profiles",
+                        f"r1_fused_o{order}_{n}_{'fma' if args.fast else 'exact'}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            k0 = json.load(f)["kernels"][0]
+        roofline["fp64_pipe_busy_ncu"] = k0.get("fp64_pipe_pct", 0.0) / 100.0
+        roofline["fp64_pipe_source"] = (os.path.relpath(prof, ROOT) + " (ncu --set full, "
+                                        "sm__pipe_fp64_cycles_active, one launch)")
     traffic = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic):
         with open(traffic) as f:

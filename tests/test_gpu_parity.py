@@ -364,3 +364,27 @@ def test_full_size_properties_256_o3(api):
     st.sync()
     out = st.download()
     assert same(out[act], c[act])
+
+
+@pytest.mark.parametrize("integrator", [hydro.ADER, hydro.RK3])
+def test_graph_replay_equals_plain_launches(api, integrator):
+    """hc_stepper_step(n > 1) replays one captured step as a CUDA graph: same bits, same
+    device time control, same launch accounting as n single steps."""
+    g = hydro.make_geometry(20, 16, 12, 3)
+    s0 = api.init_isentropic_vortex(g, 3)
+    dt0 = api.initial_dt(g, s0, 0.4)
+    outs = []
+    for graph in (True, False):
+        st = hydro.Stepper(g, hydro.make_params(3), integrator=integrator)
+        st.upload(s0)
+        st.set_time(0.0, dt0, 0.4, 0.3)
+        if graph:
+            st.step(9)
+            st.step(9)
+        else:
+            for _ in range(18):
+                st.step(1)
+        outs.append((st.download(), st.sync(), st.launches))
+        st.close()
+    (a, ta, la), (b, tb, lb) = outs
+    assert same(a, b) and ta == tb and la == lb

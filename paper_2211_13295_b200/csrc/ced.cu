@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "ct_common.cuh"
 #include "fused_types.cuh"
+#include "graph_step.cuh"
 
 namespace hc {
 namespace ced {
@@ -351,6 +352,7 @@ struct hc_ced {
     StepCtl* ctl = nullptr;
     cudaStream_t st = nullptr;
     long launches = 0;
+    StepGraph graph;
 };
 
 namespace {
@@ -532,11 +534,8 @@ int hc_ced_set_time(hc_ced* m, double t, double dt, double t_final) {
 
 int hc_ced_step(hc_ced* m, int n) {
     HC_CUDA(cudaSetDevice(m->p.device));
-    for (int s = 0; s < n; ++s) {
-        int rc = launch_step(m);
-        if (rc) return rc;
-    }
-    return HC_OK;
+    // n > 1: one captured step replayed as a CUDA graph (graph_step.cuh)
+    return replay_steps(m->graph, m->st, 0.0, m->launches, n, [&] { return launch_step(m); });
 }
 
 int hc_ced_sync(hc_ced* m, double* t, double* dt, long* steps) {

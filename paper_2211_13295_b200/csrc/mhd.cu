@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "ct_common.cuh"
 #include "fused_types.cuh"
+#include "graph_step.cuh"
 
 namespace hc {
 namespace mhd {
@@ -600,6 +601,7 @@ struct hc_mhd {
     cudaStream_t st = nullptr;
     bool own_stream = true;
     long launches = 0;
+    StepGraph graph;
     double cfl = 0.4;
 };
 
@@ -807,11 +809,8 @@ int hc_mhd_set_time(hc_mhd* m, double t, double dt, double cfl, double t_final) 
 
 int hc_mhd_step(hc_mhd* m, int n) {
     HC_CUDA(cudaSetDevice(m->p.device));
-    for (int s = 0; s < n; ++s) {
-        int rc = launch_step(m);
-        if (rc) return rc;
-    }
-    return HC_OK;
+    // n > 1: one captured step replayed as a CUDA graph (graph_step.cuh)
+    return replay_steps(m->graph, m->st, m->cfl, m->launches, n, [&] { return launch_step(m); });
 }
 
 int hc_mhd_sync(hc_mhd* m, double* t, double* dt, long* steps) {

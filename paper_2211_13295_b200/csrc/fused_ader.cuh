@@ -1,6 +1,7 @@
 // fused_ader.cuh -- ONE sm_100a kernel per ADER step: reconstruction (MC at O2, WENO3 at
-// O3) -> per-zone ADER predictor -> Rusanov/HLL fluxes on all three face families -> flux
-// differencing -> conservative update -> CFL dt estimate + exact min-reduction.
+// O3, WENO-AO at the O4 extension) -> per-zone ADER predictor -> face Riemann fluxes
+// (Rusanov/HLL, HLLC/HLLI extensions) on all three face families -> flux differencing ->
+// conservative update -> CFL dt estimate + exact min-reduction.
 //
 // Replaces the reference's pipeline stepper.cpp:49-78 (skinny_to_modal, reconstruct_patch,
 // predict_patch, make_flux_axis x3, make_du_dt, update_u_timestep) without materialising
@@ -9,8 +10,10 @@
 //
 // Decomposition (2.5D): a CTA owns a TX x TY column tile and marches a chunk of TZ planes
 // upward. For each plane p it keeps planes p-R..p+R of mode 0 (the zone averages) for the
-// tile plus a halo of G zones in shared memory (a ring buffer of 2R+2 planes refilled with
-// cp.async one plane ahead). One thread owns one "E-column": a tile column or a face-adjacent
+// tile plus a halo of G zones in shared memory (a ring buffer of 2R+1 planes at O3, 2R+2 at
+// O2, refilled one plane ahead by bulk copies -- one row per cp.async.bulk, completion on a
+// per-slot mbarrier -- or 8-byte cp.async when rows are not 16-byte aligned). One thread owns
+// one "E-column": a tile column or a face-adjacent
 // ring column (the ring zones' slopes and temporal modes are needed for the tile's boundary
 // faces -- the reference computes them on "active + one ring", predictor.cpp:68-70).
 //
@@ -19,8 +22,9 @@
 //             [sync] flux:    west-x, south-y faces (tile threads; east/north ring threads take
 //             the tile's last x/y face) and the bottom z-face against the +z state this
 //             thread kept from plane p-1
-//             [sync] rate:    east/north fluxes from smem -> partial rate of plane p; plane p-1
-//             is finalised with its top z-flux and updated (U + dt*rate), dt estimate.
+//             [sync] rate:    east/north fluxes from smem -> partial rate of plane p (kept in
+//             shared memory); plane p-1 is finalised with its top z-flux and updated
+//             (U + dt*rate), dt estimate.
 // The rate keeps the reference's association -cx*(E-W) - cy*(N-S) - cz*(T-B)
 // (corrector.cpp:89-90) split as (partial(x,y)) - cz*(z), so the result is bit-identical.
 #pragma once

@@ -292,8 +292,10 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
             const double fm = extrap<O3>(u0, -1.0, lin[d], quad[d]);
             face(2 * d, q) = fp;
             face(2 * d + 1, q) = fm;
-            sv[(size_t(2 * d) * NM + q) * N + o] = fp;
-            sv[(size_t(2 * d + 1) * NM + q) * N + o] = fm;
+            // streaming stores (evict-first): 1.2 KB of states per zone would otherwise push
+            // the reconstruction stencils out of L2
+            __stcs(sv + (size_t(2 * d) * NM + q) * N + o, fp);
+            __stcs(sv + (size_t(2 * d + 1) * NM + q) * N + o, fm);
         }
 #pragma unroll
         for (int C = 0; C < 3; ++C) {
@@ -307,7 +309,7 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
                     if (O3)
                         v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
                             (xa * xb) * cross[AA];
-                    sv[(size_t(6 + 4 * C + 2 * lb + la) * NM + q) * N + o] = v;
+                    __stcs(sv + (size_t(6 + 4 * C + 2 * lb + la) * NM + q) * N + o, v);
                 }
         }
     }
@@ -325,7 +327,7 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
         for (int q = 0; q < NM; ++q) tau[q] = -dt * div[q];
     }
 #pragma unroll
-    for (int q = 0; q < NM; ++q) a.ht[size_t(q) * N + o] = 0.5 * tau[q];
+    for (int q = 0; q < NM; ++q) __stcs(a.ht + size_t(q) * N + o, 0.5 * tau[q]);
 }
 
 template <bool O3>

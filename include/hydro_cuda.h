@@ -231,6 +231,31 @@ long hc_stepper_launches(hc_stepper* s);
 /* Storage layout of the state buffers: rows per plane, doubles per row, planes. */
 int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz);
 
+/* ------------------------------------------------ device-resident patch set
+ * PatchSet (transfer.hpp:47-73) with the patches' states resident in HBM: px x py x pz
+ * patches of `global` (the split must divide the mesh: transfer.cpp:19-22), each a fused
+ * stepper, stepped together on one stream. hc_patchset_step = run_patch_step
+ * (transfer.cpp:152-216): exchange_ghosts (one device gather reproducing the x, y, z sweeps of
+ * transfer.cpp:94-149), every patch's step (RK: an exchange before every stage), the global
+ * dt min, the t/dt hand-off -- no host round trip. Bit-identical to the single-patch run
+ * (the reference's split invariance, acceptance criterion 8). */
+typedef struct hc_patchset hc_patchset;
+
+int hc_patchset_create(const hc_geom* global, int px, int py, int pz, const hc_params* p,
+                       int boundary, int exact, int device, int integrator, hc_patchset** out);
+int hc_patchset_destroy(hc_patchset* ps);
+/* transfer.cpp:50-76 scatter_to_patches / gather_from_patches between a global HOST
+ * SkinnyState [mz][my][mx][5] (active zones only) and the patches' device states */
+int hc_patchset_scatter(hc_patchset* ps, const double* global_skinny);
+int hc_patchset_gather(hc_patchset* ps, double* global_skinny);
+int hc_patchset_set_time(hc_patchset* ps, double t, double dt, double cfl, double t_final);
+int hc_patchset_step(hc_patchset* ps, int n);
+int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done);
+/* TransferLedger (transfer.hpp:16-24) of the skinny strategy, as the reference counts it:
+ * uploads, downloads, scalar_uploads, scalar_downloads, uploads_active_only, steps */
+int hc_patchset_ledger(hc_patchset* ps, unsigned long long* counts6);
+long hc_patchset_launches(hc_patchset* ps);
+
 #ifdef __cplusplus
 }
 #endif

@@ -233,9 +233,11 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         set_error(HC_INVALID, "integrator must be 0 (ADER), 2 (RK2) or 3 (SSP-RK3)");
         return HC_INVALID;
     }
+    // -1 = caller-filled ghosts: z alone (z-slab halos) or all three axes (patch sets)
     for (int a = 0; a < 3; ++a)
-        if (o->bc[a] < -1 || o->bc[a] > 1 || (a < 2 && o->bc[a] < 0)) {
-            set_error(HC_INVALID, "bad boundary kind (x/y must be periodic or outflow)");
+        if (o->bc[a] < -1 || o->bc[a] > 1 || (a < 2 && o->bc[a] < 0 && o->bc[2] >= 0) ||
+            ((o->bc[0] < 0) != (o->bc[1] < 0))) {
+            set_error(HC_INVALID, "bad boundary kind (x/y periodic or outflow, or all -1)");
             return HC_INVALID;
         }
     int ndev = hc_device_count();
@@ -403,7 +405,7 @@ static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
                                                s->o.bc[0], s->o.bc[1], s->o.bc[2], lo, ring_mode);
         s->launches++;
     };
-    launch(a_lo, a_hi, 1);
+    if (s->o.bc[0] >= 0) launch(a_lo, a_hi, 1);  // (all -1: a patch set fills every ghost)
     if (s->o.bc[2] >= 0) {
         launch(k_lo, std::min(k_hi, g.gh), 0);
         launch(std::max(k_lo, g.gh + g.nz), k_hi, 0);
@@ -702,6 +704,289 @@ int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz) {
     if (pitch) *pitch = s->sg.pitch;
     if (mz) *mz = s->sg.mz;
     return HC_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================ patch set
+// Device-resident PatchSet (transfer.hpp:47-73): px x py x pz patches of one global mesh, each
+// an hc_stepper whose state stays in HBM, stepped together on one stream. exchange_ghosts
+// (transfer.cpp:94-149: x, y, z sweeps over neighbour patches) is one gather kernel: composing
+// the three sweeps, every ghost zone of every patch holds the global active zone at the
+// composed mapped coordinates, which lives in a computable source patch. The global dt min of
+// run_patch_step (transfer.cpp:184) is a device kernel over the patches' accumulators. The
+// TransferLedger is pure accounting (transfer.cpp:160-175) and is reproduced on the host.
+
+namespace hc {
+namespace psk {  // (a named namespace: nvcc's stub generator trips over a second anonymous one)
+
+struct PatchDev {
+    double* buf[3];
+    StepCtl* ctl;
+};
+
+struct PSGeom {
+    int px, py, pz, lnx, lny, lnz, gnx, gny, gnz;
+    int gh, mx, my, mz, my_pad, pitch, nbuf, bc;
+};
+
+__device__ __forceinline__ int map_global(int a, int n, int bc) {
+    if (bc == HC_PERIODIC) return ((a % n) + n) % n;
+    return a < 0 ? 0 : (a >= n ? n - 1 : a);
+}
+
+__global__ void k_patch_exchange(const PatchDev* __restrict__ pd, PSGeom g, int rel) {
+    const size_t per = size_t(g.mx) * g.my * g.mz;
+    const size_t np = size_t(g.px) * g.py * g.pz;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= per * np) return;
+    const int p = int(r / per);
+    size_t z = r % per;
+    const int i = int(z % g.mx), j = int((z / g.mx) % g.my), k = int(z / (size_t(g.mx) * g.my));
+    const bool act = i >= g.gh && i < g.gh + g.lnx && j >= g.gh && j < g.gh + g.lny &&
+                     k >= g.gh && k < g.gh + g.lnz;
+    if (act) return;
+    const StepCtl* c = pd[p].ctl;
+    if (c->done) return;
+    const int pi = p % g.px, pj = (p / g.px) % g.py, pk = p / (g.px * g.py);
+    const int gx = map_global(pi * g.lnx + i - g.gh, g.gnx, g.bc);
+    const int gy = map_global(pj * g.lny + j - g.gh, g.gny, g.bc);
+    const int gz = map_global(pk * g.lnz + k - g.gh, g.gnz, g.bc);
+    const int s = ((gz / g.lnz) * g.py + gy / g.lny) * g.px + gx / g.lnx;
+    const int is = g.gh + gx % g.lnx, js = g.gh + gy % g.lny, ks = g.gh + gz % g.lnz;
+    const double* src = pd[s].buf[(pd[s].ctl->cur + rel) % g.nbuf] +
+                        (size_t(ks) * g.my_pad + js) * g.pitch + size_t(is) * NV;
+    double* dst = pd[p].buf[(c->cur + rel) % g.nbuf] + (size_t(k) * g.my_pad + j) * g.pitch +
+                  size_t(i) * NV;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) dst[q] = src[q];
+}
+
+// run_patch_step's global min (transfer.cpp:184): every patch's accumulator becomes the min
+__global__ void k_patch_dt_min(const PatchDev* __restrict__ pd, int np) {
+    double m = 1.0e32;
+    for (int p = 0; p < np; ++p) m = smin(m, pd[p].ctl->acc);
+    for (int p = 0; p < np; ++p) pd[p].ctl->acc = m;
+}
+
+}  // namespace psk
+}  // namespace hc
+
+using hc::psk::PatchDev;
+using hc::psk::PSGeom;
+
+struct hc_patchset {
+    hc_geom global;
+    hc_params p;
+    int px, py, pz, bc, integrator;
+    std::vector<hc_stepper*> patches;
+    PatchDev* dev = nullptr;  // device table of the patches' buffers / control blocks
+    PSGeom pg;
+    cudaStream_t st = nullptr;
+    int device = 0;
+    long launches = 0;
+    unsigned long long ledger[6] = {0, 0, 0, 0, 0, 0};  // TransferLedger field order
+};
+
+static int ps_exchange(hc_patchset* ps, int rel) {
+    const size_t n = size_t(ps->pg.mx) * ps->pg.my * ps->pg.mz * ps->patches.size();
+    hc::psk::k_patch_exchange<<<unsigned((n + 255) / 256), 256, 0, ps->st>>>(ps->dev, ps->pg, rel);
+    ps->launches++;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_patch_exchange");
+}
+
+extern "C" {
+
+int hc_patchset_create(const hc_geom* global, int px, int py, int pz, const hc_params* p,
+                       int boundary, int exact, int device, int integrator, hc_patchset** out) {
+    if (!global || !p || !out) {
+        set_error(HC_INVALID, "null argument");
+        return HC_INVALID;
+    }
+    if (px < 1 || py < 1 || pz < 1) {  // transfer.cpp:19-20
+        set_error(HC_INVALID, "patch split counts must be positive");
+        return HC_INVALID;
+    }
+    if (global->nx % px || global->ny % py || global->nz % pz) {  // transfer.cpp:21-22
+        set_error(HC_INVALID, "patch split must divide the mesh evenly");
+        return HC_INVALID;
+    }
+    if (boundary != HC_PERIODIC && boundary != HC_OUTFLOW) {
+        set_error(HC_INVALID, "boundary kind must be periodic or outflow");
+        return HC_INVALID;
+    }
+    hc_patchset* ps = new (std::nothrow) hc_patchset;
+    if (!ps) {
+        set_error(HC_CUDA, "out of host memory");
+        return HC_CUDA;
+    }
+    ps->global = *global;
+    ps->p = *p;
+    ps->px = px;
+    ps->py = py;
+    ps->pz = pz;
+    ps->bc = boundary;
+    ps->integrator = integrator;
+    ps->device = device;
+    int rc = HC_OK;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ps->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) rc = cuda_fail(e, "hc_patchset_create");
+    const int lnx = global->nx / px, lny = global->ny / py, lnz = global->nz / pz;
+    for (int pk = 0; pk < pz && !rc; ++pk)
+        for (int pj = 0; pj < py && !rc; ++pj)
+            for (int pi = 0; pi < px && !rc; ++pi) {  // transfer.cpp:33-47
+                hc_geom g = *global;
+                g.nx = lnx;
+                g.ny = lny;
+                g.nz = lnz;
+                g.origin[0] = global->origin[0] + pi * lnx * global->dx;
+                g.origin[1] = global->origin[1] + pj * lny * global->dy;
+                g.origin[2] = global->origin[2] + pk * lnz * global->dz;
+                hc_stepper_opts o = {{-1, -1, -1}, exact, device, integrator};
+                hc_stepper* s = nullptr;
+                rc = hc_stepper_create(&g, p, &o, &s);
+                if (!rc) {
+                    ps->patches.push_back(s);
+                    rc = hc_stepper_set_stream(s, ps->st);
+                }
+            }
+    if (!rc) {
+        const hc_stepper* s0 = ps->patches[0];
+        ps->pg = PSGeom{px, py, pz, lnx, lny, lnz, global->nx, global->ny, global->nz,
+                        s0->sg.gh, s0->sg.mx, s0->sg.my, s0->sg.mz, s0->sg.my_pad,
+                        s0->sg.pitch, s0->nbuf, boundary};
+        std::vector<PatchDev> table;
+        for (hc_stepper* s : ps->patches)
+            table.push_back(PatchDev{{s->buf[0], s->buf[1], s->buf[2]}, s->ctl});
+        e = cudaMalloc(&ps->dev, sizeof(PatchDev) * table.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpy(ps->dev, table.data(), sizeof(PatchDev) * table.size(),
+                           cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) rc = cuda_fail(e, "hc_patchset_create");
+    }
+    if (rc) {
+        hc_patchset_destroy(ps);
+        return rc;
+    }
+    *out = ps;
+    return HC_OK;
+}
+
+int hc_patchset_destroy(hc_patchset* ps) {
+    if (!ps) return HC_OK;
+    cudaSetDevice(ps->device);
+    if (ps->st) cudaStreamSynchronize(ps->st);
+    for (hc_stepper* s : ps->patches) hc_stepper_destroy(s);
+    cudaFree(ps->dev);
+    if (ps->st) cudaStreamDestroy(ps->st);
+    delete ps;
+    return HC_OK;
+}
+
+// scatter_to_patches / gather_from_patches (transfer.cpp:50-76): active zones of a global HOST
+// SkinnyState <-> the patches' device states (strided 3D copies, ghosts filled on the device)
+static int ps_copy(hc_patchset* ps, double* host, bool up) {
+    const hc_geom& G = ps->global;
+    const int gh = G.ghost;
+    const size_t grow = size_t(G.nx + 2 * gh) * NV * sizeof(double);
+    for (size_t idx = 0; idx < ps->patches.size(); ++idx) {
+        hc_stepper* s = ps->patches[idx];
+        int rc = refresh_cur(s);
+        if (rc) return rc;
+        const int pi = int(idx % ps->px), pj = int((idx / ps->px) % ps->py),
+                  pk = int(idx / (size_t(ps->px) * ps->py));
+        cudaMemcpy3DParms m = {};
+        cudaPitchedPtr hp = make_cudaPitchedPtr(host, grow, grow, G.ny + 2 * gh);
+        cudaPitchedPtr dp = make_cudaPitchedPtr(s->buf[s->cur], size_t(s->sg.pitch) * sizeof(double),
+                                                size_t(s->sg.mx) * NV * sizeof(double), s->sg.my_pad);
+        const cudaPos hpos = make_cudaPos(size_t(gh + pi * ps->pg.lnx) * NV * sizeof(double),
+                                          gh + pj * ps->pg.lny, gh + pk * ps->pg.lnz);
+        const cudaPos dpos = make_cudaPos(size_t(gh) * NV * sizeof(double), gh, gh);
+        m.extent = make_cudaExtent(size_t(ps->pg.lnx) * NV * sizeof(double), ps->pg.lny, ps->pg.lnz);
+        m.srcPtr = up ? hp : dp;
+        m.dstPtr = up ? dp : hp;
+        m.srcPos = up ? hpos : dpos;
+        m.dstPos = up ? dpos : hpos;
+        m.kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+        HC_CUDA(cudaMemcpy3DAsync(&m, ps->st));
+    }
+    HC_CUDA(cudaStreamSynchronize(ps->st));
+    return HC_OK;
+}
+
+int hc_patchset_scatter(hc_patchset* ps, const double* global_skinny) {
+    HC_CUDA(cudaSetDevice(ps->device));
+    return ps_copy(ps, const_cast<double*>(global_skinny), true);
+}
+
+int hc_patchset_gather(hc_patchset* ps, double* global_skinny) {
+    HC_CUDA(cudaSetDevice(ps->device));
+    return ps_copy(ps, global_skinny, false);
+}
+
+int hc_patchset_set_time(hc_patchset* ps, double t, double dt, double cfl, double t_final) {
+    for (hc_stepper* s : ps->patches) {
+        int rc = hc_stepper_set_time(s, t, dt, cfl, t_final);
+        if (rc) return rc;
+    }
+    return HC_OK;
+}
+
+// run_patch_step (transfer.cpp:152-216) n times, all on the device: exchange_ghosts, every
+// patch's fused step (each RK stage after its own exchange), the global dt min, the t/dt
+// hand-off; the ledger counts what the reference's TransferLedger would.
+int hc_patchset_step(hc_patchset* ps, int n) {
+    HC_CUDA(cudaSetDevice(ps->device));
+    const int ns = ps->integrator == 0 ? 1 : ps->integrator;
+    const int np = int(ps->patches.size());
+    for (int it = 0; it < n; ++it) {
+        for (int k = 0; k < ns; ++k) {
+            int rc = ps_exchange(ps, ps->integrator == 0 ? 0 : k);
+            for (int p = 0; p < np && !rc; ++p) rc = hc_stepper_compute(ps->patches[p]);
+            if (rc) return rc;
+        }
+        hc::psk::k_patch_dt_min<<<1, 1, 0, ps->st>>>(ps->dev, np);
+        ps->launches++;
+        HC_CUDA(cudaGetLastError());
+        for (int p = 0; p < np; ++p) {
+            int rc = hc_stepper_advance(ps->patches[p]);
+            if (rc) return rc;
+        }
+        // TransferLedger (transfer.cpp:160-175): per patch per step, skinny strategy
+        const hc_stepper* s0 = ps->patches[0];
+        const unsigned long long total = (unsigned long long)s0->sg.mx * s0->sg.my * s0->sg.mz * NV;
+        const unsigned long long active =
+            (unsigned long long)ps->pg.lnx * ps->pg.lny * ps->pg.lnz * NV;
+        ps->ledger[0] += total * np;   // uploads
+        ps->ledger[1] += total * np;   // downloads
+        ps->ledger[2] += np;           // scalar_uploads (dt)
+        ps->ledger[3] += np;           // scalar_downloads (dt_next)
+        ps->ledger[4] += active * np;  // uploads_active_only
+        ps->ledger[5] += 1;            // steps
+    }
+    return HC_OK;
+}
+
+int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done) {
+    int rc = HC_OK;
+    for (hc_stepper* s : ps->patches) {
+        int r = hc_stepper_sync(s, t, dt, steps_done);
+        if (r && !rc) rc = r;
+    }
+    return rc;
+}
+
+int hc_patchset_ledger(hc_patchset* ps, unsigned long long* counts) {
+    for (int i = 0; i < 6; ++i) counts[i] = ps->ledger[i];
+    return HC_OK;
+}
+
+long hc_patchset_launches(hc_patchset* ps) {
+    long l = ps->launches;
+    for (hc_stepper* s : ps->patches) l += s->launches;
+    return l;
 }
 
 }  // extern "C"

@@ -404,3 +404,66 @@ def fp64_peak(device: int = 0) -> float:
     d = C.c_double()
     _check(load_library().hc_fp64_peak(device, C.byref(d)))
     return d.value
+
+
+class PatchSet:
+    """Device-resident PatchSet (transfer.hpp:47-73, include/hydro_cuda.h hc_patchset_*):
+    px x py x pz patches of `g`, states in HBM, run_patch_step on the device."""
+
+    def __init__(self, g: Geom, px, py, pz, params: Params, boundary=PERIODIC, exact=True,
+                 device=0, integrator=ADER):
+        self.lib = load_library()
+        self.lib.hc_patchset_launches.restype = C.c_long
+        for n in ("hc_patchset_destroy", "hc_patchset_launches"):
+            getattr(self.lib, n).argtypes = [C.c_void_p]
+        self.lib.hc_patchset_step.argtypes = [C.c_void_p, C.c_int]
+        self.g = g
+        h = C.c_void_p()
+        _check(self.lib.hc_patchset_create(C.byref(g), px, py, pz, C.byref(params), boundary,
+                                           int(exact), device, integrator, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.lib.hc_patchset_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def scatter(self, skinny):
+        """scatter_to_patches (transfer.cpp:50-62) from a global host SkinnyState"""
+        s = np.ascontiguousarray(skinny, dtype=np.float64)
+        _check(self.lib.hc_patchset_scatter(self.h, _p(s)))
+
+    def gather(self, out=None):
+        """gather_from_patches (transfer.cpp:64-76) into a global host SkinnyState"""
+        out = zeros_skinny(self.g) if out is None else out
+        _check(self.lib.hc_patchset_gather(self.h, _p(out)))
+        return out
+
+    def set_time(self, t, dt, cfl, t_final=-1.0):
+        _check(self.lib.hc_patchset_set_time(self.h, C.c_double(t), C.c_double(dt),
+                                             C.c_double(cfl), C.c_double(t_final)))
+
+    def step(self, n=1):
+        _check(self.lib.hc_patchset_step(self.h, n))
+
+    def sync(self):
+        t, dt, n = C.c_double(), C.c_double(), C.c_long()
+        _check(self.lib.hc_patchset_sync(self.h, C.byref(t), C.byref(dt), C.byref(n)))
+        return t.value, dt.value, n.value
+
+    def ledger(self):
+        """TransferLedger fields (uploads, downloads, scalar_uploads, scalar_downloads,
+        uploads_active_only, steps) for the skinny strategy"""
+        c = (C.c_ulonglong * 6)()
+        _check(self.lib.hc_patchset_ledger(self.h, c))
+        return tuple(int(x) for x in c)
+
+    @property
+    def launches(self):
+        return self.lib.hc_patchset_launches(self.h)

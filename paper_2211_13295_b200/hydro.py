@@ -464,6 +464,17 @@ class PatchSet:
         _check(self.lib.hc_patchset_ledger(self.h, c))
         return tuple(int(x) for x in c)
 
+    @staticmethod
+    def ledger_csv_header():
+        """transfer.cpp:218 ledger_csv_header"""
+        return "step,strategy,uploads,downloads,scalar_uploads"
+
+    def ledger_csv_row(self, step):
+        """transfer.cpp:220-227 ledger_csv_row (per-step averages, skinny strategy)"""
+        up, down, su, _, _, steps = self.ledger()
+        n = steps if steps else 1
+        return f"{step},skinny,{up // n},{down // n},{su // n}"
+
     @property
     def launches(self):
         return self.lib.hc_patchset_launches(self.h)

@@ -50,6 +50,7 @@ def test_patch_split_is_bit_identical(split, order, bc, integ):
     active = lg.nx * lg.ny * lg.nz * 5
     assert ps.ledger() == (total * np_ * steps, total * np_ * steps, np_ * steps, np_ * steps,
                            active * np_ * steps, steps)
+    assert ps.ledger_csv_row(7) == f"7,skinny,{total * np_},{total * np_},{np_}"
     ps.close()
 
 

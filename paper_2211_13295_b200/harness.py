@@ -38,14 +38,17 @@ class RunConfig:
     gamma: float = 1.4
     exact: bool = True      # bit-exact build (False: FMA build)
     device: int = 0
+    split_x: int = 1        # patch split (harness.hpp:24): > 1 runs the device PatchSet
+    split_y: int = 1
+    split_z: int = 1
 
     def effective_cfl(self) -> float:
         return self.cfl if self.cfl > 0.0 else (0.6 if self.order == 2 else 0.4)
 
     def validate(self):
         """harness.cpp:60-69."""
-        if self.order not in (2, 3):
-            raise ValueError("order must be 2 or 3")
+        if self.order not in (2, 3, 4):
+            raise ValueError("order must be 2 or 3 (4: the WENO-AO extension)")
         if min(self.nx, self.ny, self.nz) < 4:
             raise ValueError("mesh must be at least 4^3")
         if self.t_final > 0.0 and self.steps > 0:
@@ -130,10 +133,16 @@ def run_simulation(cfg: RunConfig) -> RunResult:
         t_final = cfg.t_final if cfg.t_final > 0.0 else (0.2 if cfg.problem == SOD
                                                         else g.nx * g.dx / 1.0)
         nsteps = None
-    st = hydro.Stepper(g, hydro.make_params(cfg.order, cfg.solver, cfg.gamma), bc=(bc, bc, bc),
-                       exact=cfg.exact, device=cfg.device,
-                       integrator=INTEGRATORS[cfg.integrator])
-    st.upload(s)
+    params = hydro.make_params(cfg.order, cfg.solver, cfg.gamma)
+    if cfg.split_x * cfg.split_y * cfg.split_z > 1:  # transfer.cpp PatchSet, on the device
+        st = hydro.PatchSet(g, cfg.split_x, cfg.split_y, cfg.split_z, params, boundary=bc,
+                            exact=cfg.exact, device=cfg.device,
+                            integrator=INTEGRATORS[cfg.integrator])
+        st.scatter(s)
+    else:
+        st = hydro.Stepper(g, params, bc=(bc, bc, bc), exact=cfg.exact, device=cfg.device,
+                           integrator=INTEGRATORS[cfg.integrator])
+        st.upload(s)
     st.set_time(0.0, dt0, cfl, t_final)
     t0 = time.perf_counter()
     if nsteps is not None:
@@ -149,7 +158,7 @@ def run_simulation(cfg: RunConfig) -> RunResult:
             if done - before < 256:
                 break
     wall = time.perf_counter() - t0
-    out = st.download()
+    out = st.gather() if isinstance(st, hydro.PatchSet) else st.download()
     st.close()
     gh = g.ghost
     # the reference gathers active zones into a fresh SkinnyState (ghosts zero)
@@ -189,3 +198,41 @@ def run_convergence_study(cfg: RunConfig, meshes):
             r.errors.order_estimate = math.log(e_coarse / e_fine) / math.log(n / meshes[m - 1])
         rows.append((n, r.errors, r))
     return rows
+
+
+@dataclass
+class ReproReport:
+    """harness.hpp:75-81."""
+    serial_bit_identical: bool = False
+    multiworker_l1_diff: float = 0.0
+    max_abs_diff: float = 0.0
+    max_diff_zone: tuple = (0, 0, 0)
+    passed: bool = False
+
+
+def run_reproducibility_check(cfg: RunConfig) -> ReproReport:
+    """harness.cpp:229-271 on the device: two identical runs must agree bit for bit; the
+    "multi-worker" run -- on the GPU, a different decomposition (2 x 2 x 2 patches when the mesh
+    divides, else 2 x 1 x 1) -- is compared by the density L1 (pass below 1e-10)."""
+    base = RunConfig(**{**cfg.__dict__})
+    if base.steps <= 0:
+        base.steps, base.t_final = 50, -1.0
+    a = run_simulation(RunConfig(**base.__dict__))
+    b = run_simulation(RunConfig(**base.__dict__))
+    rep = ReproReport()
+    rep.serial_bit_identical = bool((a.final_state.view(np.uint64) ==
+                                     b.final_state.view(np.uint64)).all())
+    split = (2, 2, 2) if all(n % 2 == 0 and n // 2 >= 4 for n in (base.nx, base.ny, base.nz)) \
+        else (2, 1, 1)
+    c = run_simulation(RunConfig(**{**base.__dict__, "split_x": split[0], "split_y": split[1],
+                                    "split_z": split[2]}))
+    g = a.geom
+    gh = g.ghost
+    act = np.s_[gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx]
+    d = np.abs(a.final_state[act] - c.final_state[act])
+    rep.multiworker_l1_diff = float(d[..., 0].sum() / (g.nx * g.ny * g.nz))
+    k, j, i, _ = np.unravel_index(int(np.argmax(d)), d.shape)
+    rep.max_abs_diff = float(d.max())
+    rep.max_diff_zone = (int(i), int(j), int(k))
+    rep.passed = rep.serial_bit_identical and rep.multiworker_l1_diff < 1e-10
+    return rep

@@ -127,8 +127,8 @@ def run_reference_cpu(n, order, steps, threads):
     """The reference's own harness (hydro::run_benchmark, harness.cpp:222-227) from
     oracle/_ref (built from /root/reference/proj/src); zones/s as it computes it
     (harness.cpp:177-180). Falls back to the C restatement (single thread) if absent."""
-    os.environ.setdefault("OMP_PROC_BIND", "close")  # SURVEY 8(d), before libgomp loads
-    os.environ.setdefault("OMP_PLACES", "cores")
+    # (no OMP_PROC_BIND / OMP_PLACES: binding made the reference 5 % slower on the box,
+    # 6.30 vs 6.61 M/s, and the baseline must not be handicapped)
     from oracle import pyoracle as po
     if po.have_reference():
         ref = po.Reference()
@@ -572,8 +572,7 @@ def main():
         zps, kind, cores = run_reference_cpu(c_n, order, 2, threads)
         cpu = {"value": zps / 1e6, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{c_n}^3 O{order} HLL ADER vortex, 2 steps through "
-                         "hydro::run_benchmark (harness wall clock), OMP_PROC_BIND=close "
-                         "OMP_PLACES=cores"}
+                         "hydro::run_benchmark (harness wall clock), default OpenMP placement"}
         z1, _, _ = run_reference_cpu(128, order, 1, 1)  # also one thread
         cpu["single_thread"] = {"value": z1 / 1e6, "unit": UNIT, "cores": 1,
                                 "sample": f"128^3 O{order}, 1 step, 1 thread"}

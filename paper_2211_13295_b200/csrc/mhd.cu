@@ -162,8 +162,8 @@ template <bool SHIFT, int FAST>
 __device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const double* h,
                                                const double* id, double gamma, double* div,
                                                Fault& flt) {
-#pragma unroll
-    for (int A = 0; A < 3; ++A) {
+#pragma unroll 1
+    for (int A = 0; A < 3; ++A) {  // (not unrolled: three copies of the flux cost registers)
         double a[NM], b[NM], fa[NM], fb[NM];
 #pragma unroll
         for (int q = 0; q < NM; ++q) {

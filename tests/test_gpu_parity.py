@@ -388,3 +388,25 @@ def test_graph_replay_equals_plain_launches(api, integrator):
         st.close()
     (a, ta, la), (b, tb, lb) = outs
     assert same(a, b) and ta == tb and la == lb
+
+
+def test_fma_build_long_run_within_north_star_budget(api, orc):
+    """The north star's bar: <= 1e-10 relative L1 after N steps. 200 steps of the FMA build at
+    32^3 O3 against the oracle (reference-identical) run."""
+    g, go = geoms((32, 32, 32), 3)
+    s0 = api.init_isentropic_vortex(g, 3)
+    ref = s0.copy()
+    dts = _run_oracle(orc, go, 3, hydro.HLL, po.PERIODIC, ref, 200, 0.4)
+    st = hydro.Stepper(g, hydro.make_params(3), exact=False)
+    st.upload(s0)
+    st.set_time(0.0, dts[0], 0.4)
+    st.step(200)
+    st.sync()
+    out = st.download()
+    gh = g.ghost
+    a = out[gh:-gh, gh:-gh, gh:-gh].reshape(-1, 5)
+    b = ref[gh:-gh, gh:-gh, gh:-gh].reshape(-1, 5)
+    worst = max(np.abs(a[:, q] - b[:, q]).mean() / max(np.abs(b[:, q]).mean(), 1e-300)
+                for q in range(5))
+    assert worst <= 1e-10, worst
+    st.close()

@@ -115,36 +115,29 @@ __global__ void k_ced_cell(CArgs a) {
         a.w[size_t(q) * b.N + r] = ct::face_avg<O3>(a.s + size_t(q) * b.N, r, stride(b, q % 3));
 }
 
-template <bool O3>
-__global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
-    if (a.ctl->done) return;
+// One ring zone: reconstruction of the 6 cell variables, its 12 edge-midpoint states,
+// ADER predictor, tau/2. The six face states live in shared memory ([s][q][thread]) so the
+// variable loop need not be unrolled; FAST = 1 runs the branch-free bit-exact division of
+// pointwise.cuh and the caller re-runs the zone with FAST = 0 when a flag is raised.
+template <bool O3, int FAST>
+__device__ __forceinline__ void ced_zone(const CArgs& a, size_t o, double* fs, Fault& wf) {
     const Box& b = a.b;
-    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
-    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
-    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (r >= cnt) return;
-    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
-              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
-    const size_t o = at(b, k, j, i);
     const size_t st[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
     const double dt = a.ctl->dt;
     const size_t N = b.N;
-    double face[6][NF], u0[NF];
-    Fault wf;
-    wf.clear();
-#pragma unroll
+    auto face = [&](int f, int q) -> double& { return fs[(f * NF + q) * 128]; };
+#pragma unroll 1
     for (int q = 0; q < NF; ++q) {
-        const double* w = a.w + size_t(q) * N;
+        const double* __restrict__ w = a.w + size_t(q) * N;
         const double c0 = w[o];
-        u0[q] = c0;
         double lin[3], quad[3] = {0.0, 0.0, 0.0}, cross[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             const double up = w[o + st[d]], um = w[o - st[d]];
             if (!O3) lin[d] = mc_limiter(up - c0, c0 - um, a.lim.cfac_other);
-            else weno3<0>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
-            face[2 * d][q] = extrap<O3>(c0, +1.0, lin[d], quad[d]);
-            face[2 * d + 1][q] = extrap<O3>(c0, -1.0, lin[d], quad[d]);
+            else weno3<FAST>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
+            face(2 * d, q) = extrap<O3>(c0, +1.0, lin[d], quad[d]);
+            face(2 * d + 1, q) = extrap<O3>(c0, -1.0, lin[d], quad[d]);
             if (O3) {
                 const size_t sa = st[d], sb = st[(d + 1) % 3];
                 cross[d] =
@@ -165,7 +158,7 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
                     if (O3)
                         v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
                             (xa * xb) * cross[AA];
-                    a.states[(size_t(4 * C + 2 * lb + la) * NF + q) * N + o] = v;
+                    __stcs(a.states + (size_t(4 * C + 2 * lb + la) * NF + q) * N + o, v);
                 }
         }
     }
@@ -183,8 +176,8 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
             double ua[NF], ub[NF], fa[NF], fb[NF];
 #pragma unroll
             for (int q = 0; q < NF; ++q) {
-                ua[q] = pass ? face[2 * A][q] + 0.5 * tau[q] : face[2 * A][q];
-                ub[q] = pass ? face[2 * A + 1][q] + 0.5 * tau[q] : face[2 * A + 1][q];
+                ua[q] = pass ? face(2 * A, q) + 0.5 * tau[q] : face(2 * A, q);
+                ub[q] = pass ? face(2 * A + 1, q) + 0.5 * tau[q] : face(2 * A + 1, q);
             }
             if (A == 0) { maxwell_flux<0>(ua, ie, im, fa); maxwell_flux<0>(ub, ie, im, fb); }
             if (A == 1) { maxwell_flux<1>(ua, ie, im, fa); maxwell_flux<1>(ub, ie, im, fb); }
@@ -195,14 +188,41 @@ __global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
         }
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const double dh = ex * u0[q] + ph * (0.5 * dt) * (-div[q]);
-            tau[q] = 2.0 * (dh - u0[q]);
+            const double u0 = a.w[size_t(q) * N + o];
+            const double dh = ex * u0 + ph * (0.5 * dt) * (-div[q]);
+            tau[q] = 2.0 * (dh - u0);
         }
 #pragma unroll
         for (int q = 3; q < NF; ++q) tau[q] = -dt * div[q];
     }
 #pragma unroll
-    for (int q = 0; q < NF; ++q) a.ht[size_t(q) * N + o] = 0.5 * tau[q];
+    for (int q = 0; q < NF; ++q) __stcs(a.ht + size_t(q) * N + o, 0.5 * tau[q]);
+}
+
+template <bool O3>
+__device__ __noinline__ void ced_zone_careful(const CArgs& a, size_t o, double* fs) {
+    Fault f;
+    f.clear();
+    ced_zone<O3, 0>(a, o, fs, f);
+}
+
+template <bool O3>
+__global__ void __launch_bounds__(128) k_ced_predict(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
+              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
+    const size_t o = at(b, k, j, i);
+    __shared__ double sface[6 * NF * 128];
+    double* fs = sface + threadIdx.x;
+    Fault wf;
+    wf.clear();
+    ced_zone<O3, 1>(a, o, fs, wf);
+    if (wf.redo()) ced_zone_careful<O3>(a, o, fs);  // (WENO3 raises no physical faults)
 }
 
 template <bool O3, int C>

@@ -64,18 +64,24 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic
             lo_ghost.copy_(hi_act)
             hi_ghost.copy_(lo_act)
     else:
+        # Message matching is in posting order per peer pair, and at world 2 (periodic) the
+        # neighbour below IS the neighbour above: post "send down, receive from above, send
+        # up, receive from below" on every rank so the k-th send to a peer always meets that
+        # peer's k-th receive (lowest active planes -> its top ghosts, then highest -> its
+        # bottom ghosts).
         ops = []
         bufs = []
+        rb = torch.empty_like(lo_ghost) if below is not None else None
+        ra = torch.empty_like(hi_ghost) if above is not None else None
         if below is not None:
-            rb = torch.empty_like(lo_ghost)
             ops.append(dist.P2POp(dist.isend, lo_act.contiguous(), below, group))
+        if above is not None:
+            ops.append(dist.P2POp(dist.irecv, ra, above, group))
+            ops.append(dist.P2POp(dist.isend, hi_act.contiguous(), above, group))
+            bufs.append((hi_ghost, ra))
+        if below is not None:
             ops.append(dist.P2POp(dist.irecv, rb, below, group))
             bufs.append((lo_ghost, rb))
-        if above is not None:
-            ra = torch.empty_like(hi_ghost)
-            ops.append(dist.P2POp(dist.isend, hi_act.contiguous(), above, group))
-            ops.append(dist.P2POp(dist.irecv, ra, above, group))
-            bufs.append((hi_ghost, ra))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()

@@ -42,7 +42,7 @@ def _worker(rank, world, port, order, bc, steps, nx, nzg, q):
         nloc = z1 - z0
         g = slab_geom(nx, nloc, z0, order, d)
         gglob = slab_geom(nx, nzg, 0, order, d)
-        full = orc.init_sod(gglob) if bc == po.OUTFLOW else orc.init_isentropic_vortex(gglob, order)
+        full = _full_state(orc, gglob, order, bc)
         gh = g.ghost
         s = np.ascontiguousarray(full[z0:z1 + 2 * gh])  # slab + its ghost planes (refilled)
         cfl = 0.6 if order == 2 else 0.4
@@ -85,11 +85,22 @@ def run_slabs(world, order, bc, steps, nx=8, nzg=16):
     return np.concatenate([x[1] for x in res], axis=0), res[0][2], [x[2] for x in res]
 
 
+def _full_state(orc, g, order, bc):
+    """the problem's IC with a smooth z-dependent density/energy modulation: the vortex and
+    Sod are z-invariant, so without it a swapped z halo would go unnoticed"""
+    s = orc.init_sod(g) if bc == po.OUTFLOW else orc.init_isentropic_vortex(g, order)
+    z = np.arange(s.shape[0], dtype=float)
+    mod = 1.0 + 0.05 * np.sin(0.7 * z + 0.3) + 0.02 * np.cos(1.9 * z)
+    s[..., 0] *= mod[:, None, None]
+    s[..., 4] *= mod[:, None, None]
+    return s
+
+
 def run_single(order, bc, steps, nx=8, nzg=16):
     orc = po.Oracle()
     d = 10.0 / nx
     g = slab_geom(nx, nzg, 0, order, d)
-    s = orc.init_sod(g) if bc == po.OUTFLOW else orc.init_isentropic_vortex(g, order)
+    s = _full_state(orc, g, order, bc)
     cfl = 0.6 if order == 2 else 0.4
     dts = orc.run_steps(g, po.make_params(order), bc, cfl, steps, s, orc.initial_dt(g, s, cfl))
     gh = g.ghost

@@ -82,9 +82,17 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic
         if below is not None:
             ops.append(dist.P2POp(dist.irecv, rb, below, group))
             bufs.append((lo_ghost, rb))
+        staged = planes.is_cuda and dist.get_backend(group) == "gloo"
+        if staged:  # gloo moves host memory only (testing N>1 on one GPU): stage through it
+            ops = [dist.P2POp(op.op, op.tensor.cpu() if op.op is dist.isend else
+                              torch.empty(op.tensor.shape, dtype=op.tensor.dtype), op.peer,
+                              op.group) for op in ops]
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
+        if staged:
+            recvs = iter([op.tensor for op in ops if op.op is dist.irecv])
+            bufs = [(dst, next(recvs)) for dst, _ in bufs]
         for dst, src in bufs:
             dst.copy_(src)
     if not periodic:

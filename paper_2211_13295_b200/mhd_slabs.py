@@ -48,11 +48,15 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=No
         hi_ghost.copy_(lo_send.clone())
         return
     below, above = (rank - 1) % world, (rank + 1) % world
-    rb = torch.empty_like(lo_ghost)
-    ra = torch.empty_like(hi_ghost)
-    ops = [dist.P2POp(dist.isend, lo_send.contiguous(), below, group),
+    # gloo moves host memory only (multi-rank tests on one GPU): stage through it
+    dev = "cpu" if planes.is_cuda and dist.get_backend(group) == "gloo" else planes.device
+    rb = torch.empty(lo_ghost.shape, dtype=planes.dtype, device=dev)
+    ra = torch.empty(hi_ghost.shape, dtype=planes.dtype, device=dev)
+    # posting order "send down, receive from above, send up, receive from below" matches
+    # sends and receives per peer even when below == above (world 2)
+    ops = [dist.P2POp(dist.isend, lo_send.contiguous().to(dev), below, group),
            dist.P2POp(dist.irecv, ra, above, group),
-           dist.P2POp(dist.isend, hi_send.contiguous(), above, group),
+           dist.P2POp(dist.isend, hi_send.contiguous().to(dev), above, group),
            dist.P2POp(dist.irecv, rb, below, group)]
     for w in dist.batch_isend_irecv(ops):
         w.wait()

@@ -31,3 +31,13 @@ def test_multirank_slab_run_on_one_gpu(world):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"world {world}: decomposed == single domain: True" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_mhd_slab_run_on_one_gpu(world):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.join(ROOT, "tools", "mhd_slab_gloo_gpu.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"mhd world {world}: decomposed == single domain: True" in r.stdout

@@ -60,6 +60,11 @@ int hc_mhd_cfl_dt(hc_mhd* m, double cfl, double* dt);
 int hc_mhd_max_divb(hc_mhd* m, double* out);
 /* kernels launched so far on this stepper */
 long hc_mhd_launches(hc_mhd* m);
+/* zone updates the pressure floor (p <= 1e-10 after an update -> energy raised to p = 1e-10)
+ * touched so far; with the positivity fallback of the solver states (reconstructed states
+ * with rho <= 0 or p <= 0 are replaced by the zone's cell average) the robustness measures of
+ * this extension -- 0 on smooth problems */
+int hc_mhd_floored(hc_mhd* m, unsigned long long* count);
 /* the cudaStream_t every call of this stepper runs on (for event timing) */
 int hc_mhd_stream(hc_mhd* m, void** stream);
 /* run every later call on `stream` (a cudaStream_t owned by the caller) */

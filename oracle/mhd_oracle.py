@@ -97,17 +97,33 @@ def fill_ghosts(s, g: Geom, bc):
 
 # ----------------------------------------------------------------------------- physics
 
-def prim(c, gamma):
+def prim(c, gamma, check=True):
     rho = c[0]
-    if not np.all(rho > 0.0):
+    if check and not np.all(rho > 0.0):
         raise Unphysical("non-positive density")
-    inv = 1.0 / rho
-    u = [c[1] * inv, c[2] * inv, c[3] * inv]
-    b2 = c[5] * c[5] + c[6] * c[6] + c[7] * c[7]
-    p = (gamma - 1.0) * (c[4] - 0.5 * (c[1] * u[0] + c[2] * u[1] + c[3] * u[2]) - 0.5 * b2)
-    if not np.all(p > 0.0):
+    with np.errstate(all="ignore"):
+        inv = 1.0 / rho
+        u = [c[1] * inv, c[2] * inv, c[3] * inv]
+        b2 = c[5] * c[5] + c[6] * c[6] + c[7] * c[7]
+        p = (gamma - 1.0) * (c[4] - 0.5 * (c[1] * u[0] + c[2] * u[1] + c[3] * u[2]) - 0.5 * b2)
+    if check and not np.all(p > 0.0):
         raise Unphysical("non-positive pressure")
     return rho, u, p, b2, inv
+
+
+def unphysical(c, gamma):
+    """mask of states with rho <= 0 or p <= 0 (NaN counts as unphysical)"""
+    rho, u, p, b2, inv = prim(c, gamma, check=False)
+    return ~(rho > 0.0) | ~(p > 0.0)
+
+
+def positive_or_average(u, w, sel_fn, gamma):
+    """mhd.cu positive_or_average: states with rho <= 0 or p <= 0 take the zone's cell average
+    (w: the 8 cell-centred arrays, sel_fn maps a box array to the states' zones)"""
+    bad = unphysical(u, gamma)
+    if not np.any(bad):
+        return u
+    return [np.where(bad, sel_fn(w[q]), u[q]) for q in range(NM)]
 
 
 def fast_speed(c, pr, gamma, A):
@@ -191,14 +207,18 @@ def cell_vars(s, o3=False):
     return w
 
 
-def divergence(face, h, idd, gamma):
+def divergence(face, h, idd, gamma, bad):
+    """predictor.cpp:12-22 with the MHD flux; `bad` accumulates zones with an unphysical
+    face state (those zones' tau is zeroed by the caller, as mhd.cu does)"""
     div = None
     for A in range(3):
         a = [face[2 * A][q] + h[q] if h is not None else face[2 * A][q] for q in range(NM)]
         b = [face[2 * A + 1][q] + h[q] if h is not None else face[2 * A + 1][q]
              for q in range(NM)]
-        fa = mhd_flux(a, prim(a, gamma), A)
-        fb = mhd_flux(b, prim(b, gamma), A)
+        bad |= unphysical(a, gamma) | unphysical(b, gamma)
+        with np.errstate(all="ignore"):
+            fa = mhd_flux(a, prim(a, gamma, check=False), A)
+            fb = mhd_flux(b, prim(b, gamma, check=False), A)
         if A == 0:
             div = [(fa[q] - fb[q]) * idd[0] for q in range(NM)]
         else:
@@ -263,12 +283,16 @@ def predict(s, g: Geom, par: Params, dt):
                 mm = sh(w[q], [-da[x] - db[x] for x in range(3)])
                 cross[d][q] = 0.25 * ((pp - pm) - (mp - mm))
     idd = [1.0 / g.d[0], 1.0 / g.d[1], 1.0 / g.d[2]]
-    div = divergence(face, None, idd, par.gamma)
-    tau = [(-dt) * div[q] for q in range(NM)]
-    if o3:
-        h = [0.5 * tau[q] for q in range(NM)]
-        div = divergence(face, h, idd, par.gamma)
+    bad = np.zeros(u0[0].shape, dtype=bool)
+    with np.errstate(all="ignore"):
+        div = divergence(face, None, idd, par.gamma, bad)
         tau = [(-dt) * div[q] for q in range(NM)]
+        if o3:
+            h = [0.5 * tau[q] for q in range(NM)]
+            div = divergence(face, h, idd, par.gamma, bad)
+            tau = [(-dt) * div[q] for q in range(NM)]
+    # mhd.cu: an unphysical predictor state zeroes the zone's tau (first order in time)
+    tau = [np.where(bad, 0.0, tau[q]) for q in range(NM)]
 
     def box(v):
         out = np.zeros((R, Q, P))
@@ -279,6 +303,8 @@ def predict(s, g: Geom, par: Params, dt):
     # faces s = 2A (+A), 2A+1 (-A); edge midpoints s = 6 + 4C + 2 lb + la at
     # (xa, xb) = (la ? -1/2 : +1/2, lb ? -1/2 : +1/2) in the (C+1, C+2) plane
     m = Modes()
+    # cell averages with B = mean of the zone's face pair: the consumers' positivity fallback
+    m.w = cell_vars(s, False)
     m.ht = [box(0.5 * tau[q]) for q in range(NM)]
     m.st = [[None] * NM for _ in range(18)]
     for q in range(NM):
@@ -304,7 +330,11 @@ def face_fluxes(m, g: Geom, par: Params, A):
     valid at faces 0..n_A, active transverse."""
     ul = [_shift(m.st[2 * A][q], A, -1) + _shift(m.ht[q], A, -1) for q in range(NM)]
     ur = [m.st[2 * A + 1][q] + m.ht[q] for q in range(NM)]
+    ul = positive_or_average(ul, m.w, lambda x: _shift(x, A, -1), par.gamma)
+    ur = positive_or_average(ur, m.w, lambda x: x, par.gamma)
     bn = 0.5 * (ul[5 + A] + ur[5 + A])
+    ul[4] = ul[4] + 0.5 * (bn * bn - ul[5 + A] * ul[5 + A])
+    ur[4] = ur[4] + 0.5 * (bn * bn - ur[5 + A] * ur[5 + A])
     ul[5 + A] = bn
     ur[5 + A] = bn
     sel = [slice(None)] * 3
@@ -348,6 +378,7 @@ def edge_emf(m, g: Geom, par: Params, C):
                     out = _shift(out, BB, -1)
                 return out[sel]
             u = [z(m.st[6 + 4 * C + 2 * lb + la][q]) + z(m.ht[q]) for q in range(NM)]
+            u = positive_or_average(u, m.w, z, par.gamma)
             pr = prim(u, par.gamma)
             vel = pr[1]
             ec[la, lb] = vel[BB] * u[5 + AA] - vel[AA] * u[5 + BB]
@@ -403,6 +434,26 @@ def update(s, F, E, g: Geom, dt):
     return s
 
 
+P_FLOOR = 1.0e-10  # mhd.cu P_FLOOR
+
+
+def pressure_floor(s, g: Geom, par: Params):
+    """mhd.cu zone_dt(floor=true): active zones whose pressure (B = mean of the zone's face
+    pair) is <= P_FLOOR get E raised to p = P_FLOOR; returns how many"""
+    w = cell_vars(s, False)
+    gh = g.gh
+    act = (slice(gh, gh + g.n[2]), slice(gh, gh + g.n[1]), slice(gh, gh + g.n[0]))
+    u = [x[act] for x in w]
+    rho, v, p, b2, inv = prim(u, par.gamma, check=False)
+    bad = (rho > 0.0) & ~(p > P_FLOOR)
+    if not np.any(bad):
+        return 0
+    e = (P_FLOOR / (par.gamma - 1.0) + 0.5 * (u[1] * v[0] + u[2] * v[1] + u[3] * v[2])
+         + 0.5 * b2)
+    s[4][act] = np.where(bad, e, s[4][act])
+    return int(np.count_nonzero(bad))
+
+
 def cfl_dt(s, g: Geom, par: Params, cfl):
     # each zone's own two faces (mean): no ghost face enters, so the estimate is the same
     # under any domain decomposition
@@ -439,6 +490,7 @@ def compute(s, g: Geom, par: Params, dt, cfl):
     F = [face_fluxes(m, g, par, A) for A in range(3)]
     E = [edge_emf(m, g, par, C) for C in range(3)]
     update(s, F, E, g, dt)
+    pressure_floor(s, g, par)
     return cfl_dt(s, g, par, cfl)
 
 

@@ -62,6 +62,7 @@ struct MArgs {
     int bc[3];
     StepCtl* ctl;
     ErrBlock* eb;
+    unsigned long long* floored;  // zones the pressure floor touched (k_mhd_dt)
 };
 
 // --------------------------------------------------------------------------- physics
@@ -359,7 +360,12 @@ __global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
     predict_zone<O3, 1>(a, o, face, dt, f);
     if (f.redo()) {
         Fault c = predict_zone_careful<O3>(a, o, face, dt);
-        if (c.code) record_fault(a.eb, ST_PREDICT, c, i - b.gh, j - b.gh, k - b.gh, 0);
+        // an unphysical reconstructed state in the predictor: this zone goes first order in
+        // time (tau = 0); its solver states are checked again by their consumers, which fall
+        // back to the cell average (positivity fallback; only unphysical averages are errors)
+        if (c.code)
+#pragma unroll
+            for (int q = 0; q < NM; ++q) a.ht[size_t(q) * b.N + o] = 0.0;
     }
 }
 
@@ -369,6 +375,20 @@ __device__ __forceinline__ void half_state(const MArgs& a, size_t o, int s, doub
 #pragma unroll
     for (int q = 0; q < NM; ++q)
         u[q] = __ldg(a.states + (size_t(s) * NM + q) * N + o) + __ldg(a.ht + size_t(q) * N + o);
+}
+
+// Positivity fallback: a half-time state with rho <= 0 or p <= 0 is replaced by the zone's
+// cell average (fluid variables, B as the mean of the zone's face pair -- the state the
+// pressure floor of k_mhd_dt guarantees); when even that is unphysical the caller's solver
+// records the fault.
+__device__ __forceinline__ void positive_or_average(const MArgs& a, size_t o, double gamma,
+                                                    double* u) {
+    Fault t;
+    t.clear();
+    (void)mhd_prim(u, gamma, t);
+    if (!t.code) return;
+#pragma unroll
+    for (int q = 0; q < NM; ++q) u[q] = cellvar<false>(a, q, o);  // (mean B: see k_mhd_dt)
 }
 
 template <bool O3, int A>
@@ -390,7 +410,13 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     double ul[NM], ur[NM], f5[5];
     half_state(a, ol, 2 * A, ul);      // +A face of the left zone
     half_state(a, o, 2 * A + 1, ur);   // -A face of the right zone
+    positive_or_average(a, ol, a.gamma, ul);
+    positive_or_average(a, o, a.gamma, ur);
+    // single-valued normal field; the energies absorb the change of B_n^2/2 so the states
+    // keep their pressures (a positive state stays positive)
     const double bn = 0.5 * (ul[5 + A] + ur[5 + A]);
+    ul[4] = ul[4] + 0.5 * (bn * bn - ul[5 + A] * ul[5 + A]);
+    ur[4] = ur[4] + 0.5 * (bn * bn - ur[5 + A] * ur[5 + A]);
     ul[5 + A] = bn;
     ur[5 + A] = bn;
     Fault f;
@@ -437,6 +463,7 @@ __global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
             const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
             double u[NM];
             half_state(a, z, 6 + 4 * C + 2 * lb + la, u);
+            positive_or_average(a, z, a.gamma, u);
             MPrim p = mhd_prim(u, a.gamma, f);
             ec[la][lb] = p.u[BB] * u[5 + AA] - p.u[AA] * u[5 + BB];
             ba[la][lb] = u[5 + AA];
@@ -498,13 +525,30 @@ __global__ void k_mhd_update(MArgs a) {
 }
 
 // CFL estimate of a zone (eval_tstep_ptwise shape with the fast speed), exact min
+// pressure floor applied after every update (robustness of the extension, not part of any
+// reference scheme): zones whose pressure fell to <= P_FLOOR get their energy raised to
+// p = P_FLOOR, and are counted (hc_mhd_floored)
+constexpr double P_FLOOR = 1.0e-10;
+
 template <bool O3>
-__device__ __forceinline__ double zone_dt(const MArgs& a, size_t o, double cfl, Fault& f) {
+__device__ __forceinline__ double zone_dt(const MArgs& a, size_t o, double cfl, Fault& f,
+                                          bool floor) {
     // the zone's own two faces only (mean): the estimate must not read ghost faces, which
     // are stale after the update, so it is identical under any domain decomposition
     double u[NM];
 #pragma unroll
     for (int q = 0; q < NM; ++q) u[q] = cellvar<false>(a, q, o);
+    if (floor && u[0] > 0.0) {
+        Fault t;
+        t.clear();
+        MPrim q0 = mhd_prim(u, a.gamma, t);
+        if (!(q0.p > P_FLOOR)) {
+            u[4] = P_FLOOR / (a.gamma - 1.0) +
+                   0.5 * (u[1] * q0.u[0] + u[2] * q0.u[1] + u[3] * q0.u[2]) + 0.5 * q0.b2;
+            a.s[size_t(4) * a.b.N + o] = u[4];
+            atomicAdd(a.floored, 1ull);
+        }
+    }
     MPrim p = mhd_prim(u, a.gamma, f);
     const double sx = fabs(p.u[0]) + fast_speed<0>(u, p, a.gamma);
     const double sy = fabs(p.u[1]) + fast_speed<1>(u, p, a.gamma);
@@ -524,7 +568,8 @@ __global__ void k_mhd_dt(MArgs a, double cfl, double* out, int stage) {
                   k = int(r / (size_t(b.n[0]) * b.n[1]));
         Fault f;
         f.clear();
-        const double v = zone_dt<O3>(a, at(b, k + b.gh, j + b.gh, i + b.gh), cfl, f);
+        const double v =
+            zone_dt<O3>(a, at(b, k + b.gh, j + b.gh, i + b.gh), cfl, f, stage == ST_UPDATE);
         if (f.code) record_fault(a.eb, stage, f, i, j, k, 0);
         else d = v;
     }
@@ -598,6 +643,7 @@ struct hc_mhd {
     double* emf = nullptr;
     double* bc = nullptr;
     double* scratch = nullptr;  // one double for reductions
+    unsigned long long* floored = nullptr;
     StepCtl* ctl = nullptr;
     ErrBlock* eb = nullptr;
     cudaStream_t st = nullptr;
@@ -628,6 +674,7 @@ MArgs margs(const hc_mhd* m) {
     for (int d = 0; d < 3; ++d) a.bc[d] = m->p.bc[d];
     a.ctl = m->ctl;
     a.eb = m->eb;
+    a.floored = m->floored;
     return a;
 }
 
@@ -740,6 +787,8 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, sizeof(double) * 3 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->bc, sizeof(double) * 3 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->scratch, sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&m->floored, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(m->floored, 0, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&m->ctl, sizeof(StepCtl));
     if (e == cudaSuccess) e = cudaMalloc(&m->eb, sizeof(ErrBlock));
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->st, cudaStreamNonBlocking);
@@ -771,6 +820,7 @@ int hc_mhd_destroy(hc_mhd* m) {
     cudaFree(m->emf);
     cudaFree(m->bc);
     cudaFree(m->scratch);
+    cudaFree(m->floored);
     cudaFree(m->ctl);
     cudaFree(m->eb);
     if (m->st && m->own_stream) cudaStreamDestroy(m->st);
@@ -858,6 +908,13 @@ int hc_mhd_max_divb(hc_mhd* m, double* out) {
 }
 
 long hc_mhd_launches(hc_mhd* m) { return m ? m->launches : 0; }
+
+int hc_mhd_floored(hc_mhd* m, unsigned long long* count) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    HC_CUDA(cudaMemcpyAsync(count, m->floored, sizeof *count, cudaMemcpyDeviceToHost, m->st));
+    HC_CUDA(cudaStreamSynchronize(m->st));
+    return HC_OK;
+}
 
 int hc_mhd_stream(hc_mhd* m, void** stream) {
     *stream = m->st;

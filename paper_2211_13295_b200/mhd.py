@@ -114,6 +114,13 @@ class MhdStepper:
     def launches(self):
         return self.lib.hc_mhd_launches(self.h)
 
+    @property
+    def floored(self):
+        """zone updates the pressure floor touched so far (hc_mhd_floored)"""
+        v = C.c_ulonglong()
+        _check(self.lib.hc_mhd_floored(self.h, C.byref(v)))
+        return v.value
+
     def set_stream(self, ptr):
         _check(self.lib.hc_mhd_set_stream(self.h, C.c_void_p(ptr)))
 
@@ -344,4 +351,35 @@ def random_field(g: Geom, order, seed=3, gamma=5.0 / 3.0, amp=0.3, modes=4):
     s = np.zeros(state_shape(g))
     s[:5] = _cells_from_point(g, order, point, z_invariant=False)
     s[5], s[6], s[7] = _faces_from_potential(g, afun[0], afun[1], afun[2])
+    return s
+
+
+def rotor(g: Geom, order, gamma=1.4):
+    """Balsara & Spicer (1999) MHD rotor on [0,1]^2 (z-invariant): a dense (rho = 10) disk of
+    radius 0.1 spinning at omega = 20 in a light (rho = 1) medium at rest, tapered linearly to
+    r = 0.115; p = 1, B = (5 / sqrt(4 pi), 0, 0) uniform (a constant Bx from Az = B0 y)."""
+    r0, r1, w0 = 0.1, 0.115, 20.0
+    b0 = 5.0 / math.sqrt(4 * math.pi)
+
+    def point(x, y, z):
+        dx, dy = x - 0.5, y - 0.5
+        r = np.sqrt(dx * dx + dy * dy) + 0.0 * z
+        f = np.clip((r1 - r) / (r1 - r0), 0.0, 1.0)
+        inside = r < r0
+        rho = np.where(inside, 10.0, 1.0 + 9.0 * f)
+        fac = np.where(inside, 1.0, f * r0 / np.maximum(r, 1e-300))
+        vx = -w0 * dy * fac
+        vy = w0 * dx * fac
+        zero = 0.0 * r
+        return rho, vx, vy, zero, 1.0 + zero, b0 + zero, zero, zero, gamma
+
+    def az(x, y, z):
+        return -b0 * y + 0.0 * (x + z)  # Bx = dAz/dy ... sign: bx = (Az(y+) - Az(y-))/dy
+
+    def zero(x, y, z):
+        return 0.0 * (x + y + z)
+
+    s = np.zeros(state_shape(g))
+    s[:5] = _cells_from_point(g, order, point)
+    s[5], s[6], s[7] = _faces_from_potential(g, zero, zero, lambda x, y, zz: b0 * y + 0.0 * (x + zz))
     return s

@@ -125,33 +125,36 @@ constexpr int FM = HC_REASSOC ? 2 : 1;
 // for physical states, so the triple products stay far from over/underflow.
 template <int FAST>
 __device__ __forceinline__ void weno3_1div(double s0, double s1, double s2, double s3,
-                                           double s4, const Limiter& L, double& ux, double& uxx,
-                                           Fault& f) {
+                                           double s4, const Limiter& L, double& ux2,
+                                           double& uxx2, Fault& f) {
+    // doubled slopes and 4 eps as in weno3_2x: returns (2 ux, 2 uxx)
     double d0 = s1 - s0, d1 = s2 - s1, d2 = s3 - s2, d3 = s4 - s3;
-    double ux_l = 0.5 * (3.0 * d1 - d0);
-    double uxx_l = 0.5 * (d1 - d0);
-    double ux_c = 0.5 * (d1 + d2);
-    double uxx_c = 0.5 * (d2 - d1);
-    double ux_r = 0.5 * (3.0 * d2 - d3);
-    double uxx_r = 0.5 * (d3 - d2);
+    double ux_l = 3.0 * d1 - d0;
+    double uxx_l = d1 - d0;
+    double ux_c = d1 + d2;
+    double uxx_c = d2 - d1;
+    double ux_r = 3.0 * d2 - d3;
+    double uxx_r = d3 - d2;
     const double k2 = 13.0 / 3.0;
-    double el = L.eps + (ux_l * ux_l + k2 * uxx_l * uxx_l);
-    double ec = L.eps + (ux_c * ux_c + k2 * uxx_c * uxx_c);
-    double er = L.eps + (ux_r * ux_r + k2 * uxx_r * uxx_r);
+    const double eps4 = 4.0 * L.eps;
+    double el = eps4 + (ux_l * ux_l + k2 * uxx_l * uxx_l);
+    double ec = eps4 + (ux_c * ux_c + k2 * uxx_c * uxx_c);
+    double er = eps4 + (ux_r * ux_r + k2 * uxx_r * uxx_r);
     double pl = el * el, pc = ec * ec, pr = er * er;
     double al = L.w0 * (pc * pr), ac = L.w1 * (pl * pr), ar = L.w2 * (pl * pc);
     double inv = ddiv<FAST>(1.0, al + ac + ar, f);
-    ux = (al * ux_l + ac * ux_c + ar * ux_r) * inv;
-    uxx = (al * uxx_l + ac * uxx_c + ar * uxx_r) * inv;
+    ux2 = (al * ux_l + ac * ux_c + ar * ux_r) * inv;
+    uxx2 = (al * uxx_l + ac * uxx_c + ar * uxx_r) * inv;
 }
 
+// both return twice the slopes (consumers: extrap2)
 template <int FAST>
 __device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double s3, double s4,
-                                        const Limiter& L, double& ux, double& uxx, Fault& f) {
+                                        const Limiter& L, double& ux2, double& uxx2, Fault& f) {
     if (HC_REASSOC)
-        weno3_1div<FAST>(s0, s1, s2, s3, s4, L, ux, uxx, f);
+        weno3_1div<FAST>(s0, s1, s2, s3, s4, L, ux2, uxx2, f);
     else
-        weno3<FAST>(s0, s1, s2, s3, s4, L, ux, uxx, f);
+        weno3_2x<FAST>(s0, s1, s2, s3, s4, L, ux2, uxx2, f);
 }
 
 // Face states (extrapolate_to_face + 0.5 * tau, corrector.cpp:30-33) of one zone from its
@@ -199,12 +202,12 @@ __device__ __forceinline__ void zone_states(const double* pc, int row, const dou
             weno3_k<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q],
                           a.lim, uy, uyy, f);
             weno3_k<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, uz, uzz, f);
-            face[0][q] = extrap<true>(u0, +1.0, ux, uxx);
-            face[1][q] = extrap<true>(u0, -1.0, ux, uxx);
-            face[2][q] = extrap<true>(u0, +1.0, uy, uyy);
-            face[3][q] = extrap<true>(u0, -1.0, uy, uyy);
-            face[4][q] = extrap<true>(u0, +1.0, uz, uzz);
-            face[5][q] = extrap<true>(u0, -1.0, uz, uzz);
+            face[0][q] = extrap2<true>(u0, +1.0, ux, uxx);  // doubled modes
+            face[1][q] = extrap2<true>(u0, -1.0, ux, uxx);
+            face[2][q] = extrap2<true>(u0, +1.0, uy, uyy);
+            face[3][q] = extrap2<true>(u0, -1.0, uy, uyy);
+            face[4][q] = extrap2<true>(u0, +1.0, uz, uzz);
+            face[5][q] = extrap2<true>(u0, -1.0, uz, uzz);
         }
     }
     double tau[NV];

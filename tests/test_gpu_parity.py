@@ -212,10 +212,15 @@ def test_fused_rk_stepper_bitwise(api, orc, order, nst, bc, n):
     assert same(out[act], s[act])
 
 
-@pytest.mark.parametrize("order,bc,chunks", [(3, hydro.PERIODIC, 5), (2, hydro.OUTFLOW, 3),
-                                             (3, hydro.PERIODIC, 1)])
-def test_pipelined_host_step_equals_device_step(api, order, bc, chunks):
-    """hc_stepper_step_host (H2D / fused / D2H overlapped by z-chunks) == resident steps."""
+@pytest.mark.parametrize("order,bc,chunks,inplace", [(3, hydro.PERIODIC, 5, True),
+                                                     (2, hydro.OUTFLOW, 3, True),
+                                                     (3, hydro.PERIODIC, 1, True),
+                                                     (3, hydro.PERIODIC, 4, False),
+                                                     (2, hydro.PERIODIC, 2, False)])
+def test_pipelined_host_step_equals_device_step(api, order, bc, chunks, inplace):
+    """hc_stepper_step_host (H2D / fused / D2H overlapped by z-chunks) == resident steps; in
+    place (whole-plane copies) and into a separate buffer (active-zone copies), the caller's
+    ghost zones untouched either way."""
     from tests.zmod import modulate_z
     g = hydro.make_geometry(20, 12, 23, order)
     s0 = modulate_z(api.init_isentropic_vortex(g, order))  # z chunks see different data
@@ -235,12 +240,20 @@ def test_pipelined_host_step_equals_device_step(api, order, bc, chunks):
     ghost[gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx] = False
     host[ghost] = np.nan  # only active zones cross PCIe; the device fills the ghosts
     for _ in range(3):
-        b.step_host(host, host, chunks)  # in place, like the bench's e2e loop
+        if inplace:
+            b.step_host(host, host, chunks)  # like the bench's e2e loop
+        else:
+            out = np.full_like(host, -7.0)
+            b.step_host(host, out, chunks)
+            assert (out[ghost] == -7.0).all()
+            host = out
+            host[ghost] = np.nan
     tb = b.sync()
     gh = g.ghost
     act = np.s_[gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx]
     assert ta == tb
     assert same(host[act], ra[act])
+    assert np.isnan(host[ghost]).all()
 
 
 def test_fused_stepper_c1_golden(api):

@@ -446,11 +446,62 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                     for (int q = 0; q < NV; ++q) YP[((cj + 1) * TX + ci) * NV + q] = st[2][q];
             }
         }
+        // z face at the bottom of plane p and the finalisation of plane p-1 need only this
+        // thread's own data (its +z state of p-1 and -z state of p, its carried partial rate
+        // and bottom flux of p-1): done before the barrier, so only the x/y states stay live
+        if (owned) {
+            if (lp >= 0) {
+                double fz_cur[NV];
+                {
+                    Fault f;
+                    f.clear();
+                    face_flux<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
+                }
+                if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
+                    const double* u = P(p - 1) + zoff_c * NV;
+                    const size_t zi = size_t(p - 1 + a.gh) * plane_stride +
+                                      size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
+                    double un[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        double r = part[q * CS] - cz * (fz_cur[q] - fz_prev[q * CS]);
+                        if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
+                            un[q] = a.rk_a * ustart[zi + q] + a.rk_b * (u[q] + r);
+                        else
+                            un[q] = u[q] + r;
+                    }
+                    double* dst = uout + zi;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                    if (!RK || a.want_dt) {
+                        Fault f;
+                        f.clear();
+                        double d = FM == 2 ? eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz,
+                                                                a.gamma, f)
+                                           : eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz,
+                                                            a.gamma, f);
+                        if (f.redo()) {
+                            V5 u5;
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
+                            f.clear();
+                            d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
+                        }
+                        if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
+                        else dt_min = smin(dt_min, d);
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < NV; ++q) fz_prev[q * CS] = fz_cur[q];
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];
+        }
         __syncthreads();
         // plane p-R is no longer read this iteration: refill its slot with p+R+1
         if (S::LATE_LOAD && lp <= nzc - 1) load_plane(p + R + 1);
         // ---------------------------------------------------------------- flux
-        double fz_cur[NV];
         if (do_zone) {
             if (!zring && xface) {  // x face at the west of this column
                 {
@@ -478,63 +529,15 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                     for (int q = 0; q < NV; ++q) FY[(cj * TX + ci) * NV + q] = f5[q];
                 }
             }
-            if (owned && lp >= 0) {  // z face at the bottom of plane p
-                Fault f;
-                f.clear();
-                face_flux<SOLVER, 2>(zp_prev, st[5], a.gamma, fz_cur, f);
-                if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
-            }
         }
         __syncthreads();
         // ---------------------------------------------------------------- rate
-        if (owned) {
-            if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
-                const double* u = P(p - 1) + zoff_c * NV;
-                const size_t zi = size_t(p - 1 + a.gh) * plane_stride + size_t(ja + a.gh) * a.pitch +
-                                  size_t(ia + a.gh) * NV;
-                double un[NV];
+        if (owned && lp >= 0 && lp < nzc) {  // x/y part of the rate of plane p
+            const double* fxw = FX + (cj * (TX + 1) + ci) * NV;
+            const double* fys = FY + (cj * TX + ci) * NV;
 #pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    double r = part[q * CS] - cz * (fz_cur[q] - fz_prev[q * CS]);
-                    if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
-                        un[q] = a.rk_a * ustart[zi + q] + a.rk_b * (u[q] + r);
-                    else
-                        un[q] = u[q] + r;
-                }
-                double* dst = uout + zi;
-#pragma unroll
-                for (int q = 0; q < NV; ++q) dst[q] = un[q];
-                if (RK && !a.want_dt) goto next_plane;
-                {
-                Fault f;
-                f.clear();
-                double d = FM == 2 ? eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz, a.gamma, f)
-                                  : eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f);
-                if (f.redo()) {
-                    V5 u5;
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
-                    f.clear();
-                    d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
-                }
-                if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
-                else dt_min = smin(dt_min, d);
-                }
-            next_plane:;
-            }
-            if (lp >= 0 && lp < nzc) {
-                const double* fxw = FX + (cj * (TX + 1) + ci) * NV;
-                const double* fys = FY + (cj * TX + ci) * NV;
-#pragma unroll
-                for (int q = 0; q < NV; ++q)
-                    part[q * CS] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
-            }
-            if (lp >= 0) {
-#pragma unroll
-                for (int q = 0; q < NV; ++q) fz_prev[q * CS] = fz_cur[q];
-            }
-#pragma unroll
-            for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];
+            for (int q = 0; q < NV; ++q)
+                part[q * CS] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
         }
     }
 

@@ -341,7 +341,7 @@ __device__ __noinline__ Fault predict_zone_careful(const MArgs& a, size_t o, Fac
 }
 
 template <bool O3>
-__global__ void __launch_bounds__(128) k_mhd_predict(MArgs a) {
+__global__ void __launch_bounds__(128, 4) k_mhd_predict(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     const int rx = b.n[0] + 2, ry = b.n[1] + 2;

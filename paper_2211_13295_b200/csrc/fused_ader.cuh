@@ -147,6 +147,55 @@ __device__ __forceinline__ void weno3_1div(double s0, double s1, double s2, doub
     uxx2 = (al * uxx_l + ac * uxx_c + ar * uxx_r) * inv;
 }
 
+// WENO-AO(5,3) (pointwise.cuh weno_ao) for the FMA build with one division: with
+// P_k = (eps + beta_k)^2 and A_k = g_k prod_{j!=k} P_j, the normalised weights are
+// A_k / sum A and the quartic's ratio w_h / g_h is prod_{j!=h} P_j / sum A. Products of three
+// P_k lie in [eps^6, ~1e40] for physical states (eps = 1e-12), far from over/underflow.
+template <int FAST>
+__device__ __forceinline__ void weno_ao_1div(double s0, double s1, double s2, double s3,
+                                             double s4, const Limiter& L, double* m, Fault& f) {
+    const double ghi = AO_GAMMA_HI;
+    double o1 = 0.5 * (s3 - s1), o2 = 0.5 * (s4 - s0);
+    double e1 = 0.5 * (s3 + s1) - s2, e2 = 0.5 * (s4 + s0) - s2;
+    double u3 = (o2 - 2.0 * o1) * (1.0 / 6.0);
+    double u1 = o1 - (11.0 / 10.0) * u3;
+    double u4 = (e2 - 4.0 * e1) * (1.0 / 12.0);
+    double u2 = e1 - (9.0 / 7.0) * u4;
+    double d0 = s1 - s0, d1 = s2 - s1, d2 = s3 - s2, d3 = s4 - s3;
+    double ux_l = 0.5 * (3.0 * d1 - d0), uxx_l = 0.5 * (d1 - d0);
+    double ux_c = 0.5 * (d1 + d2), uxx_c = 0.5 * (d2 - d1);
+    double ux_r = 0.5 * (3.0 * d2 - d3), uxx_r = 0.5 * (d3 - d2);
+    const double k2 = 13.0 / 3.0;
+    double ta = u1 + (1.0 / 10.0) * u3, tb = u2 + (123.0 / 455.0) * u4;
+    double eh = L.eps + (ta * ta + k2 * tb * tb + (781.0 / 20.0) * u3 * u3 +
+                         (1421461.0 / 2275.0) * u4 * u4);
+    double el = L.eps + (ux_l * ux_l + k2 * uxx_l * uxx_l);
+    double ec = L.eps + (ux_c * ux_c + k2 * uxx_c * uxx_c);
+    double er = L.eps + (ux_r * ux_r + k2 * uxx_r * uxx_r);
+    double ph = eh * eh, pl = el * el, pc = ec * ec, pr = er * er;
+    double phl = ph * pl, pcr = pc * pr;
+    double nh = pl * pcr, nl = ph * pcr, nc = phl * pr, nr = phl * pc;  // prod_{j!=k} P_j
+    double gl = (1.0 - ghi) * L.w0, gc = (1.0 - ghi) * L.w1, gr = (1.0 - ghi) * L.w2;
+    double al = gl * nl, ac = gc * nc, ar = gr * nr;
+    double inv = ddiv<FAST>(1.0, ghi * nh + al + ac + ar, f);
+    double wl = al * inv, wc = ac * inv, wr = ar * inv;
+    double ratio = nh * inv;
+    m[0] = ratio * (u1 - (gl * ux_l + gc * ux_c + gr * ux_r)) + (wl * ux_l + wc * ux_c + wr * ux_r);
+    m[1] = ratio * (u2 - (gl * uxx_l + gc * uxx_c + gr * uxx_r)) +
+           (wl * uxx_l + wc * uxx_c + wr * uxx_r);
+    m[2] = ratio * u3;
+    m[3] = ratio * u4;
+}
+
+template <int FAST>
+__device__ __forceinline__ void weno_ao_k(double s0, double s1, double s2, double s3, double s4,
+                                          const Limiter& L, double* m, Fault& f) {
+    if (HC_REASSOC)
+        weno_ao_1div<FAST>(s0, s1, s2, s3, s4, L, m, f);
+    else
+        weno_ao<FAST>(s0, s1, s2, s3, s4, L, m, f);
+}
+
 // both return twice the slopes (consumers: extrap2)
 template <int FAST>
 __device__ __forceinline__ void weno3_k(double s0, double s1, double s2, double s3, double s4,
@@ -173,11 +222,11 @@ __device__ __forceinline__ void zone_states(const double* pc, int row, const dou
         const double u0 = pc[q];
         if (ORD == 4) {  // WENO-AO(5,3) extension (pointwise.cuh weno_ao)
             double mx[4], my[4], mz[4];
-            weno_ao<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
+            weno_ao_k<FAST>(pc[-2 * NV + q], pc[-NV + q], u0, pc[NV + q], pc[2 * NV + q], a.lim,
                           mx, f);
-            weno_ao<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q],
+            weno_ao_k<FAST>(pc[-2 * row + q], pc[-row + q], u0, pc[row + q], pc[2 * row + q],
                           a.lim, my, f);
-            weno_ao<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, mz, f);
+            weno_ao_k<FAST>(zm2[q], zm1[q], u0, zp1[q], zp2[q], a.lim, mz, f);
             face[0][q] = extrap4(u0, +1.0, mx);
             face[1][q] = extrap4(u0, -1.0, mx);
             face[2][q] = extrap4(u0, +1.0, my);

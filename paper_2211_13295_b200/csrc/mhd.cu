@@ -78,7 +78,7 @@ template <int FAST = 0>
 __device__ __forceinline__ MPrim mhd_prim(const double* c, double gamma, Fault& f) {
     MPrim q;
     q.rho = c[0];
-    if (FAST) f.bad |= !(c[0] > 0.0);
+    if (FAST) f.bad |= not_pos_fast(c[0]);
     else if (!(c[0] > 0.0)) f.set(1, c[0]);
     q.inv_rho = ddiv<FAST>(1.0, c[0], f);
     q.u[0] = c[1] * q.inv_rho;
@@ -87,7 +87,7 @@ __device__ __forceinline__ MPrim mhd_prim(const double* c, double gamma, Fault& 
     q.b2 = c[5] * c[5] + c[6] * c[6] + c[7] * c[7];
     q.p = (gamma - 1.0) *
           (c[4] - 0.5 * (c[1] * q.u[0] + c[2] * q.u[1] + c[3] * q.u[2]) - 0.5 * q.b2);
-    if (FAST) f.bad |= !(q.p > 0.0);
+    if (FAST) f.bad |= not_pos_fast(q.p);
     else if (!(q.p > 0.0)) f.set(2, q.p);
     return q;
 }

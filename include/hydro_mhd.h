@@ -77,6 +77,13 @@ int hc_mhd_set_stream(hc_mhd* m, void* stream);
 int hc_mhd_fill_ghosts(hc_mhd* m);
 int hc_mhd_compute(hc_mhd* m);
 int hc_mhd_advance(hc_mhd* m);
+/* compute = compute_range(0, nz) + finish. compute_range prepares the update of the active
+ * z planes [zlo, zhi) (cell B, predictor, face fluxes, edge EMFs); finish updates every zone
+ * and face and takes the CFL estimate. A z-slab driver runs the interior range, whose
+ * stencils never reach the z ghosts ([gh, nz - gh - 1)), while the halos are in flight, then
+ * the two boundary ranges, then finish -- bit-identical to compute. */
+int hc_mhd_compute_range(hc_mhd* m, int zlo, int zhi);
+int hc_mhd_finish(hc_mhd* m);
 /* device state pointer, doubles per variable array, doubles per z plane */
 int hc_mhd_state(hc_mhd* m, double** dptr, size_t* var_stride, size_t* plane_elems);
 /* device address of the step's dt_next accumulator (1 double) */

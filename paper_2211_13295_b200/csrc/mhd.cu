@@ -63,6 +63,10 @@ struct MArgs {
     StepCtl* ctl;
     ErrBlock* eb;
     unsigned long long* floored;  // zones the pressure floor touched (k_mhd_dt)
+    // active z range [zlo, zhi) whose update the front kernels (cell B, predictor, faces,
+    // edges) prepare: the whole slab, or its interior / boundary parts when a z-slab driver
+    // overlaps the halo exchange (hc_mhd_compute_range)
+    int zlo, zhi;
 };
 
 // --------------------------------------------------------------------------- physics
@@ -232,9 +236,12 @@ template <bool O3>
 __global__ void k_mhd_cellb(MArgs a) {
     if (a.ctl && a.ctl->done) return;
     const Box& b = a.b;
+    // zones the predictor of [zlo - 1, zhi] reads: its stencil reach (2 at O3, 1 at O2) + 1
+    const int k0 = b.gh + a.zlo - (O3 ? 3 : 2);
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (r >= b.N) return;
-    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = int(r / (size_t(b.P) * b.Q));
+    if (r >= size_t(b.P) * b.Q * (a.zhi - a.zlo + (O3 ? 6 : 4))) return;
+    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = k0 + int(r / (size_t(b.P) * b.Q));
+    r = at(b, k, j, i);
     const int lo = O3 ? 1 : 0, hi = O3 ? 2 : 1;  // faces c-1 .. c+2 (O3) / c .. c+1
     if (i < lo || j < lo || k < lo || i + hi >= b.P || j + hi >= b.Q || k + hi >= b.R) return;
 #pragma unroll
@@ -345,12 +352,12 @@ __global__ void __launch_bounds__(128, 4) k_mhd_predict(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     const int rx = b.n[0] + 2, ry = b.n[1] + 2;
-    const size_t cnt = size_t(rx) * ry * (b.n[2] + 2);
+    const size_t cnt = size_t(rx) * ry * (a.zhi - a.zlo + 2);
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (r >= cnt) return;
-    // ring zone (active coords -1..n) -> storage
+    // ring zone (active x/y -1..n, z zlo-1..zhi) -> storage
     const int i = int(r % rx) - 1 + b.gh, j = int((r / rx) % ry) - 1 + b.gh,
-              k = int(r / (size_t(rx) * ry)) - 1 + b.gh;
+              k = int(r / (size_t(rx) * ry)) + a.zlo - 1 + b.gh;
     const size_t o = at(b, k, j, i);
     const double dt = a.ctl->dt;
     __shared__ double sface[6 * NM * 128];
@@ -397,14 +404,14 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     const Box& b = a.b;
     constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
     // x fastest for every axis (coalesced): extents n_d, +1 along A (faces 0..n_A)
-    const int ex = b.n[0] + (A == 0), ey = b.n[1] + (A == 1), ez = b.n[2] + (A == 2);
+    const int ex = b.n[0] + (A == 0), ey = b.n[1] + (A == 1), ez = a.zhi - a.zlo + (A == 2);
     const size_t cnt = size_t(ex) * ey * ez;
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (r >= cnt) return;
     int c[3];
     c[0] = int(r % ex);
     c[1] = int((r / ex) % ey);
-    c[2] = int(r / (size_t(ex) * ey));
+    c[2] = a.zlo + int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);  // zone right of the face
     const size_t ol = o - stride(b, A);
     double ul[NM], ur[NM], f5[5];
@@ -440,14 +447,14 @@ __global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
     const Box& b = a.b;
     constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
     // x fastest (coalesced): extents n_d, +1 across the edge (a and b run 0..n)
-    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = b.n[2] + (C != 2);
+    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = a.zhi - a.zlo + (C != 2);
     const size_t cnt = size_t(ex) * ey * ez;
     size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
     if (r >= cnt) return;
     int c[3];
     c[0] = int(r % ex);
     c[1] = int((r / ex) % ey);
-    c[2] = int(r / (size_t(ex) * ey));
+    c[2] = a.zlo + int(r / (size_t(ex) * ey));
     const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
     const size_t sa = stride(b, AA), sb = stride(b, BB);
     const size_t N = b.N;
@@ -675,6 +682,8 @@ MArgs margs(const hc_mhd* m) {
     a.ctl = m->ctl;
     a.eb = m->eb;
     a.floored = m->floored;
+    a.zlo = 0;
+    a.zhi = m->b.n[2];
     return a;
 }
 
@@ -688,21 +697,27 @@ int launch_ghosts(hc_mhd* m) {
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd ghost launch");
 }
 
-int launch_compute(hc_mhd* m) {
+// the front kernels of a step for the active z range [zlo, zhi): cell B, predictor, face
+// fluxes and edge EMFs of every face/edge the update of those zones reads
+int launch_front(hc_mhd* m, int zlo, int zhi) {
     MArgs a = margs(m);
+    a.zlo = zlo;
+    a.zhi = zhi;
     const Box& b = m->b;
     const bool o3 = m->p.order == 3;
-    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
-    if (o3) k_mhd_cellb<true><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
-    else k_mhd_cellb<false><<<blocks(b.N, 256), 256, 0, m->st>>>(a);
+    const int nz = zhi - zlo;
+    const size_t cb = size_t(b.P) * b.Q * (nz + (o3 ? 6 : 4));
+    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (nz + 2);
+    if (o3) k_mhd_cellb<true><<<blocks(cb, 256), 256, 0, m->st>>>(a);
+    else k_mhd_cellb<false><<<blocks(cb, 256), 256, 0, m->st>>>(a);
     if (o3) k_mhd_predict<true><<<blocks(ring, 128), 128, 0, m->st>>>(a);
     else k_mhd_predict<false><<<blocks(ring, 128), 128, 0, m->st>>>(a);
-    const size_t fx = size_t(b.n[0] + 1) * b.n[1] * b.n[2];
-    const size_t fy = size_t(b.n[0]) * (b.n[1] + 1) * b.n[2];
-    const size_t fz = size_t(b.n[0]) * b.n[1] * (b.n[2] + 1);
-    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (b.n[2] + 1);
-    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (b.n[2] + 1);
-    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * b.n[2];
+    const size_t fx = size_t(b.n[0] + 1) * b.n[1] * nz;
+    const size_t fy = size_t(b.n[0]) * (b.n[1] + 1) * nz;
+    const size_t fz = size_t(b.n[0]) * b.n[1] * (nz + 1);
+    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (nz + 1);
+    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (nz + 1);
+    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * nz;
     if (o3) {
         k_mhd_flux<true, 0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
         k_mhd_flux<true, 1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
@@ -718,15 +733,30 @@ int launch_compute(hc_mhd* m) {
         k_mhd_emf<false, 1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
         k_mhd_emf<false, 2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
     }
+    m->launches += 8;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd step launch");
+}
+
+// the update of every active zone and face, then the CFL estimate of the new state
+int launch_finish(hc_mhd* m) {
+    MArgs a = margs(m);
+    const Box& b = m->b;
+    const bool o3 = m->p.order == 3;
     const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
     k_mhd_update<<<blocks(up, 256), 256, 0, m->st>>>(a);
     const size_t act = size_t(b.n[0]) * b.n[1] * b.n[2];
     // CFL estimate of the updated state from each zone's own faces (ghosts are stale)
     if (o3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
     else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, m->cfl, &m->ctl->acc, ST_UPDATE);
-    m->launches += 10;
+    m->launches += 2;
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd step launch");
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd update launch");
+}
+
+int launch_compute(hc_mhd* m) {
+    int rc = launch_front(m, 0, m->b.n[2]);
+    return rc ? rc : launch_finish(m);
 }
 
 int launch_advance(hc_mhd* m) {
@@ -938,6 +968,20 @@ int hc_mhd_fill_ghosts(hc_mhd* m) {
 int hc_mhd_compute(hc_mhd* m) {
     HC_CUDA(cudaSetDevice(m->p.device));
     return launch_compute(m);
+}
+
+int hc_mhd_compute_range(hc_mhd* m, int zlo, int zhi) {
+    if (!m || zlo < 0 || zhi > m->b.n[2] || zlo >= zhi) {
+        set_error(HC_INVALID, "hc_mhd_compute_range: need 0 <= zlo < zhi <= nz");
+        return HC_INVALID;
+    }
+    HC_CUDA(cudaSetDevice(m->p.device));
+    return launch_front(m, zlo, zhi);
+}
+
+int hc_mhd_finish(hc_mhd* m) {
+    HC_CUDA(cudaSetDevice(m->p.device));
+    return launch_finish(m);
 }
 
 int hc_mhd_advance(hc_mhd* m) {

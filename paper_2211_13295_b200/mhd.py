@@ -50,9 +50,11 @@ def _lib():
     if not getattr(lib, "_mhd_typed", False):
         lib.hc_mhd_launches.restype = C.c_long
         lib.hc_mhd_launches.argtypes = [C.c_void_p]
-        for n in ("hc_mhd_destroy", "hc_mhd_fill_ghosts", "hc_mhd_compute", "hc_mhd_advance"):
+        for n in ("hc_mhd_destroy", "hc_mhd_fill_ghosts", "hc_mhd_compute", "hc_mhd_advance",
+                  "hc_mhd_finish"):
             getattr(lib, n).argtypes = [C.c_void_p]
         lib.hc_mhd_step.argtypes = [C.c_void_p, C.c_int]
+        lib.hc_mhd_compute_range.argtypes = [C.c_void_p, C.c_int, C.c_int]
         lib._mhd_typed = True
     return lib
 
@@ -129,6 +131,13 @@ class MhdStepper:
 
     def compute(self):
         _check(self.lib.hc_mhd_compute(self.h))
+
+    def compute_range(self, zlo, zhi):
+        """front kernels for the active z planes [zlo, zhi) (hc_mhd_compute_range)"""
+        _check(self.lib.hc_mhd_compute_range(self.h, zlo, zhi))
+
+    def finish(self):
+        _check(self.lib.hc_mhd_finish(self.h))
 
     def advance(self):
         _check(self.lib.hc_mhd_advance(self.h))

@@ -13,6 +13,12 @@ in one ``mhd.MhdStepper`` with caller-filled z ghosts (params.bc[2] = -1). Per s
   3. the step (hc_mhd_compute), the all-reduce (MIN) of the dt_next accumulator (exact), then
      the device t/dt hand-off (hc_mhd_advance).
 
+With N > 1 the exchange is overlapped (as slabs.py does for the Euler path): it runs on a
+second stream while hc_mhd_compute_range prepares the interior planes [gh, nloc - gh - 1),
+whose cell-B, predictor, face and edge stencils never reach a z-ghost plane or the shared top
+face plane; the two boundary ranges follow once the halos have landed, then hc_mhd_finish
+(update + CFL estimate) -- bit-identical to the sequential step.
+
 The z-face plane shared by two slabs is updated by both ranks from identical inputs, so the
 decomposed run is bit-identical to the single-domain run (tests/test_mhd_slabs_gloo.py runs
 the exchange over gloo with the numpy restatement as the per-slab compute). Periodic z only.
@@ -78,7 +84,9 @@ class MhdSlabDomain:
         self.geom = g
         self.st = mhd.MhdStepper(g, mhd.make_params(order, bc=(0, 0, -1), device=device))
         self.stream = torch.cuda.Stream(device=device)
+        self.comm = torch.cuda.Stream(device=device)
         self.st.set_stream(self.stream.cuda_stream)
+        self.overlap = world > 1
 
     def initial_state(self):
         return mhd.orszag_tang(self.geom, self.order)
@@ -105,12 +113,30 @@ class MhdSlabDomain:
             dt = float(t.item())
         return dt
 
-    def step(self):
+    def step(self, overlap=None):
         import torch
+        if overlap is None:
+            overlap = self.overlap
+        gh, n = self.geom.ghost, self.nloc
+        lo, hi = gh, n - gh - 1  # interior: no stencil reaches a z ghost or the top face
         with torch.cuda.stream(self.stream):
             self.st.fill_ghosts()
-            exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank, self.world)
-            self.st.compute()
+            if overlap and hi > lo:
+                ready = torch.cuda.Event()
+                ready.record(self.stream)
+                self.comm.wait_event(ready)
+                with torch.cuda.stream(self.comm):
+                    exchange_z_halos(self._planes(), gh, n, self.rank, self.world)
+                    halos = torch.cuda.Event()
+                    halos.record(self.comm)
+                self.st.compute_range(lo, hi)  # overlaps the exchange
+                self.stream.wait_event(halos)
+                self.st.compute_range(0, lo)
+                self.st.compute_range(hi, n)
+                self.st.finish()
+            else:
+                exchange_z_halos(self._planes(), gh, n, self.rank, self.world)
+                self.st.compute()
             if self.world > 1:
                 import torch.distributed as dist
                 dist.all_reduce(self._acc(), op=dist.ReduceOp.MIN)

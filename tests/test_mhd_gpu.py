@@ -144,19 +144,22 @@ def test_mhd_rejects_small_ghost():
         mhd.MhdStepper(g, mhd.make_params(3))
 
 
-def test_mhd_slab_path_single_rank_matches_stepper():
+@pytest.mark.parametrize("order,overlap", [(3, False), (3, True), (2, True)])
+def test_mhd_slab_path_single_rank_matches_stepper(order, overlap):
     """the multi-GPU step split (fill_ghosts -> z exchange -> compute -> advance) with one
-    rank equals the periodic single-domain stepper bit for bit"""
+    rank equals the periodic single-domain stepper bit for bit; with overlap, the interior
+    range is prepared while the (local) exchange runs on the second stream, then the two
+    boundary ranges and the update"""
     import torch
     from paper_2211_13295_b200 import mhd_slabs
-    n, order = 16, 3
+    n = 16
     dom = mhd_slabs.MhdSlabDomain(n, n, n, order)
     s0 = dom.initial_state()
     dom.st.upload(s0)
     dt0 = dom.initial_dt(0.4)
     dom.st.set_time(0.0, dt0, 0.4)
     for _ in range(3):
-        dom.step()
+        dom.step(overlap=overlap)
     torch.cuda.synchronize()
     a = active(dom.st.download(), dom.geom)
     t1 = dom.st.sync()
@@ -171,6 +174,34 @@ def test_mhd_slab_path_single_rank_matches_stepper():
     assert (bits(a) == bits(b)).all()
     assert st.sync() == t1
     st.close()
+
+
+@pytest.mark.parametrize("order,cuts", [(3, (0, 4, 11, 16)), (2, (0, 1, 7, 16)),
+                                        (3, (0, 16))])
+def test_mhd_compute_range_split_is_bitwise(order, cuts):
+    """compute = compute_range over any cover of [0, nz) + finish, bit for bit (3D random
+    field, periodic, the stepper's own z ghosts)"""
+    n = 16
+    g = mhd.make_geometry(n, n, n, order, (0, 0, 0), (1, 1, 1))
+    s0 = mhd.random_field(g, order, seed=7)
+    out = []
+    for split in (False, True):
+        st = mhd.MhdStepper(g, mhd.make_params(order))
+        st.upload(s0)
+        st.set_time(0.0, st.cfl_dt(0.4), 0.4)
+        for _ in range(3):
+            st.fill_ghosts()
+            if split:
+                for lo, hi in zip(cuts[:-1], cuts[1:]):
+                    st.compute_range(lo, hi)
+                st.finish()
+            else:
+                st.compute()
+            st.advance()
+        out.append((st.download(), st.sync()))
+        st.close()
+    (a, ta), (b, tb) = out
+    assert (bits(a) == bits(b)).all() and ta == tb
 
 
 @pytest.mark.parametrize("order", [2, 3])

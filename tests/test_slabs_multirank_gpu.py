@@ -40,4 +40,5 @@ def test_multirank_mhd_slab_run_on_one_gpu(world):
            f"--master-port={free_port()}", os.path.join(ROOT, "tools", "mhd_slab_gloo_gpu.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert f"mhd world {world}: decomposed == single domain: True" in r.stdout
+    for ov in (True, False):
+        assert f"mhd world {world} overlap {ov}: decomposed == single domain: True" in r.stdout

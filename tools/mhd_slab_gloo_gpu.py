@@ -20,13 +20,19 @@ def main():
     nzg = n * world
     gfull = mhd.make_geometry(n, n, nzg, order, (0, 0, 0), (1, 1, nzg / n))
     full = mhd.random_field(gfull, order, seed=5)
+    for overlap in (True, False):
+        check(n, order, steps, nzg, gfull, full, rank, world, overlap)
+    dist.destroy_process_group()
+
+
+def check(n, order, steps, nzg, gfull, full, rank, world, overlap):
     dom = mhd_slabs.MhdSlabDomain(n, n, nzg, order, rank=rank, world=world, device=0)
     gh = dom.geom.ghost
     dom.st.upload(np.ascontiguousarray(full[:, dom.z0:dom.z1 + 2 * gh + 1]))
     dt0 = dom.initial_dt(0.4)
     dom.st.set_time(0.0, dt0, 0.4)
     for _ in range(steps):
-        dom.step()
+        dom.step(overlap=overlap)
     torch.cuda.synchronize()
     mine = np.ascontiguousarray(dom.st.download()[:, gh:gh + dom.nloc])
     parts = [None] * world
@@ -42,10 +48,9 @@ def main():
         a = got[:, :, gh:gh + n, gh:gh + n]
         b = ref[:, :, gh:gh + n, gh:gh + n]
         same = bool((a.view(np.uint64) == b.view(np.uint64)).all())
-        print(f"mhd world {world}: decomposed == single domain: {same}")
+        print(f"mhd world {world} overlap {overlap}: decomposed == single domain: {same}")
         assert same
     dom.close()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -135,9 +135,12 @@ __device__ __forceinline__ void ced_zone(const CArgs& a, size_t o, double* fs, F
         for (int d = 0; d < 3; ++d) {
             const double up = w[o + st[d]], um = w[o - st[d]];
             if (!O3) lin[d] = mc_limiter(up - c0, c0 - um, a.lim.cfac_other);
-            else weno3<FAST>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
-            face(2 * d, q) = extrap<O3>(c0, +1.0, lin[d], quad[d]);
-            face(2 * d + 1, q) = extrap<O3>(c0, -1.0, lin[d], quad[d]);
+            else  // doubled slopes (weno3_2x, bit-exact): consumers halve their weights
+                weno3_2x<FAST>(w[o - 2 * st[d]], um, c0, up, w[o + 2 * st[d]], a.lim, lin[d], quad[d], wf);
+            face(2 * d, q) = O3 ? extrap2<true>(c0, +1.0, lin[d], quad[d])
+                                : extrap<false>(c0, +1.0, lin[d], quad[d]);
+            face(2 * d + 1, q) = O3 ? extrap2<true>(c0, -1.0, lin[d], quad[d])
+                                    : extrap<false>(c0, -1.0, lin[d], quad[d]);
             if (O3) {
                 const size_t sa = st[d], sb = st[(d + 1) % 3];
                 cross[d] =
@@ -154,9 +157,10 @@ __device__ __forceinline__ void ced_zone(const CArgs& a, size_t o, double* fs, F
 #pragma unroll
                 for (int la = 0; la < 2; ++la) {
                     const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
-                    double v = c0 + xa * lin[AA] + xb * lin[BB];
+                    const double hl = O3 ? 0.5 : 1.0;  // O3 slopes are doubled (exact halving)
+                    double v = c0 + (hl * xa) * lin[AA] + (hl * xb) * lin[BB];
                     if (O3)
-                        v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
+                        v = v + (1.0 / 12.0) * quad[AA] + (1.0 / 12.0) * quad[BB] +
                             (xa * xb) * cross[AA];
                     __stcs(a.states + (size_t(4 * C + 2 * lb + la) * NF + q) * N + o, v);
                 }

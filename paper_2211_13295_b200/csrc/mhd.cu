@@ -287,7 +287,8 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
             } else {
                 const double upp = wvar(a, q, o + 2 * st[d]);
                 const double umm = wvar(a, q, o - 2 * st[d]);
-                weno3<FAST>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], f);
+                // doubled slopes (weno3_2x, bit-exact): consumers halve their weights
+                weno3_2x<FAST>(umm, um, u0, up, upp, a.lim, lin[d], quad[d], f);
                 // cross mode of the pair (d, d+1): unlimited central mixed difference
                 const size_t sa = st[d], sb = st[(d + 1) % 3];
                 cross[d] = 0.25 * ((wvar(a, q, o + sa + sb) - wvar(a, q, o + sa - sb)) -
@@ -296,8 +297,10 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double fp = extrap<O3>(u0, +1.0, lin[d], quad[d]);
-            const double fm = extrap<O3>(u0, -1.0, lin[d], quad[d]);
+            const double fp = O3 ? extrap2<true>(u0, +1.0, lin[d], quad[d])
+                                 : extrap<false>(u0, +1.0, lin[d], quad[d]);
+            const double fm = O3 ? extrap2<true>(u0, -1.0, lin[d], quad[d])
+                                 : extrap<false>(u0, -1.0, lin[d], quad[d]);
             face(2 * d, q) = fp;
             face(2 * d + 1, q) = fm;
             // streaming stores (evict-first): 1.2 KB of states per zone would otherwise push
@@ -313,9 +316,10 @@ __device__ __forceinline__ void predict_zone(const MArgs& a, size_t o, const Fac
 #pragma unroll
                 for (int la = 0; la < 2; ++la) {
                     const double xa = la == 0 ? 0.5 : -0.5, xb = lb == 0 ? 0.5 : -0.5;
-                    double v = u0 + xa * lin[AA] + xb * lin[BB];
+                    const double hl = O3 ? 0.5 : 1.0;  // O3 slopes are doubled (exact halving)
+                    double v = u0 + (hl * xa) * lin[AA] + (hl * xb) * lin[BB];
                     if (O3)
-                        v = v + (1.0 / 6.0) * quad[AA] + (1.0 / 6.0) * quad[BB] +
+                        v = v + (1.0 / 12.0) * quad[AA] + (1.0 / 12.0) * quad[BB] +
                             (xa * xb) * cross[AA];
                     __stcs(sv + (size_t(6 + 4 * C + 2 * lb + la) * NM + q) * N + o, v);
                 }

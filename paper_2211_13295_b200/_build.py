@@ -44,6 +44,10 @@ def _compile(name, flags, verbose):
     deps += [os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
+    stem = name.replace(".cu", ".")
+    for old in os.listdir(BUILD):  # objects of this source under other flag sets
+        if old.startswith(stem) and old.endswith(".o") and os.path.join(BUILD, old) != obj:
+            os.remove(os.path.join(BUILD, old))
     cmd = [NVCC, "-c", src, "-o", obj] + COMMON + flags
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:

@@ -345,10 +345,14 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     using S = FusedShape<O3, TX, TY>;
     constexpr int R = S::R, G = S::G, NB = S::NB, W = S::W, H = S::H;
     if (a.ctl->done) return;
-    const int cur = a.ctl->cur;  // buffer holding the start-of-step state
-    const double* __restrict__ uin = a.buf[(cur + a.in_rel) % a.nbuf];
-    double* uout = a.buf[(cur + a.out_rel) % a.nbuf];  // may alias ustart (last RK stage)
-    const double* ustart = a.buf[cur];
+    // the step's buffers, picked once by thread 0 and kept in shared memory (read where used)
+    __shared__ double* sbuf[3];  // in, out (may alias start at the last RK stage), start
+    if (threadIdx.x == 0) {
+        const int cur = a.ctl->cur;  // buffer holding the start-of-step state
+        sbuf[0] = a.buf[(cur + a.in_rel) % a.nbuf];
+        sbuf[1] = a.buf[(cur + a.out_rel) % a.nbuf];
+        sbuf[2] = a.buf[cur];
+    }
 
     extern __shared__ __align__(128) double smem[];
     __shared__ unsigned long long mbar[NB];
@@ -398,13 +402,20 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     const bool exists = ia >= -1 && ia <= a.nx && ja >= -1 && ja <= a.ny;
     const int kz0 = a.kz_first + blockIdx.z * a.tz;  // first active plane (active z)
     const int nzc = min(a.tz, a.kz_last - kz0);
-    const double dt = a.ctl->dt;
-    const double cx = dt / a.dx, cy = dt / a.dy, cz = dt / a.dz;  // corrector.cpp:75
+    // dt and cx, cy, cz (corrector.cpp:75) live in shared memory (red[16..19], free until the
+    // final reduction): loop-invariant values kept in registers would be spilled
+    if (tid == 0) {
+        const double dt0 = a.ctl->dt;
+        red[16] = dt0 / a.dx;
+        red[17] = dt0 / a.dy;
+        red[18] = dt0 / a.dz;
+        red[19] = dt0;
+    }
 
     // storage pointer of (active plane z, active row ty0 - G, active col tx0 - G)
     const size_t plane_stride = size_t(a.my_pad) * a.pitch;
     auto gsrc = [&](int zact) -> const double* {
-        return uin + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
+        return sbuf[0] + size_t(zact + a.gh) * plane_stride + size_t(ty0 - G + a.gh) * a.pitch +
                size_t(tx0 - G + a.gh) * NV;
     };
     // ring slot of a plane: planes are loaded in order from zfirst, so slot = index % NB and
@@ -477,9 +488,10 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
             const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
             Fault f;
             f.clear();
-            zone_states<ORD, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt, st, f);
+            zone_states<ORD, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, red[19], st, f);
             if (f.redo()) {
-                Careful c = zone_states_careful<ORD, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, dt);
+                Careful c =
+                    zone_states_careful<ORD, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, red[19]);
 #pragma unroll
                 for (int s = 0; s < 6; ++s)
 #pragma unroll
@@ -514,13 +526,13 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                     double un[NV];
 #pragma unroll
                     for (int q = 0; q < NV; ++q) {
-                        double r = part[q * CS] - cz * (fz_cur[q] - fz_prev[q * CS]);
+                        double r = part[q * CS] - red[18] * (fz_cur[q] - fz_prev[q * CS]);
                         if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
-                            un[q] = a.rk_a * ustart[zi + q] + a.rk_b * (u[q] + r);
+                            un[q] = a.rk_a * sbuf[2][zi + q] + a.rk_b * (u[q] + r);
                         else
                             un[q] = u[q] + r;
                     }
-                    double* dst = uout + zi;
+                    double* dst = sbuf[1] + zi;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) dst[q] = un[q];
                     if (!RK || a.want_dt) {
@@ -586,7 +598,8 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
             const double* fys = FY + (cj * TX + ci) * NV;
 #pragma unroll
             for (int q = 0; q < NV; ++q)
-                part[q * CS] = -cx * (fxw[NV + q] - fxw[q]) - cy * (fys[TX * NV + q] - fys[q]);
+                part[q * CS] =
+                    -red[16] * (fxw[NV + q] - fxw[q]) - red[17] * (fys[TX * NV + q] - fys[q]);
         }
     }
 

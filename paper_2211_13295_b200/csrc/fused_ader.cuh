@@ -105,7 +105,8 @@ struct FusedShape {
     // then writes that face's flux to the same slot (no other reader in between)
     // per-thread carried state of the owned zones (partial x/y rate of plane p, z flux at the
     // bottom of plane p), [NV][TX*TY]: explicit shared memory instead of register spills
-    static constexpr int CARRY = 2 * NV * TX * TY;
+    // (+ each owned thread's running CFL minimum)
+    static constexpr int CARRY = 2 * NV * TX * TY + TX * TY;
     static constexpr size_t SMEM =
         sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32 + CARRY);
 };
@@ -466,7 +467,8 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     double zp_prev[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) zp_prev[q] = 0.0;
-    double dt_min = 1.0e32;
+    double* dt_min = fz_prev + NV * CS;  // this owned thread's running CFL minimum
+    if (owned) dt_min[0] = 1.0e32;
     const int zoff_c = (cj + G) * W + (ci + G);  // zone index of this column in a smem plane
 
     for (int lp = -1; lp <= nzc; ++lp) {
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                             d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f);
                         }
                         if (f.code) record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f, ia, ja, p - 1, 0);
-                        else dt_min = smin(dt_min, d);
+                        else dt_min[0] = smin(dt_min[0], d);
                     }
                 }
 #pragma unroll
@@ -605,8 +607,9 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
 
     // ---- block min -> one atomic per CTA (exact: min is order independent)
     if (RK && !a.want_dt) return;
-    dt_min = warp_min(dt_min);
-    if ((tid & 31) == 0) red[tid >> 5] = dt_min;
+    double dmin = owned ? dt_min[0] : 1.0e32;
+    dmin = warp_min(dmin);
+    if ((tid & 31) == 0) red[tid >> 5] = dmin;
     __syncthreads();
     if (tid < 32) {
         constexpr int NW = (S::NT + 31) / 32;

@@ -106,7 +106,7 @@ struct FusedShape {
     // per-thread carried state of the owned zones (partial x/y rate of plane p, z flux at the
     // bottom of plane p), [NV][TX*TY]: explicit shared memory instead of register spills
     // (+ each owned thread's running CFL minimum)
-    static constexpr int CARRY = 2 * NV * TX * TY + TX * TY;
+    static constexpr int CARRY = 2 * NV * TX * TY + TX * TY + NT / 2;  // (+ column offsets)
     static constexpr size_t SMEM =
         sizeof(double) * (size_t(NB) * PLANE + NV * (XP_N + YP_N) + 32 + CARRY);
 };
@@ -469,7 +469,10 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     for (int q = 0; q < NV; ++q) zp_prev[q] = 0.0;
     double* dt_min = fz_prev + NV * CS;  // this owned thread's running CFL minimum
     if (owned) dt_min[0] = 1.0e32;
-    const int zoff_c = (cj + G) * W + (ci + G);  // zone index of this column in a smem plane
+    // offset (doubles) of this column's zone in a smem plane, kept in shared memory and read
+    // where used (a register copy would be spilled)
+    int* zoff = reinterpret_cast<int*>(dt_min - tid + CS) + tid;
+    zoff[0] = ((cj + G) * W + (ci + G)) * NV;
 
     for (int lp = -1; lp <= nzc; ++lp) {
         const int p = kz0 + lp;
@@ -483,11 +486,11 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
         // ------------------------------------------------------------- predict
         double st[6][NV];  // face states incl. 0.5*tau: E, W, N, S, T, B
         if (do_zone) {
-            const double* pc = P(p) + zoff_c * NV;
-            const double* zm1 = P(p - 1) + zoff_c * NV;
-            const double* zp1 = P(p + 1) + zoff_c * NV;
-            const double* zm2 = O3 ? P(p - 2) + zoff_c * NV : zm1;
-            const double* zp2 = O3 ? P(p + 2) + zoff_c * NV : zp1;
+            const double* pc = P(p) + zoff[0];
+            const double* zm1 = P(p - 1) + zoff[0];
+            const double* zp1 = P(p + 1) + zoff[0];
+            const double* zm2 = O3 ? P(p - 2) + zoff[0] : zm1;
+            const double* zp2 = O3 ? P(p + 2) + zoff[0] : zp1;
             Fault f;
             f.clear();
             zone_states<ORD, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, red[19], st, f);
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                     if (f.code) record_fault(a.eb, ST_FLUX, f, p, ia, ja, 2);
                 }
                 if (lp >= 1) {  // finalise plane p-1 with its top face flux fz_cur
-                    const double* u = P(p - 1) + zoff_c * NV;
+                    const double* u = P(p - 1) + zoff[0];
                     const size_t zi = size_t(p - 1 + a.gh) * plane_stride +
                                       size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
                     double un[NV];

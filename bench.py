@@ -75,26 +75,33 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if r & bit and bit != 0x1:
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h,
-                                                                  self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.002)
+            self._sample()
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            time.sleep(0.001)  # let the sampler take its first reading
         return self
 
     def __exit__(self, *a):
+        # (and one sample from the main thread at the end of the timed region, still under
+        # load: a short region must not go unsampled if the thread was starved)
+        if self.nv:
+            self._sample()
         self._stop.set()
         if self.nv:
             self.t.join()

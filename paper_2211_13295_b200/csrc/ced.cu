@@ -81,9 +81,9 @@ __device__ __forceinline__ void maxwell_flux(const double* u, double ie, double 
 __global__ void k_ced_ghosts(CArgs a, int with_sigma) {
     if (a.ctl && a.ctl->done) return;
     const Box& b = a.b;
-    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (r >= b.N) return;
-    const int c[3] = {int(r % b.P), int((r / b.P) % b.Q), int(r / (size_t(b.P) * b.Q))};
+    int c[3];  // the ghost shell only
+    if (!shell_zone(b, blockIdx.x * size_t(blockDim.x) + threadIdx.x, c[0], c[1], c[2])) return;
+    const size_t r = at(b, c[2], c[1], c[0]);
 #pragma unroll 1
     for (int q = 0; q < NF + with_sigma; ++q) {
         int src[3];
@@ -410,7 +410,7 @@ int launch_step(hc_ced* m) {
     const Box& b = m->b;
     const bool o3 = m->p.order == 3;
     cudaStream_t st = m->st;
-    k_ced_ghosts<<<blocks(b.N, 256), 256, 0, st>>>(a, 0);
+    k_ced_ghosts<<<blocks(shell_count(b), 256), 256, 0, st>>>(a, 0);
     if (o3) k_ced_cell<true><<<blocks(b.N, 256), 256, 0, st>>>(a);
     else k_ced_cell<false><<<blocks(b.N, 256), 256, 0, st>>>(a);
     const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
@@ -522,7 +522,7 @@ int hc_ced_upload(hc_ced* m, const double* host, const double* sigma) {
     HC_CUDA(cudaMemcpyAsync(m->sigma, sigma, B, cudaMemcpyHostToDevice, m->st));
     CArgs a = cargs(m);
     a.ctl = nullptr;
-    k_ced_ghosts<<<blocks(m->b.N, 256), 256, 0, m->st>>>(a, 1);  // sigma's ghost zones
+    k_ced_ghosts<<<blocks(shell_count(m->b), 256), 256, 0, m->st>>>(a, 1);  // sigma's ghosts
     m->launches += 1;
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(m->st));

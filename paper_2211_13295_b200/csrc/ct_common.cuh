@@ -20,6 +20,46 @@ struct Box {
 __device__ __forceinline__ size_t at(const Box& b, int k, int j, int i) {
     return (size_t(k) * b.Q + j) * b.P + i;
 }
+// Zones of the padded box outside the active cell box [gh, gh+n)^3 (the ghost shell every
+// ghost of every variable lies in): count, and the r-th one (z slabs, then y rows of the
+// active planes, then x columns of the active rows). Ghost fills launch over this shell only.
+__host__ __device__ __forceinline__ size_t shell_count(const Box& b) {
+    const size_t nx = b.n[0], ny = b.n[1], nz = b.n[2];
+    return size_t(b.R - nz) * b.P * b.Q + nz * (b.Q - ny) * b.P + nz * ny * (b.P - nx);
+}
+__device__ __forceinline__ bool shell_zone(const Box& b, size_t r, int& i, int& j, int& k) {
+    const int nx = b.n[0], ny = b.n[1], nz = b.n[2], g = b.gh;
+    const size_t PQ = size_t(b.P) * b.Q;
+    const size_t zc = size_t(b.R - nz) * PQ;
+    if (r < zc) {
+        const int kk = int(r / PQ);
+        const size_t rem = r % PQ;
+        k = kk < g ? kk : kk + nz;
+        j = int(rem / b.P);
+        i = int(rem % b.P);
+        return true;
+    }
+    r -= zc;
+    const size_t yp = size_t(b.Q - ny) * b.P, yc = size_t(nz) * yp;
+    if (r < yc) {
+        k = g + int(r / yp);
+        const size_t rem = r % yp;
+        const int jj = int(rem / b.P);
+        j = jj < g ? jj : jj + ny;
+        i = int(rem % b.P);
+        return true;
+    }
+    r -= yc;
+    const size_t xp = size_t(b.P - nx), xr = size_t(ny) * xp;
+    if (r >= size_t(nz) * xr) return false;
+    k = g + int(r / xr);
+    const size_t rem = r % xr;
+    j = g + int(rem / xp);
+    const int ii = int(rem % xp);
+    i = ii < g ? ii : ii + nx;
+    return true;
+}
+
 __device__ __forceinline__ size_t stride(const Box& b, int axis) {
     return axis == 0 ? size_t(1) : (axis == 1 ? size_t(b.P) : size_t(b.P) * b.Q);
 }

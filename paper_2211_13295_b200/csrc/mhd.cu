@@ -200,9 +200,9 @@ __device__ __forceinline__ void mhd_divergence(const FaceSmem& face, const doubl
 __global__ void k_mhd_ghosts(MArgs a) {
     if (a.ctl && a.ctl->done) return;
     const Box& b = a.b;
-    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-    if (r >= b.N) return;
-    const int i = int(r % b.P), j = int((r / b.P) % b.Q), k = int(r / (size_t(b.P) * b.Q));
+    int i, j, k;  // the ghost shell only
+    if (!shell_zone(b, blockIdx.x * size_t(blockDim.x) + threadIdx.x, i, j, k)) return;
+    const size_t r = at(b, k, j, i);
     const int c[3] = {i, j, k};
 #pragma unroll 1
     for (int q = 0; q < NM; ++q) {
@@ -695,7 +695,7 @@ using ct::blocks;
 
 int launch_ghosts(hc_mhd* m) {
     MArgs a = margs(m);
-    k_mhd_ghosts<<<blocks(m->b.N, 256), 256, 0, m->st>>>(a);
+    k_mhd_ghosts<<<blocks(shell_count(m->b), 256), 256, 0, m->st>>>(a);
     m->launches += 1;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd ghost launch");

@@ -474,8 +474,16 @@ __global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
             const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
             double u[NM];
             half_state(a, z, 6 + 4 * C + 2 * lb + la, u);
-            positive_or_average(a, z, a.gamma, u);
-            MPrim p = mhd_prim(u, a.gamma, f);
+            // positivity fallback with the primitive state reused (same bits as a second
+            // mhd_prim of the kept state)
+            Fault t;
+            t.clear();
+            MPrim p = mhd_prim(u, a.gamma, t);
+            if (t.code) {
+#pragma unroll
+                for (int q = 0; q < NM; ++q) u[q] = cellvar<false>(a, q, z);
+                p = mhd_prim(u, a.gamma, f);
+            }
             ec[la][lb] = p.u[BB] * u[5 + AA] - p.u[AA] * u[5 + BB];
             ba[la][lb] = u[5 + AA];
             bb[la][lb] = u[5 + BB];

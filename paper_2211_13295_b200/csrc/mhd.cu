@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
 // over the corners of v + c_f), alpha- = max(0, max of c_f - v); B_b[a-] = mean of the two
 // low-a corner values (and so on); E_C = -(v x B)_C = v_b B_a - v_a B_b.
 template <bool O3, int C>
-__global__ void __launch_bounds__(128, 4) k_mhd_emf(MArgs a) {
+__global__ void __launch_bounds__(128, 5) k_mhd_emf(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;

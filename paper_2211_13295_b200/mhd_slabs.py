@@ -39,7 +39,7 @@ def slab_range(nz_global: int, rank: int, world: int):
     return rank * nloc, (rank + 1) * nloc
 
 
-def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=None):
+def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=None, p2p=False):
     """planes: torch tensor [NVAR, nloc + 2 gh + 1, plane_elems] viewing the slab's state
     (CPU or CUDA). Fills the z ghosts of every variable from the periodic z neighbours."""
     import torch
@@ -49,7 +49,7 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=No
     hi_send = planes[:, nloc:nloc + gh]           # -> upper rank's [0, gh)
     lo_ghost = planes[:, 0:gh]
     hi_ghost = planes[:, gh + nloc:2 * gh + nloc + 1]
-    if world == 1:
+    if world == 1 and not p2p:  # (p2p: through the process group, to itself)
         lo_ghost.copy_(hi_send.clone())
         hi_ghost.copy_(lo_send.clone())
         return
@@ -87,6 +87,7 @@ class MhdSlabDomain:
         self.comm = torch.cuda.Stream(device=device)
         self.st.set_stream(self.stream.cuda_stream)
         self.overlap = world > 1
+        self.collectives = world > 1  # True at N = 1: the NCCL path to itself (testing)
 
     def initial_state(self):
         return mhd.orszag_tang(self.geom, self.order)
@@ -126,7 +127,8 @@ class MhdSlabDomain:
                 ready.record(self.stream)
                 self.comm.wait_event(ready)
                 with torch.cuda.stream(self.comm):
-                    exchange_z_halos(self._planes(), gh, n, self.rank, self.world)
+                    exchange_z_halos(self._planes(), gh, n, self.rank, self.world,
+                                     p2p=self.collectives)
                     halos = torch.cuda.Event()
                     halos.record(self.comm)
                 self.st.compute_range(lo, hi)  # overlaps the exchange
@@ -135,9 +137,10 @@ class MhdSlabDomain:
                 self.st.compute_range(hi, n)
                 self.st.finish()
             else:
-                exchange_z_halos(self._planes(), gh, n, self.rank, self.world)
+                exchange_z_halos(self._planes(), gh, n, self.rank, self.world,
+                                 p2p=self.collectives)
                 self.st.compute()
-            if self.world > 1:
+            if self.world > 1 or self.collectives:
                 import torch.distributed as dist
                 dist.all_reduce(self._acc(), op=dist.ReduceOp.MIN)
             self.st.advance()

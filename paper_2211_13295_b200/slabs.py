@@ -44,13 +44,15 @@ def neighbours(rank: int, world: int, periodic: bool):
 
 
 def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic: bool,
-                     group=None):
+                     group=None, p2p=False):
     """Fills the z-ghost planes of a slab in place.
 
     planes: torch tensor [nloc + 2 gh, plane_elems] (CPU or CUDA) = the slab's storage with
     one row per z plane. Sends the gh lowest active planes down and the gh highest up; the
     receiving side stores them as its top / bottom ghosts. Single rank + periodic is the local
-    wrap; outflow ends copy the edge active plane (boundary.cpp:7-10 map_index)."""
+    wrap; outflow ends copy the edge active plane (boundary.cpp:7-10 map_index). p2p: a single
+    periodic rank exchanges with itself through the process group (NCCL send/recv to self --
+    the N > 1 code path, runnable on one GPU)."""
     import torch
     import torch.distributed as dist
 
@@ -59,7 +61,7 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic
     hi_ghost = planes[gh + nloc:gh + nloc + gh]
     lo_act = planes[gh:2 * gh]
     hi_act = planes[nloc:nloc + gh]
-    if world == 1:
+    if world == 1 and not p2p:
         if periodic:
             lo_ghost.copy_(hi_act)
             hi_ghost.copy_(lo_act)
@@ -140,6 +142,9 @@ class SlabDomain:
         self.stream = torch.cuda.Stream(device=device)
         self.comm = torch.cuda.Stream(device=device)  # halo exchange, overlapped
         self.st.set_stream(self.stream.cuda_stream)
+        # route a single rank's halos and dt all-reduce through the process group too
+        # (exercises the NCCL path on one GPU; tools/nccl_self_gpu.py)
+        self.collectives = world > 1
 
     # ---- host side
     def host_shape(self):
@@ -226,7 +231,7 @@ class SlabDomain:
                     self.comm.wait_event(ready)
                     with torch.cuda.stream(self.comm):
                         exchange_z_halos(self._planes(), self.geom.ghost, self.nloc, self.rank,
-                                         self.world, self.periodic)
+                                         self.world, self.periodic, p2p=self.collectives)
                         halos = torch.cuda.Event()
                         halos.record(self.comm)
                     self.st.compute_range(G, self.nloc - G, False)  # overlaps the exchange
@@ -234,13 +239,14 @@ class SlabDomain:
                     self.st.compute_range(0, G, False)
                     self.st.compute_range(self.nloc - G, self.nloc, True)
                 else:
-                    if self.world > 1:
+                    if self.world > 1 or self.collectives:
                         exchange_z_halos(self._planes(), self.geom.ghost, self.nloc,
-                                         self.rank, self.world, self.periodic)
+                                         self.rank, self.world, self.periodic,
+                                         p2p=self.collectives)
                     self.st.compute()
             if kernel_events is not None:
                 kernel_events[1].record(s)
-            if self.world > 1:
+            if self.world > 1 or self.collectives:
                 import torch.distributed as dist
                 dist.all_reduce(self._acc(), op=dist.ReduceOp.MIN)
             self.st.advance()

@@ -42,3 +42,14 @@ def test_multirank_mhd_slab_run_on_one_gpu(world):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     for ov in (True, False):
         assert f"mhd world {world} overlap {ov}: decomposed == single domain: True" in r.stdout
+
+
+def test_nccl_self_exchange_on_one_gpu():
+    """The NCCL code path itself: one rank whose halos go through NCCL send/recv to itself and
+    whose dt_next goes through an NCCL all-reduce, overlapped with the interior planes, equals
+    the single-domain steppers bit for bit (Euler and MHD; tools/nccl_self_gpu.py)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "nccl_self_gpu.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "euler nccl-self overlap: decomposed == single domain: True" in r.stdout
+    assert "mhd nccl-self overlap: decomposed == single domain: True" in r.stdout

@@ -13,11 +13,12 @@ in one ``mhd.MhdStepper`` with caller-filled z ghosts (params.bc[2] = -1). Per s
   3. the step (hc_mhd_compute), the all-reduce (MIN) of the dt_next accumulator (exact), then
      the device t/dt hand-off (hc_mhd_advance).
 
-With N > 1 the exchange is overlapped (as slabs.py does for the Euler path): it runs on a
+step(overlap=True) overlaps the exchange (as slabs.py can for the Euler path): it runs on a
 second stream while hc_mhd_compute_range prepares the interior planes [gh, nloc - gh - 1),
 whose cell-B, predictor, face and edge stencils never reach a z-ghost plane or the shared top
 face plane; the two boundary ranges follow once the halos have landed, then hc_mhd_finish
-(update + CFL estimate) -- bit-identical to the sequential step.
+(update + CFL estimate) -- bit-identical to the sequential step, but measured slower than it
+at the configs[4] slab size (the default is the sequential step).
 
 The z-face plane shared by two slabs is updated by both ranks from identical inputs, so the
 decomposed run is bit-identical to the single-domain run (tests/test_mhd_slabs_gloo.py runs
@@ -86,7 +87,9 @@ class MhdSlabDomain:
         self.stream = torch.cuda.Stream(device=device)
         self.comm = torch.cuda.Stream(device=device)
         self.st.set_stream(self.stream.cuda_stream)
-        self.overlap = world > 1
+        # (off by default: the split front kernels cost ~5 % on a 512^2 x 64 slab, more than
+        # the ~1.5 % an NVLink exchange of the halos takes; tools/nccl_self_bench.py)
+        self.overlap = False
         self.collectives = world > 1  # True at N = 1: the NCCL path to itself (testing)
 
     def initial_state(self):

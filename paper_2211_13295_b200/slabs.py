@@ -118,8 +118,11 @@ class SlabDomain:
     def __init__(self, nx, ny, nz_global, order, rank=0, world=1, device=0, exact=True,
                  solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER, overlap=None):
         self.rank, self.world, self.order = rank, world, order
-        # overlap: z halos by the (local, at N=1) exchange, interior planes computed meanwhile
-        overlap = world > 1 if overlap is None else overlap
+        # overlap: interior planes computed while the z halos are exchanged. Off by default:
+        # splitting the fused launch into interior + two boundary ranges costs more than the
+        # exchange it hides (512^2 x 64 slab of configs[4]: +13 % vs +0.2 % for the sequential
+        # NCCL exchange, tools/nccl_self_bench.py; an NVLink exchange of 2 x 32 MB is ~2 %)
+        overlap = False if overlap is None else overlap
         self.overlap = overlap
         self.periodic = bc == PERIODIC
         self.z0, self.z1 = slab_range(nz_global, rank, world)

@@ -30,7 +30,8 @@ def test_multirank_slab_run_on_one_gpu(world):
            f"--master-port={free_port()}", os.path.join(ROOT, "tools", "slab_gloo_gpu.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert f"world {world}: decomposed == single domain: True" in r.stdout
+    for ov in (True, False):
+        assert f"world {world} overlap {ov}: decomposed == single domain: True" in r.stdout
 
 
 @pytest.mark.parametrize("world", [2, 3])

@@ -25,10 +25,17 @@ def modulate(s, k0):
 
 def main():
     dist.init_process_group(os.environ.get("HC_DIST_BACKEND", "gloo"))
+    for overlap in (True, False):
+        check(overlap)
+    dist.destroy_process_group()
+
+
+def check(overlap):
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
     n, order, steps = 24, 3, 4
-    dom = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=0)
+    dom = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=0,
+                           overlap=overlap)
     gh = dom.geom.ghost
     s0 = modulate(dom.initial_state(), dom.z0)  # local storage plane p = global z0 + p
     dt0 = dom.initial_dt(s0, 0.4)
@@ -54,10 +61,10 @@ def main():
         got = np.concatenate(parts, axis=0)
         same = bool((got[:, gh:gh + n, gh:gh + n].view(np.uint64) ==
                      ref[:, gh:gh + n, gh:gh + n].view(np.uint64)).all())
-        print(f"world {world}: decomposed == single domain: {same}; t {t[0]} vs {st.sync()[0]}")
+        print(f"world {world} overlap {overlap}: decomposed == single domain: {same}; "
+              f"t {t[0]} vs {st.sync()[0]}")
         assert same
     dom.close()
-    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -17,12 +17,17 @@ template <int ORD, int SOLVER, int TX, int TY, int MINB, bool RK>
 static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     using S = FusedShape<(ORD >= 3), TX, TY>;
     auto kern = fused_ader_kernel<ORD, SOLVER, TX, TY, MINB, RK>;
-    static bool configured = false;
-    if (!configured) {
+    // the shared-memory opt-in is a per-device attribute: one bit per device ordinal
+    static unsigned long long configured = 0;
+    int dev = 0;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return cuda_fail(de, "cudaGetDevice");
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
         cudaError_t e =
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fused)");
-        configured = true;
+        __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
     }
     // bulk-copy plane loads need 16-byte aligned rows: halo G == storage ghost width (tile
     // origins at multiples of TX, TX + 2G even) and an even row pitch; else per-8-byte cp.async

@@ -46,6 +46,8 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=No
     import torch
     import torch.distributed as dist
 
+    if nloc < gh + 1:  # the lower send (gh + 1 planes incl. the shared face) must be owned
+        raise ValueError(f"slab of {nloc} planes is thinner than the {gh + 1}-plane halo")
     lo_send = planes[:, gh:2 * gh + 1]            # -> lower rank's [gh+nloc, 2gh+nloc+1)
     hi_send = planes[:, nloc:nloc + gh]           # -> upper rank's [0, gh)
     lo_ghost = planes[:, 0:gh]
@@ -71,6 +73,19 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, group=No
     hi_ghost.copy_(ra)
 
 
+def slab_geometry(nx, ny, nz_global, order, z0, z1):
+    """Geometry of the z-slab [z0, z1) of the nx x ny x nz_global mesh on [0,1] x [0, ny d] x
+    [0, nz_global d], d = 1/nx: the spacings are set to d itself (not re-derived as
+    (hi - lo)/n, which is an ulp off for some slabs when n is not a power of two), so every
+    rank steps with the single domain's dx, dy, dz and the decomposition stays bit-transparent.
+    slab_geometry(nx, ny, nz, order, 0, nz) is the matching single domain."""
+    d = 1.0 / nx
+    g = mhd.make_geometry(nx, ny, z1 - z0, order, (0.0, 0.0, z0 * d), (1.0, ny * d, z1 * d))
+    g.dx = g.dy = g.dz = d
+    g.origin[0], g.origin[1], g.origin[2] = 0.0, 0.0, z0 * d
+    return g
+
+
 class MhdSlabDomain:
     """One rank's slab of a periodic nx x ny x nz_global MHD mesh on [0,1]^2 x [0, nz dz]."""
 
@@ -79,9 +94,7 @@ class MhdSlabDomain:
         self.rank, self.world, self.order = rank, world, order
         self.z0, self.z1 = slab_range(nz_global, rank, world)
         self.nloc = self.z1 - self.z0
-        d = 1.0 / nx
-        g = mhd.make_geometry(nx, ny, self.nloc, order, (0.0, 0.0, self.z0 * d),
-                              (1.0, ny * d, self.z1 * d))
+        g = slab_geometry(nx, ny, nz_global, order, self.z0, self.z1)
         self.geom = g
         self.st = mhd.MhdStepper(g, mhd.make_params(order, bc=(0, 0, -1), device=device))
         self.stream = torch.cuda.Stream(device=device)

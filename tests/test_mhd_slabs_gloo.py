@@ -23,10 +23,18 @@ def free_port():
     return p
 
 
+def oracle_geom(nx, nzg, order, z0, z1):
+    """mo.Geom of the slab [z0, z1) with the spacings of mhd_slabs.slab_geometry (exactly 1/nx,
+    not re-derived per slab)"""
+    g = mhd_slabs.slab_geometry(nx, nx, nzg, order, z0, z1)
+    G = mo.Geom(nx, nx, z1 - z0, order, (0, 0, g.origin[2]), (1, 1, z1 / nx))
+    G.d = (g.dx, g.dy, g.dz)
+    return G
+
+
 def full_state(nx, nzg, order):
-    g = mhd.make_geometry(nx, nx, nzg, order, (0, 0, 0), (1, 1, nzg / nx))
-    return mhd.random_field(g, order, seed=11), mo.Geom(nx, nx, nzg, order, (0, 0, 0),
-                                                         (1, 1, nzg / nx))
+    g = mhd_slabs.slab_geometry(nx, nx, nzg, order, 0, nzg)
+    return mhd.random_field(g, order, seed=11), oracle_geom(nx, nzg, order, 0, nzg)
 
 
 def _worker(rank, world, port, order, steps, nx, nzg, q):
@@ -37,7 +45,7 @@ def _worker(rank, world, port, order, steps, nx, nzg, q):
         z0, z1 = mhd_slabs.slab_range(nzg, rank, world)
         nloc = z1 - z0
         full, G = full_state(nx, nzg, order)
-        g = mo.Geom(nx, nx, nloc, order, (0, 0, z0 / nx), (1, 1, z1 / nx))
+        g = oracle_geom(nx, nzg, order, z0, z1)
         gh = g.gh
         s = np.ascontiguousarray(full[:, z0:z1 + 2 * gh + 1])
         par = mo.Params(order, bc=(0, 0, None))
@@ -99,11 +107,14 @@ def test_single_rank_exchange_is_the_periodic_fill():
     assert (s == ref).all()
 
 
-@pytest.mark.parametrize("world,order", [(2, 2), (2, 3), (4, 2)])
-def test_decomposed_mhd_run_is_bit_identical(world, order):
+@pytest.mark.parametrize("world,order,nx,nzg", [(2, 2, 8, 16), (2, 3, 8, 16), (4, 2, 8, 16),
+                                                 (3, 2, 6, 12), (3, 3, 6, 18)])
+def test_decomposed_mhd_run_is_bit_identical(world, order, nx, nzg):
+    """(world 3 on 6 x 6 x 12 and 6 x 6 x 18 meshes: spacings 1/6 are not powers of two -- every slab must
+    still step with exactly the single domain's dz)"""
     steps = 3
-    got, dts, all_dts = run_slabs(world, order, steps)
-    want, dts_ref = run_single(order, steps)
+    got, dts, all_dts = run_slabs(world, order, steps, nx=nx, nzg=nzg)
+    want, dts_ref = run_single(order, steps, nx=nx, nzg=nzg)
     assert (got.view(np.uint64) == want.view(np.uint64)).all()
     assert dts == dts_ref
     assert all(d == dts for d in all_dts)

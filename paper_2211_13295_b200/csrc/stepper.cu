@@ -786,7 +786,29 @@ struct hc_patchset {
     int device = 0;
     long launches = 0;
     unsigned long long ledger[6] = {0, 0, 0, 0, 0, 0};  // TransferLedger field order
+    long long accounted = 0;  // device steps already entered in the ledger
 };
+
+// TransferLedger (transfer.cpp:160-175): per patch per EXECUTED step, skinny strategy. The
+// device turns steps after t_final or after a fault into no-ops, so the ledger follows the
+// device step counter (read at sync), not the number of steps queued.
+static void ps_account(hc_patchset* ps, long long steps_now) {
+    const long long d = steps_now - ps->accounted;
+    if (d <= 0) return;
+    ps->accounted = steps_now;
+    const unsigned long long np = ps->patches.size();
+    const hc_stepper* s0 = ps->patches[0];
+    const unsigned long long total = (unsigned long long)s0->sg.mx * s0->sg.my * s0->sg.mz * NV;
+    const unsigned long long active =
+        (unsigned long long)ps->pg.lnx * ps->pg.lny * ps->pg.lnz * NV;
+    const unsigned long long n = (unsigned long long)d;
+    ps->ledger[0] += total * np * n;   // uploads
+    ps->ledger[1] += total * np * n;   // downloads
+    ps->ledger[2] += np * n;           // scalar_uploads (dt)
+    ps->ledger[3] += np * n;           // scalar_downloads (dt_next)
+    ps->ledger[4] += active * np * n;  // uploads_active_only
+    ps->ledger[5] += n;                // steps
+}
 
 static int ps_exchange(hc_patchset* ps, int rel) {
     const size_t n = size_t(ps->pg.mx) * ps->pg.my * ps->pg.mz * ps->patches.size();
@@ -954,31 +976,29 @@ int hc_patchset_step(hc_patchset* ps, int n) {
             int rc = hc_stepper_advance(ps->patches[p]);
             if (rc) return rc;
         }
-        // TransferLedger (transfer.cpp:160-175): per patch per step, skinny strategy
-        const hc_stepper* s0 = ps->patches[0];
-        const unsigned long long total = (unsigned long long)s0->sg.mx * s0->sg.my * s0->sg.mz * NV;
-        const unsigned long long active =
-            (unsigned long long)ps->pg.lnx * ps->pg.lny * ps->pg.lnz * NV;
-        ps->ledger[0] += total * np;   // uploads
-        ps->ledger[1] += total * np;   // downloads
-        ps->ledger[2] += np;           // scalar_uploads (dt)
-        ps->ledger[3] += np;           // scalar_downloads (dt_next)
-        ps->ledger[4] += active * np;  // uploads_active_only
-        ps->ledger[5] += 1;            // steps
     }
     return HC_OK;
 }
 
 int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done) {
     int rc = HC_OK;
+    long first = -1;
     for (hc_stepper* s : ps->patches) {
-        int r = hc_stepper_sync(s, t, dt, steps_done);
+        long n = 0;
+        int r = hc_stepper_sync(s, t, dt, &n);
+        if (first < 0) first = n;
         if (r && !rc) rc = r;
     }
+    if (steps_done) *steps_done = first;
+    ps_account(ps, first);
     return rc;
 }
 
 int hc_patchset_ledger(hc_patchset* ps, unsigned long long* counts) {
+    long n = 0;
+    int rc = hc_stepper_sync(ps->patches[0], nullptr, nullptr, &n);
+    if (rc && rc != HC_UNPHYSICAL) return rc;
+    ps_account(ps, n);
     for (int i = 0; i < 6; ++i) counts[i] = ps->ledger[i];
     return HC_OK;
 }

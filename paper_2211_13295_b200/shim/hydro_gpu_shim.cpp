@@ -12,6 +12,7 @@
 //
 // Compiled against the reference headers (-I/root/reference/proj/include); nothing here is
 // copied from the reference sources.
+#include <chrono>
 #include <stdexcept>
 #include <string>
 
@@ -99,6 +100,21 @@ void add_profile(StageProfile* prof, const double* s) {
     prof->update += s[4];
     prof->transfer += s[5];
 }
+
+// Host wall time of a shim call that has no per-kernel device split (the reference's
+// StageTimer attribution in rk_step, stepper.cpp:145-156): adds the seconds to one field.
+class CallTimer {
+  public:
+    explicit CallTimer(double* field) : f_(field), t0_(std::chrono::steady_clock::now()) {}
+    ~CallTimer() {
+        if (f_)
+            *f_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+    }
+
+  private:
+    double* f_;
+    std::chrono::steady_clock::time_point t0_;
+};
 
 }  // namespace
 
@@ -263,9 +279,13 @@ void rk_step(ModalState& modal, SkinnyState& skinny, TimeState& time, const Patc
              const StepParams& par, StepScratch& scratch, BoundaryKind bc, StageProfile* prof) {
     rk_save_u0(skinny, g, scratch);
     for (const RkStage& stage : rk_stages(par.integrator)) {
-        apply_boundary(skinny, g, bc);
+        {
+            CallTimer t(prof ? &prof->transfer : nullptr);  // stepper.cpp:148-151
+            apply_boundary(skinny, g, bc);
+        }
         rk_stage(modal, skinny, time, g, par, scratch, stage, prof);
     }
+    CallTimer t(prof ? &prof->update : nullptr);  // stepper.cpp:154-155
     time.dt_next = compute_dt_next(modal, g, par.gas, time.cfl);
 }
 

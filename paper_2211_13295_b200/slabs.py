@@ -71,20 +71,22 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic
         # up, receive from below" on every rank so the k-th send to a peer always meets that
         # peer's k-th receive (lowest active planes -> its top ghosts, then highest -> its
         # bottom ghosts).
+        # The ghost ranges are whole contiguous planes of [z][y][x][5]: NCCL receives straight
+        # into them and sends straight from the active planes (no packing, no temporaries).
         ops = []
         bufs = []
-        rb = torch.empty_like(lo_ghost) if below is not None else None
-        ra = torch.empty_like(hi_ghost) if above is not None else None
+        staged = planes.is_cuda and dist.get_backend(group) == "gloo"
+        rb = lo_ghost if below is not None else None
+        ra = hi_ghost if above is not None else None
         if below is not None:
-            ops.append(dist.P2POp(dist.isend, lo_act.contiguous(), below, group))
+            ops.append(dist.P2POp(dist.isend, lo_act, below, group))
         if above is not None:
             ops.append(dist.P2POp(dist.irecv, ra, above, group))
-            ops.append(dist.P2POp(dist.isend, hi_act.contiguous(), above, group))
+            ops.append(dist.P2POp(dist.isend, hi_act, above, group))
             bufs.append((hi_ghost, ra))
         if below is not None:
             ops.append(dist.P2POp(dist.irecv, rb, below, group))
             bufs.append((lo_ghost, rb))
-        staged = planes.is_cuda and dist.get_backend(group) == "gloo"
         if staged:  # gloo moves host memory only (testing N>1 on one GPU): stage through it
             ops = [dist.P2POp(op.op, op.tensor.cpu() if op.op is dist.isend else
                               torch.empty(op.tensor.shape, dtype=op.tensor.dtype), op.peer,
@@ -92,11 +94,10 @@ def exchange_z_halos(planes, gh: int, nloc: int, rank: int, world: int, periodic
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        if staged:
+        if staged:  # the received host copies land in the ghost planes
             recvs = iter([op.tensor for op in ops if op.op is dist.irecv])
-            bufs = [(dst, next(recvs)) for dst, _ in bufs]
-        for dst, src in bufs:
-            dst.copy_(src)
+            for dst, _ in bufs:
+                dst.copy_(next(recvs))
     if not periodic:
         if below is None:
             lo_ghost.copy_(planes[gh:gh + 1].expand(gh, -1))
@@ -137,8 +138,10 @@ class SlabDomain:
         self.geom = g
         self.params = hydro.make_params(order, solver)
         self.api = hydro.HostApi()
-        self.st = hydro.Stepper(g, self.params, bc=(bc, bc, bc if world == 1 and not overlap
-                                                     else None),
+        # who fills the z ghosts is fixed here: the stepper itself only for a single rank that
+        # never overlaps; otherwise every step exchanges them (whatever step()'s overlap says)
+        self.owns_z = world == 1 and not overlap
+        self.st = hydro.Stepper(g, self.params, bc=(bc, bc, bc if self.owns_z else None),
                                 exact=exact, device=device, integrator=integrator)
         # every device op of the step (our kernels, NCCL, events) is ordered on one stream
         import torch
@@ -219,7 +222,7 @@ class SlabDomain:
         s = self.stream
         if overlap is None:
             overlap = self.overlap
-        if self.world == 1 and kernel_events is None and not overlap:
+        if self.owns_z and kernel_events is None and not overlap:
             self.st.step(1)
             return
         G = self.order  # stencil halo R + 1 (R = 1 at order 2, 2 at order 3)
@@ -228,7 +231,7 @@ class SlabDomain:
                 self.st.fill_ghosts()
                 if kernel_events is not None and k == 0:
                     kernel_events[0].record(s)
-                if overlap and self.nloc > 2 * G:
+                if overlap and not self.owns_z and self.nloc > 2 * G:
                     ready = torch.cuda.Event()
                     ready.record(s)
                     self.comm.wait_event(ready)
@@ -242,7 +245,7 @@ class SlabDomain:
                     self.st.compute_range(0, G, False)
                     self.st.compute_range(self.nloc - G, self.nloc, True)
                 else:
-                    if self.world > 1 or self.collectives:
+                    if not self.owns_z:
                         exchange_z_halos(self._planes(), self.geom.ghost, self.nloc,
                                          self.rank, self.world, self.periodic,
                                          p2p=self.collectives)

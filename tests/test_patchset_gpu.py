@@ -60,3 +60,20 @@ def test_patch_split_must_divide():
     g = hydro.make_geometry(24, 16, 20, 3)
     with pytest.raises(ValueError, match="divide"):
         hydro.PatchSet(g, 5, 1, 1, hydro.make_params(3))
+
+
+def test_ledger_counts_executed_steps_only():
+    """The device turns steps past t_final into no-ops; the TransferLedger counts the steps the
+    reference would have run (transfer.cpp:160-216), not the steps queued."""
+    g = hydro.make_geometry(16, 16, 16, 2)
+    api = hydro.HostApi()
+    s0 = api.init_isentropic_vortex(g, 2)
+    dt0 = api.initial_dt(g, s0, 0.6)
+    ps = hydro.PatchSet(g, 2, 1, 1, hydro.make_params(2))
+    ps.scatter(s0)
+    ps.set_time(0.0, dt0, 0.6, 3.5 * dt0)  # lands on t_final after a few steps
+    ps.step(40)
+    t, dt, done = ps.sync()
+    assert 0 < done < 40
+    assert ps.ledger()[5] == done
+    ps.close()

@@ -189,6 +189,10 @@ typedef struct {
 int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opts* o,
                       hc_stepper** out);
 int hc_stepper_destroy(hc_stepper* s);
+/* Which fused kernel the stepper launches: kernel = 1 for the persistent ring-free kernel
+ * (opt-in with HC_PERSIST=1 in the environment at create time; x/y periodic, nx a multiple
+ * of 32, every tile resident; ctas = its grid), 0 for the ring kernel (the default). */
+int hc_stepper_info(hc_stepper* s, int* kernel, int* ctas);
 /* stream used by every later call (cudaStream_t; NULL = a private stream) */
 int hc_stepper_set_stream(hc_stepper* s, void* stream);
 /* host skinny [mz][my][mx][5] (ghosts included) <-> device state; async on the stream when the

@@ -8,7 +8,7 @@
 
 #include <cstdlib>
 
-#include "fused_ader.cuh"
+#include "fused_persist.cuh"
 
 namespace hc {
 namespace HC_FUSED_NS {
@@ -62,8 +62,54 @@ static int launch_one(const FusedArgs& a, cudaStream_t st) {
     return launch_cfg<ORD, SOLVER, T::TX, T::TY, T::MINB, RK>(a, st);
 }
 
+// The ring-free persistent kernel (fused_persist.cuh). blocks_per_sm != nullptr: only report
+// how many of its CTAs fit on one SM (the launcher's co-residency check), no launch.
+template <int ORD, int SOLVER, bool RK>
+static int persist_one(const FusedArgs& a, const PersistLaunch* pl, cudaStream_t st,
+                       int* blocks_per_sm) {
+    using S = PersistShape<ORD>;
+    auto kern = persist_ader_kernel<ORD, SOLVER, RK>;
+    static unsigned long long configured = 0;  // per device, as launch_cfg
+    int dev = 0;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return cuda_fail(de, "cudaGetDevice");
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+        cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(persist)");
+        __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+    }
+    if (blocks_per_sm) {
+        cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, S::NT, S::SMEM);
+        return e == cudaSuccess ? HC_OK : cuda_fail(e, "occupancy(persist)");
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(pl->args.ntx), unsigned(pl->args.nty), 1);
+    cfg.blockDim = dim3(S::NT, 1, 1);
+    cfg.dynamicSmemBytes = S::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: they wait on each other
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, pl->args);
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "persist_ader_kernel launch");
+}
+
 template <int ORD, bool RK>
-static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
+static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st, const PersistLaunch* pl,
+                         int* bps) {
+    if (pl || bps) {
+        switch (solver) {
+            case 0: return persist_one<ORD, 0, RK>(a, pl, st, bps);
+            case 1: return persist_one<ORD, 1, RK>(a, pl, st, bps);
+            case 2: return persist_one<ORD, 2, RK>(a, pl, st, bps);
+            default: return persist_one<ORD, 3, RK>(a, pl, st, bps);
+        }
+    }
     switch (solver) {
         case 0: return launch_one<ORD, 0, RK>(a, st);
         case 1: return launch_one<ORD, 1, RK>(a, st);
@@ -74,16 +120,18 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st) {
 
 }  // namespace HC_FUSED_NS
 
-int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st) {
+int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st,
+                      const PersistLaunch* pl, int* persist_blocks_per_sm) {
     using namespace HC_FUSED_NS;
+    int* b = persist_blocks_per_sm;
     if (rk) {
-        if (order == 2) return launch_solver<2, true>(a, solver, st);
-        return order == 3 ? launch_solver<3, true>(a, solver, st)
-                          : launch_solver<4, true>(a, solver, st);
+        if (order == 2) return launch_solver<2, true>(a, solver, st, pl, b);
+        return order == 3 ? launch_solver<3, true>(a, solver, st, pl, b)
+                          : launch_solver<4, true>(a, solver, st, pl, b);
     }
-    if (order == 2) return launch_solver<2, false>(a, solver, st);
-    return order == 3 ? launch_solver<3, false>(a, solver, st)
-                      : launch_solver<4, false>(a, solver, st);
+    if (order == 2) return launch_solver<2, false>(a, solver, st, pl, b);
+    return order == 3 ? launch_solver<3, false>(a, solver, st, pl, b)
+                      : launch_solver<4, false>(a, solver, st, pl, b);
 }
 
 }  // namespace hc

@@ -2,6 +2,8 @@
 // driver (stepper.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace hc {
@@ -51,7 +53,54 @@ struct FusedTile {
     static constexpr int MINB = 2;  // resident CTAs per SM the registers must allow
 };
 
-int launch_fused_exact(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st);
-int launch_fused_fast(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st);
+// ---- the persistent ring-free kernel's exchange (fused_persist.cuh)
+// One exchanged face state or face flux (5 doubles), on its own 64-byte line.
+struct alignas(64) XRec {
+    double v[NV];
+};
+
+struct PersistHdr {
+    unsigned long long epoch;  // launches so far (+1): the high bits of every sequence number
+    unsigned int done;         // CTAs finished in the current launch
+    unsigned int timeout;      // a neighbour wait gave up (reported by the host)
+};
+
+constexpr int PX_TX = 32;   // tile width: one warp per tile row
+constexpr int PX_TYM = 7;   // rows per tile at most
+constexpr int PX_SLOTS = 4;  // exchange slots (plane p uses slot p % 4)
+// exchange records per tile and slot: +x states of the east column, +y states of the north
+// row, west boundary fluxes, south boundary fluxes
+constexpr int PX_XS = 0, PX_YS = PX_TYM, PX_XF = PX_TYM + PX_TX, PX_YF = 2 * PX_TYM + PX_TX;
+constexpr int PX_REC = 2 * (PX_TYM + PX_TX);
+constexpr int PX_FLAG_STRIDE = 16;  // u64 per flag: one 128-byte line each
+// per-thread carried values of the edge zones (global scratch, read back by the same thread):
+// fluxes W, E, S, N of the last two planes, bottom z flux of the last two planes, the
+// zone's -x and -y face states of the last two planes
+constexpr int PX_SCR_FL = 0, PX_SCR_FZ = 40, PX_SCR_MX = 50, PX_SCR_MY = 60, PX_SCR = 70;
+
+struct PersistArgs {
+    XRec* rec;                // [tile][slot][PX_REC]
+    unsigned long long* flag;  // [tile][row] x PX_FLAG_STRIDE: last plane the row published
+    double* scr;              // [tile][thread][PX_SCR]
+    PersistHdr* hdr;
+    const CUtensorMap* maps;  // [3] in device memory: one TMA map per state buffer
+    int ntx, nty;             // tiles along x (nx / 32) and y
+};
+
+struct PersistLaunch {
+    PersistArgs args;
+};
+
+// TMA box of one plane for the persistent kernel: (32 + 2 gh) zones x 5 doubles, 7 + 2R rows
+inline int px_box_w(int order) { return PX_TX + 2 * (order >= 3 ? 3 : 2); }
+inline int px_box_h(int order) { return PX_TYM + 2 * (order >= 3 ? 2 : 1); }
+
+// pl == nullptr: the ring kernel (fused_ader.cuh); else the persistent ring-free kernel
+// (fused_persist.cuh) with these exchange buffers and tensor maps. persist_blocks_per_sm !=
+// nullptr: only report the persistent kernel's resident CTAs per SM.
+int launch_fused_exact(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st,
+                       const PersistLaunch* pl = nullptr, int* persist_blocks_per_sm = nullptr);
+int launch_fused_fast(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st,
+                      const PersistLaunch* pl = nullptr, int* persist_blocks_per_sm = nullptr);
 
 }  // namespace hc

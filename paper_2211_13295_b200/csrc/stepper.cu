@@ -8,10 +8,12 @@
 // that performs the harness's dt/dt_next hand-off and t_final clip on the device
 // (harness.cpp:155-170), so any number of steps queue on the stream without a host sync.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "fused_types.cuh"
@@ -132,6 +134,9 @@ struct hc_stepper {
     cudaGraphExec_t graph = nullptr;
     double graph_cfl = -1.0;
     long graph_launches = 0;  // kernels per replayed step
+    // the persistent ring-free kernel (fused_persist.cuh), when the mesh allows it
+    bool persist = false;
+    PersistLaunch pl{};
 };
 
 namespace {
@@ -199,6 +204,86 @@ FusedArgs fused_args(const hc_stepper* s) {
 
 
 }  // namespace
+
+// Enables the persistent ring-free kernel (fused_persist.cuh) when the mesh allows it: x and y
+// periodic (a tile's neighbour across the mesh edge holds exactly the zone the ring would
+// recompute), nx a multiple of the 32-wide tile, 16-byte row pitch (TMA strides), and every
+// tile resident at once (nx/32 x nty CTAs within the occupancy). Opt-in (HC_PERSIST=1): it
+// is bit-identical to the ring kernel but measured 1.8x slower at 256^3.
+static int setup_persist(hc_stepper* s) {
+    const char* v = std::getenv("HC_PERSIST");
+    if (!v || std::atoi(v) == 0) return HC_OK;
+    const hc_geom& g = s->g;
+    if (s->o.bc[0] != HC_PERIODIC || s->o.bc[1] != HC_PERIODIC) return HC_OK;
+    // TMA boxes start on 16-byte boundaries: tile origins x0 = 32 k and an x halo equal to
+    // the storage ghost width, so the box starts at storage column 32 k
+    if (g.nx % PX_TX || (s->sg.pitch & 1) || g.ghost != (s->p.order >= 3 ? 3 : 2)) return HC_OK;
+    const bool rk = s->o.integrator != 0;
+    int bps = 0, sms = 0;
+    FusedArgs a = fused_args(s);
+    int rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, nullptr, nullptr, &bps)
+                        : launch_fused_fast(a, s->p.order, s->p.solver, rk, nullptr, nullptr, &bps);
+    if (rc) return rc;
+    HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->o.device));
+    const long cap = long(bps) * sms;
+    const int ntx = g.nx / PX_TX;
+    if (cap < ntx) return HC_OK;
+    int nty = int(std::min<long>(g.ny, cap / ntx));  // spread over every resident slot
+    if (const char* v = std::getenv("HC_PERSIST_NTY"))  // tests: force taller tiles
+        nty = std::max(1, std::min(nty, std::atoi(v)));
+    if (long(nty) * PX_TYM < g.ny) return HC_OK;    // tiles would exceed 7 rows
+    PersistArgs& pa = s->pl.args;
+    pa.ntx = ntx;
+    pa.nty = nty;
+    const size_t tiles = size_t(ntx) * nty;
+    const size_t nrec = tiles * PX_SLOTS * PX_REC;
+    const size_t nflag = tiles * PX_TYM * PX_FLAG_STRIDE;
+    const size_t nscr = tiles * PX_TX * PX_TYM * PX_SCR;
+    HC_CUDA(cudaMalloc(&pa.rec, nrec * sizeof(XRec)));
+    HC_CUDA(cudaMalloc(&pa.flag, nflag * sizeof(unsigned long long)));
+    HC_CUDA(cudaMalloc(&pa.scr, nscr * sizeof(double)));
+    HC_CUDA(cudaMalloc(&pa.hdr, sizeof(PersistHdr)));
+    HC_CUDA(cudaMemsetAsync(pa.rec, 0, nrec * sizeof(XRec), s->st));
+    HC_CUDA(cudaMemsetAsync(pa.flag, 0, nflag * sizeof(unsigned long long), s->st));
+    PersistHdr h0{};
+    h0.epoch = 1;
+    HC_CUDA(cudaMemcpyAsync(pa.hdr, &h0, sizeof h0, cudaMemcpyHostToDevice, s->st));
+    // one TMA tensor map per state buffer: dims (x * 5 doubles, y rows, z planes)
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    HC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) {
+        set_error(HC_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return HC_CUDA;
+    }
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    const SG& sg = s->sg;
+    const cuuint64_t dims[3] = {cuuint64_t(sg.mx) * NV, cuuint64_t(sg.my), cuuint64_t(sg.mz)};
+    const cuuint64_t strides[2] = {cuuint64_t(sg.pitch) * sizeof(double),
+                                   cuuint64_t(sg.my_pad) * sg.pitch * sizeof(double)};
+    const cuuint32_t box[3] = {cuuint32_t(px_box_w(s->p.order) * NV),
+                               cuuint32_t(px_box_h(s->p.order)), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap maps[3];
+    std::memset(maps, 0, sizeof maps);
+    for (int i = 0; i < s->nbuf; ++i) {
+        CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, s->buf[i], dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error(HC_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+            return HC_CUDA;
+        }
+    }
+    // the maps live in device memory (written before any launch reads them)
+    CUtensorMap* dmaps = nullptr;
+    HC_CUDA(cudaMalloc(&dmaps, sizeof maps));
+    HC_CUDA(cudaMemcpy(dmaps, maps, sizeof maps, cudaMemcpyHostToDevice));
+    pa.maps = dmaps;
+    s->persist = true;
+    return HC_OK;
+}
 
 static size_t state_bytes(const hc_stepper* s) {
     return size_t(s->sg.mz) * s->sg.my * s->sg.mx * NV * sizeof(double);
@@ -310,6 +395,12 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         hc_stepper_destroy(s);
         return rc;
     }
+    if ((rc = setup_persist(s)) || (rc = (cudaStreamSynchronize(s->st) == cudaSuccess
+                                              ? HC_OK : cuda_fail(cudaGetLastError(),
+                                                                  "persist setup")))) {
+        hc_stepper_destroy(s);
+        return rc;
+    }
     *out = s;
     return HC_OK;
 }
@@ -323,6 +414,11 @@ int hc_stepper_destroy(hc_stepper* s) {
     cudaFree(s->buf[2]);
     cudaFree(s->ctl);
     cudaFree(s->eb);
+    cudaFree(s->pl.args.rec);
+    cudaFree(s->pl.args.flag);
+    cudaFree(s->pl.args.scr);
+    cudaFree(s->pl.args.hdr);
+    cudaFree(const_cast<CUtensorMap*>(s->pl.args.maps));
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     if (s->graph) cudaGraphExecDestroy(s->graph);
     if (s->s_h2d) cudaStreamDestroy(s->s_h2d);
@@ -456,8 +552,9 @@ int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last)
         a.want_dt = k == ns - 1;
     }
     if (kz_last > kz_first) {
-        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st)
-                        : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st);
+        const PersistLaunch* pl = s->persist ? &s->pl : nullptr;
+        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st, pl)
+                        : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st, pl);
         if (rc) return rc;
         s->launches++;
     }
@@ -679,7 +776,23 @@ int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done) {
     if (t) *t = c.t;
     if (dt) *dt = c.dt;
     if (steps_done) *steps_done = long(c.steps);
+    if (s->persist) {
+        unsigned int to = 0;
+        HC_CUDA(cudaMemcpy(&to, &s->pl.args.hdr->timeout, sizeof to, cudaMemcpyDeviceToHost));
+        if (to) {
+            set_error(HC_CUDA, "persistent fused kernel: a tile-exchange wait timed out "
+                               "(CTAs not co-resident); results are invalid");
+            return HC_CUDA;
+        }
+    }
     return report_device_errors(eb);
+}
+
+int hc_stepper_info(hc_stepper* s, int* kernel, int* ctas) {
+    if (!s) return HC_INVALID;
+    if (kernel) *kernel = s->persist ? 1 : 0;
+    if (ctas) *ctas = s->persist ? s->pl.args.ntx * s->pl.args.nty : 0;
+    return HC_OK;
 }
 
 int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {

@@ -398,6 +398,12 @@ class Stepper:
     def launches(self) -> int:
         return self.lib.hc_stepper_launches(self.h)
 
+    def kernel_info(self):
+        """("persistent", ctas) for the ring-free persistent kernel, ("ring", 0) otherwise."""
+        k, n = C.c_int(), C.c_int()
+        _check(self.lib.hc_stepper_info(self.h, C.byref(k), C.byref(n)))
+        return ("persistent" if k.value else "ring"), n.value
+
 
 def fp64_peak(device: int = 0) -> float:
     """Measured DFMA throughput of the device in TFLOP/s (hc_fp64_peak)."""

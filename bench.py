@@ -35,19 +35,31 @@ METRIC = "zone-updates/sec (M/s) per GPU and 8-GPU box, % of HBM/FP64 roofline"
 UNIT = "Mzone-updates/s"
 
 
-def flops_per_zone(n, order, solver):
+def flops_per_zone(n, order, solver, ny=None, nz=None):
     """Algorithmic FP64 flops per active zone-update of the reference as written (add, sub,
     mul, div, sqrt = 1): F = R(recon+pred) + Phi*face + cross + 70 with
-    R = ((n+2)/n)^3 (ring), Phi = 3(n+1)/n (faces)."""
+    R = ring zones / active zones ((n+2)/n)^3 on a cube) and Phi = faces / active zones
+    (3(n+1)/n on a cube); C1 (128 x 128 x 4) gives 2837."""
     # order 4 (WENO-AO extension, no reference): 15 WENO-AO points x ~135 flops (6 divisions)
     # plus the quartic face extrapolations, counted by hand from the restatement as written
     recon, pred = {2: (120.0, 258.0), 3: (810.0, 543.0), 4: (2265.0, 543.0)}[order]
     face = {2: {1: 168.0, 0: 154.0}, 3: {1: 188.0, 0: 174.0},
             4: {1: 188.0, 0: 174.0}}[order].get(solver, 188.0)
     cross = 60.0 if order == 3 else 0.0
-    R = ((n + 2.0) / n) ** 3
-    phi = 3.0 * (n + 1.0) / n
+    nx = float(n)
+    ny = float(ny or n)
+    nz = float(nz or n)
+    act = nx * ny * nz
+    R = (nx + 2.0) * (ny + 2.0) * (nz + 2.0) / act
+    phi = ((nx + 1.0) * ny * nz + nx * (ny + 1.0) * nz + nx * ny * (nz + 1.0)) / act
     return R * (recon + pred) + phi * face + cross + 70.0
+
+
+def fp64_nominal_tflops(device, max_mhz):
+    """Nominal DFMA rate: SMs x 64 FP64 lanes x 2 flop x the maximum SM clock."""
+    import torch
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return sms * 64 * 2 * max_mhz * 1e6 / 1e12
 
 
 BYTES_PER_ZONE = 80.0  # read + write U_skinny (5 doubles), SURVEY.md 8(d)
@@ -130,6 +142,11 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def mesh_of(args):
+    """(nx, ny, nz) of the workload on one GPU / one CPU run."""
+    return (128, 128, 4) if args.workload == "c1" else (args.n, args.n, args.n)
+
+
 def run_reference_cpu(n, order, steps, threads):
     """The reference's own harness (hydro::run_benchmark, harness.cpp:222-227) from
     oracle/_ref (built from /root/reference/proj/src); zones/s as it computes it
@@ -142,13 +159,14 @@ def run_reference_cpu(n, order, steps, threads):
         zps, _, _, _ = ref.run_benchmark(0, order, 0, 1, n, steps, threads=threads)
         return zps, "reference", threads
     orc = po.Oracle()
-    g = po.make_geometry(n, n, n, order)
+    nx, ny, nz = (n, n, n) if isinstance(n, int) else n
+    g = po.make_geometry(nx, ny, nz, order)
     s = orc.init_isentropic_vortex(g, order)
     cfl = 0.6 if order == 2 else 0.4
     dt0 = orc.initial_dt(g, s, cfl)
     t0 = time.perf_counter()
     orc.run_steps(g, po.make_params(order), po.PERIODIC, cfl, steps, s, dt0)
-    return n ** 3 * steps / (time.perf_counter() - t0), "port", 1
+    return nx * ny * nz * steps / (time.perf_counter() - t0), "port", 1
 
 
 def reference_arm(args):
@@ -158,46 +176,61 @@ def reference_arm(args):
     if rank != 0:
         return
     threads = cpu_threads()
-    n, order = args.n, args.order
-    # bounded sample: one warm-up step measures the step cost, then up to K timed steps,
+    mesh, order = mesh_of(args), args.order
+    zones = mesh[0] * mesh[1] * mesh[2]
+    # W warm-up steps (untimed; they also measure the step cost), then up to K timed steps,
     # capped so the timed part stays near 2 minutes of host time
-    zps1, kind, cores = run_reference_cpu(n, order, 1, threads)
-    step_s = n ** 3 / zps1
+    zps1, kind, cores = run_reference_cpu(mesh, order, max(1, args.warmup), threads)
+    step_s = zones / zps1
     steps = max(1, min(args.steps, int(120.0 / max(step_s, 1e-3))))
-    zps, kind, cores = run_reference_cpu(n, order, steps, threads)
+    zps, kind, cores = run_reference_cpu(mesh, order, steps, threads)
     val = zps / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": 1,
-        "ms_per_step": n ** 3 / zps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": zones / zps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (isentropic vortex IC)",
-        "config": dict(workload_config(args),
-                       build=("the reference's C++ (oracle/_ref: g++ -O3 -march=x86-64-v3 "
-                              "-ffp-contract=off -fopenmp, its own sources)")
-                       if kind == "reference" else "C restatement (oracle/, single thread)"),
+        "config": workload_config(args),
+        "build": ("the reference's C++ (oracle/_ref: g++ -O3 -march=x86-64-v3 "
+                  "-ffp-contract=off -fopenmp, its own sources)")
+                 if kind == "reference" else "C restatement (oracle/, single thread)",
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{n}^3 O{order} HLL ADER vortex, {steps} timed steps (of K="
-                                   f"{args.steps} requested, capped at ~120 s) via "
-                                   "hydro::run_benchmark on the host cores"},
+                         "sample": f"{'x'.join(map(str, mesh))} O{order} HLL ADER vortex, "
+                                   f"{steps} timed steps (of K={args.steps} requested, capped "
+                                   "at ~120 s) via hydro::run_benchmark on the host cores"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 def workload_config(args):
+    """The workload, identical in both arms (the build of each arm is the line's "build")."""
+    if args.workload == "c1":
+        return {
+            "workload": ("C1: 2D Euler isentropic vortex 128 x 128 (x 4 z-invariant planes, "
+                         "the reference's minimum), WENO-ADER O3 + HLL, periodic, on [-5,5]^3 "
+                         "(configs[0], the reference's CPU-runnable case)"),
+            "n": [128, 128, 4], "order": args.order, "solver": "hll", "integrator": "ader",
+            "problem": "vortex",
+            "l2": "state 7.2 MB fits L2: launch/latency-bound (absolute rate only)",
+            "parallelism": f"{args.gpus} independent replicas" if args.gpus > 1
+            else "single GPU"}
     return {
         "workload": (f"C2: 3D Euler isentropic vortex {args.n}^3 per GPU, WENO-ADER O{args.order}"
                      " + HLL, periodic (configs[1]; the reference has no O4, O3 is its closest"
                      "; --order 4 runs the WENO-AO extension)"),
         "n": args.n, "order": args.order, "solver": "hll", "integrator": "ader",
         "problem": "vortex",
-        "build": ("fma (DFMA contraction + ~2-ulp division; <= 1e-12 rel. L1 vs the reference "
-                  "after 20 steps, tests/test_gpu_parity.py)") if args.fast else
-                 "bit-exact (identical to the reference build)",
         "l2": "state 2 x {:.0f} MB per GPU > 126 MB L2 (no flush needed)".format(
             (args.n + 2 * args.order) ** 3 * 40 / 1e6),
         "parallelism": f"z-slab x{args.gpus}" if args.gpus > 1 else "single GPU",
     }
+
+
+def build_of(args):
+    return ("fma (DFMA contraction + ~2-ulp division; <= 7e-16 rel. L1 vs the reference after "
+            "5 steps at 256^3, tests/test_fullsize_parity_gpu.py)") if args.fast else \
+        "bit-exact (identical to the reference build)"
 
 
 # ---------------------------------------------------------------------- MHD (extension)
@@ -412,11 +445,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only-timed", action="store_true",
                     help="profiling runs (ncu launch lists): warm-up + timed steps only")
-    ap.add_argument("--workload", default="euler", choices=["euler", "mhd", "ced"],
-                    help="euler: configs[1] (the headline); mhd: configs[2], 3D Orszag-Tang "
-                         "with CT + the multidimensional Riemann solver (extension, 384^3)")
+    ap.add_argument("--workload", default="euler", choices=["euler", "c1", "mhd", "ced"],
+                    help="euler: configs[1] (the headline, 256^3); c1: configs[0] (128 x 128 "
+                         "x 4, the reference's CPU-runnable case); mhd: configs[2], 3D "
+                         "Orszag-Tang with CT + the multidimensional Riemann solver "
+                         "(extension, 384^3); ced: configs[3] (extension, 256^3)")
     args = ap.parse_args()
     args.fast = not args.exact
+    if args.workload == "c1" and "--steps" not in sys.argv:
+        args.steps = 50  # C1 is quoted over 50 steps
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
     if args.workload == "ced":
@@ -452,8 +489,29 @@ def main():
     assert world == args.gpus or world == 1, "launch N>1 with torchrun --nproc-per-node N"
 
     n, order = args.n, args.order
-    dom = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
-                           exact=not args.fast)
+    mesh = mesh_of(args)
+    c1 = args.workload == "c1"
+
+    def make_domain(exact):
+        if c1:  # configs[0]: one independent replica per rank, the reference's geometry
+            return slabs.SlabDomain(128, 128, 4, order, rank=0, world=1, device=local,
+                                    exact=exact, dz=2.5)
+        return slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
+                                exact=exact)
+
+    def max_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+    dom = make_domain(not args.fast)
     s0 = dom.initial_state()
     cfl = 0.6 if order == 2 else 0.4
     dt0 = dom.initial_dt(s0, cfl)
@@ -466,7 +524,7 @@ def main():
         for _ in range(args.warmup):
             d.step()
         torch.cuda.synchronize()
-        d.barrier()
+        barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
@@ -476,22 +534,27 @@ def main():
             d.step(kernel_events=kev[k])
         ev1.record(d.stream)
         torch.cuda.synchronize()
-        d.barrier()
+        barrier()
         ms = ev0.elapsed_time(ev1)
         kern = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-        return d.max_over_ranks(ms), kern, d.launches - l0
+        return max_ranks(ms), kern, d.launches - l0
 
     with ClockSampler(local) as clocks:
         ms_max, kern_ms, launches = timed(dom)
     t, dt, done = dom.sync()
 
-    zones_local = n ** 3
+    zones_local = mesh[0] * mesh[1] * mesh[2]
     zones_total = zones_local * world
     value = zones_total * args.steps / (ms_max * 1e-3) / 1e6
 
-    # roofline of the dominant kernel (the fused step), per launch on this rank
-    fpz = flops_per_zone(n, order, 1)
-    peak_fp64 = hydro.fp64_peak(local)
+    # roofline of the dominant kernel (the fused step), per launch on this rank. Denominator:
+    # the nominal DFMA rate at the maximum SM clock (MEASURED_PEAKS.json has no FP64 figure);
+    # the in-run DFMA probe (hc_fp64_peak) and the clock it ran at are reported beside it.
+    fpz = flops_per_zone(mesh[0], order, 1, mesh[1], mesh[2])
+    with ClockSampler(local) as pclk:
+        probe_fp64 = hydro.fp64_peak(local)
+    max_mhz = clocks.max_mhz or pclk.max_mhz or 1965
+    peak_fp64 = fp64_nominal_tflops(local, max_mhz)
     achieved = fpz * zones_local / (kern_ms * 1e-3) / 1e12
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
@@ -499,8 +562,12 @@ def main():
     roofline = {
         "bound": "fp64", "achieved": achieved, "peak": peak_fp64, "unit": "TFLOP/s",
         "frac": achieved / peak_fp64,
-        "peak_source": "DFMA throughput measured in this run (hc_fp64_peak); "
-                       "MEASURED_PEAKS.json has no FP64 figure",
+        "peak_source": f"nominal DFMA rate (SMs x 64 lanes x 2 flop x {max_mhz} MHz max SM "
+                       "clock; MEASURED_PEAKS.json has no FP64 figure)",
+        "peak_probe": {"value": probe_fp64, "unit": "TFLOP/s", "clocks": pclk.summary(),
+                       "frac": achieved / probe_fp64,
+                       "source": "hc_fp64_peak: 16 DFMA chains per thread, 32 warps per SM, "
+                                 "best of 10 launches, this process"},
         "flops_per_zone": fpz, "kernel_ms_per_launch": kern_ms,
         "traffic": None,
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -509,7 +576,9 @@ def main():
     }
     # the binding unit's busy fraction from the committed ncu capture of this kernel
     prof = os.path.join(ROOT, "profiles",
-                        f"r1_fused_o{order}_{n}_{'fma' if args.fast else 'exact'}.json")
+                        f"r2_fused_o{order}_{n}_{'fma' if args.fast else 'exact'}.json")
+    if not os.path.exists(prof):
+        prof = prof.replace("r2_", "r1_")
     if os.path.exists(prof):
         with open(prof) as f:
             k0 = json.load(f)["kernels"][0]
@@ -525,6 +594,11 @@ def main():
             roofline["traffic_per_zone"] = tj["bytes_per_zone"]
             roofline["traffic_source"] = tj["source"]
 
+    if c1:  # launch-bound, fits L2: no HBM / traffic figures apply
+        roofline["traffic"] = None
+        for k in ("fp64_pipe_busy_ncu", "fp64_pipe_source", "hbm", "traffic_per_zone",
+                  "traffic_source"):
+            roofline.pop(k, None)
     if args.only_timed:
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -539,8 +613,8 @@ def main():
     host[...] = s0
 
     def e2e_step():
-        if world == 1:  # H2D / fused step / D2H pipelined by z-chunks
-            dom.st.step_host(host, host, args.e2e_chunks)
+        if world == 1 or c1:  # H2D / fused step / D2H pipelined by z-chunks
+            dom.st.step_host(host, host, 1 if c1 else args.e2e_chunks)
         else:  # slab: upload, step with the NCCL halo exchange, download
             dom.upload(host)
             dom.step()
@@ -548,28 +622,28 @@ def main():
         dom.sync()
     e2e_step()  # untimed warm-up: creates the copy streams and events of the pipeline
     torch.cuda.synchronize()
-    dom.barrier()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.e2e_steps):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = dom.max_over_ranks(e0.elapsed_time(e1))
+    e_ms = max_ranks(e0.elapsed_time(e1))
     # world 1: step_host moves only the active zones (40 B each) both ways; N>1: whole slabs
-    nbytes = zones_local * 40 if world == 1 else host.nbytes
+    nbytes = zones_local * 40 if (world == 1 or c1) else host.nbytes
     e2e = {"value": zones_total * args.e2e_steps / (e_ms * 1e-3) / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": (nbytes + 16) * world,
            "steps": args.e2e_steps,
            "api": ("hc_stepper_step_host (H2D of the active U_skinny zones, fused step, D2H, "
                    "pipelined in "
-                   f"{args.e2e_chunks} z-chunks) + hc_stepper_sync (dt_next)") if world == 1 else
+                   f"{1 if c1 else args.e2e_chunks} z-chunks) + hc_stepper_sync (dt_next)")
+           if (world == 1 or c1) else
                   "per rank: hc_stepper_upload + slab step (NCCL halos) + hc_stepper_download"}
 
     # the other contraction policy on the same workload (bit-exact build when the headline is
     # the FMA build and vice versa), reported beside the headline
-    other = slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
-                             exact=args.fast)
+    other = make_domain(args.fast)
     other.upload(s0)
     other.set_time(0.0, dt0, cfl)
     o_ms, o_kern, _ = timed(other)
@@ -577,16 +651,18 @@ def main():
     other_line = {"build": "bit-exact" if args.fast else "fma",
                   "value": zones_total * args.steps / (o_ms * 1e-3) / 1e6, "unit": UNIT,
                   "ms_per_step": o_ms / args.steps, "kernel_ms_per_launch": o_kern,
-                  "roofline_frac": fpz * zones_local / (o_kern * 1e-3) / 1e12 / peak_fp64}
+                  "roofline_frac": fpz * zones_local / (o_kern * 1e-3) / 1e12 / peak_fp64,
+                  "roofline_frac_probe": fpz * zones_local / (o_kern * 1e-3) / 1e12 / probe_fp64}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
-        c_n = n
-        zps, kind, cores = run_reference_cpu(c_n, order, 2, threads)
+        c_steps = 10 if c1 else 2
+        zps, kind, cores = run_reference_cpu(mesh, order, c_steps, threads)
         cpu = {"value": zps / 1e6, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"{c_n}^3 O{order} HLL ADER vortex, 2 steps through "
-                         "hydro::run_benchmark (harness wall clock), default OpenMP placement"}
+               "sample": f"{'x'.join(map(str, mesh))} O{order} HLL ADER vortex, {c_steps} steps "
+                         "through hydro::run_benchmark (harness wall clock), default OpenMP "
+                         "placement"}
         z1, _, _ = run_reference_cpu(128, order, 1, 1)  # also one thread
         cpu["single_thread"] = {"value": z1 / 1e6, "unit": UNIT, "cores": 1,
                                 "sample": f"128^3 O{order}, 1 step, 1 thread"}
@@ -597,7 +673,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (isentropic vortex IC sampled on the host, problems.cpp)",
-            "config": workload_config(args), "roofline": roofline, "cpu_baseline": cpu,
+            "config": workload_config(args), "build": build_of(args), "roofline": roofline,
+            "cpu_baseline": cpu,
             "e2e": e2e, "other_build": other_line, "gpu_launches": launches,
             "clocks": clocks.summary(),
             "final": {"t": t, "dt_next": dt, "steps_done": done},

@@ -366,13 +366,28 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     double* red = YP + S::YP_N * NV;                // [32]
 
     const int tid = threadIdx.x;
-    double* part = red + 32 + tid;          // [NV] stride TX*TY (owned threads only)
+    // E-column index of this thread. a.interleave = 0: tile columns on the first warps, ring
+    // columns on the last; 1: every warp holds (NE / warps) columns, tile and ring mixed, so
+    // the phases after the predictor (faces, update) weigh the same on every warp
+    int eidx = tid;
+    {
+        constexpr int NW = S::NT / 32, TPW = TX * TY / NW, RPW = (S::NE - TX * TY) / NW;
+        // (only tile shapes whose tile and ring columns split evenly over the warps)
+        if constexpr (TX * TY % NW == 0 && (S::NE - TX * TY) % NW == 0 && TPW + RPW <= 32) {
+            if (a.interleave) {
+                const int w = tid >> 5, l = tid & 31;
+                eidx = l < TPW ? w * TPW + l
+                               : (l < TPW + RPW ? TX * TY + w * RPW + (l - TPW) : S::NE + w);
+            }
+        }
+    }
+    double* part = red + 32 + eidx;         // [NV] stride TX*TY (owned threads only)
     double* fz_prev = part + NV * TX * TY;  // [NV] stride TX*TY
     // ---- E-column of this thread
     int ci, cj;
     bool is_tile;
     {
-        int t = tid;
+        int t = eidx;
         if (t >= S::NE) {  // padding lanes: no column
             ci = cj = -(1 << 20);
             is_tile = false;
@@ -472,7 +487,7 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
     if (owned) dt_min[0] = 1.0e32;
     // offset (doubles) of this column's zone in a smem plane, kept in shared memory and read
     // where used (a register copy would be spilled)
-    int* zoff = reinterpret_cast<int*>(dt_min - tid + CS) + tid;
+    int* zoff = reinterpret_cast<int*>(dt_min - eidx + CS) + tid;
     zoff[0] = ((cj + G) * W + (ci + G)) * NV;
 
     for (int lp = -1; lp <= nzc; ++lp) {

@@ -33,6 +33,12 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     // origins at multiples of TX, TX + 2G even) and an even row pitch; else per-8-byte cp.async
     FusedArgs b = a;
     b.bulk = (a.gh == S::G && (a.pitch & 1) == 0) ? 1 : 0;
+    static const int inter = [] {
+        const char* v = std::getenv("HC_INTERLEAVE");
+        return v ? std::atoi(v) : 0;
+    }();
+    constexpr int NW = S::NT / 32;
+    b.interleave = (inter && (TX * TY) % NW == 0 && (S::NE - TX * TY) % NW == 0) ? 1 : 0;
     dim3 grid((a.nx + TX - 1) / TX, (a.ny + TY - 1) / TY,
               (a.kz_last - a.kz_first + a.tz - 1) / a.tz);
     kern<<<grid, S::NT, S::SMEM, st>>>(b);

@@ -27,6 +27,7 @@ struct FusedArgs {
     int out_rel;     // and writes buf[(cur + out_rel) % nbuf]
     int want_dt;     // take the CFL estimate (ADER: always; RK: last stage)
     int bulk;        // plane loads by bulk copy (set by the launcher)
+    int interleave;  // ring kernel: tile and ring E-columns mixed on every warp (launcher)
     double rk_a, rk_b;  // RK stage coefficients U' = a U0 + b (U + dt rate)
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width

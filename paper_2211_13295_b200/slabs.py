@@ -117,7 +117,8 @@ class SlabDomain:
     """One rank's slab of an ``nx x ny x nz_global`` mesh on [-5,5]^2 x [-5, -5 + nz*dz]."""
 
     def __init__(self, nx, ny, nz_global, order, rank=0, world=1, device=0, exact=True,
-                 solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER, overlap=None):
+                 solver=hydro.HLL, bc=PERIODIC, dx=None, integrator=hydro.ADER, overlap=None,
+                 dz=None):
         self.rank, self.world, self.order = rank, world, order
         # overlap: interior planes computed while the z halos are exchanged. Off by default:
         # splitting the fused launch into interior + two boundary ranges costs more than the
@@ -132,7 +133,9 @@ class SlabDomain:
         g = hydro.Geom()
         g.nx, g.ny, g.nz, g.ghost = nx, ny, self.nloc, hydro.ghost_for_order(order)
         g.dx = g.dy = g.dz = d
-        g.origin[0], g.origin[1], g.origin[2] = -5.0, -5.0, -5.0 + self.z0 * d
+        if dz is not None:  # e.g. configs[0]: 128 x 128 x 4 on [-5, 5]^3 (dz = 2.5)
+            g.dz = dz
+        g.origin[0], g.origin[1], g.origin[2] = -5.0, -5.0, -5.0 + self.z0 * g.dz
         # the vortex is columnar (problems.cpp:11-38), so every slab samples the same
         # (x, y) profile as the single-GPU mesh
         self.geom = g

@@ -24,3 +24,16 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_reference_arm_c1_line_matches_our_config_keys():
+    """configs[0] through --workload c1: the reference's own 128 x 128 x 4 mesh; the config
+    carries the workload only (each arm's build is the line's "build"), so both arms' configs
+    compare equal."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", "c1", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["n"] == [128, 128, 4] and d["warmup"] == 3
+    assert "build" not in d["config"] and "reference" in d["build"]

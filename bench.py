@@ -233,6 +233,54 @@ def build_of(args):
         "bit-exact (identical to the reference build)"
 
 
+# ------------------------------------------------------------- extensions (MHD, CED)
+
+
+def ext_roofline(name, order, n, ms_step, bytes_per_zone, max_mhz):
+    """Roofline of an extension step from ALGORITHMIC work: FP64 flops per zone-update counted
+    on the numpy restatement as written (tools/count_flops_ext.py -> profiles/r2_ext_flops.json,
+    fitted a + b/n + c/n^2) and the compulsory HBM bytes (read + write the state once: MHD 8
+    doubles, CED 6 doubles + the conductivity read). Both are per zone-update; the binding roof
+    is the larger fraction. `traffic` is the measured DRAM traffic of a whole step
+    (tools/ext_traffic.sh -> profiles/r2_ext_traffic.json)."""
+    import torch
+    zones = n ** 3
+    with open(os.path.join(ROOT, "profiles", "r2_ext_flops.json")) as f:
+        c = json.load(f)[f"{name}_o{order}"]
+    fpz = c["a"] + c["b"] / n + c["c"] / n ** 2
+    t = ms_step * 1e-3
+    fp = fpz * zones / t / 1e12
+    fp_peak = fp64_nominal_tflops(torch.cuda.current_device(), max_mhz or 1965)
+    hbm_peak = measured_peaks().get("hbm_gbs", 6650.0)
+    hb = bytes_per_zone * zones / t / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r2_ext_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(name, {}).get("dram_bytes_per_zone")
+    fp_frac, hb_frac = fp / fp_peak, hb / hbm_peak
+    r = {"bound": "fp64" if fp_frac >= hb_frac else "hbm",
+         "achieved": fp if fp_frac >= hb_frac else hb,
+         "peak": fp_peak if fp_frac >= hb_frac else hbm_peak,
+         "unit": "TFLOP/s" if fp_frac >= hb_frac else "GB/s",
+         "frac": max(fp_frac, hb_frac),
+         "flops_per_zone": fpz, "flops_source": "profiles/r2_ext_flops.json (restatement as "
+                                                "written, tools/count_flops_ext.py)",
+         "fp64": {"achieved": fp, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp_frac,
+                  "peak_source": "nominal DFMA rate at the max SM clock"},
+         "hbm": {"achieved": hb, "peak": hbm_peak, "unit": "GB/s", "frac": hb_frac,
+                 "bytes_per_zone": bytes_per_zone,
+                 "bytes_source": "compulsory: read + write the state once per step"},
+         "traffic": traffic * zones if traffic else None,
+         "traffic_per_zone": traffic,
+         "traffic_note": ("measured DRAM bytes of a whole step per zone at 128^3 "
+                          "(profiles/r2_ext_traffic.json); vs the compulsory bytes this is the "
+                          "unfused design's re-read factor") if traffic else
+                         "no capture (tools/ext_traffic.sh)",
+         "kernel_ms_per_launch": ms_step}
+    return r
+
+
 # ---------------------------------------------------------------------- MHD (extension)
 
 
@@ -294,12 +342,7 @@ def bench_mhd(args):
     t, dt, done = st.sync()
     zones = n ** 3 * world
     value = zones * args.steps / (ms * 1e-3) / 1e6
-    # roofline: this first MHD path is unfused (predict -> 3 flux -> 3 EMF -> update), so it
-    # is HBM-bound: ideal traffic with one pass per kernel
-    bytes_per_zone = 3300.0
-    peaks = measured_peaks()
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = bytes_per_zone * n ** 3 / (ms / args.steps * 1e-3) / 1e9
+    roofline = ext_roofline("mhd", order, n, ms / args.steps, 128.0, clocks.max_mhz)
     # end to end through the public API with host buffers (H2D state, step, D2H state)
     host = torch.empty(s0.shape, dtype=torch.float64, pin_memory=True).numpy()
     host[...] = s0
@@ -342,11 +385,7 @@ def bench_mhd(args):
                    "l2": "state + modes ~50 GB > L2",
                    "parallelism": f"z-slab x{world} (NCCL halos of 8 arrays)" if world > 1
                    else "single GPU"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak,
-                     "traffic": None, "bytes_per_zone": bytes_per_zone,
-                     "note": "whole step (11 kernels) against the ideal one-pass traffic of "
-                             "the unfused design"},
+        "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": zones / e2e_s / 1e6, "unit": UNIT,  # (all ranks' zones)
                 "h2d_bytes_per_step": host.nbytes, "d2h_bytes_per_step": host.nbytes,
@@ -401,10 +440,7 @@ def bench_ced(args):
     t, _, done = st.sync()
     zones = n ** 3
     divb, divd = st.max_div()
-    bytes_per_zone = 2070.0  # ideal one-pass traffic of the unfused O3 design
-    peaks = measured_peaks()
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = bytes_per_zone * zones / (ms / args.steps * 1e-3) / 1e9
+    roofline = ext_roofline("ced", order, n, ms / args.steps, 104.0, clocks.max_mhz)
     line = {
         "metric": METRIC, "value": zones * args.steps / (ms * 1e-3) / 1e6, "unit": UNIT,
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -415,10 +451,7 @@ def bench_ced(args):
                                "step (configs[3]; extension, no reference counterpart)",
                    "n": n, "order": order, "build": "bit-exact (--fmad=false)",
                    "parallelism": "single GPU"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
-                     "bytes_per_zone": bytes_per_zone,
-                     "note": "whole step (8 kernels) against the ideal one-pass traffic"},
+        "roofline": roofline,
         "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks.summary(),
         "final": {"t": t, "steps_done": done, "max_divb": divb, "max_divd": divd},
     }

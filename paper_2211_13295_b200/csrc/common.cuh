@@ -51,6 +51,15 @@ __device__ __forceinline__ void atomic_min_pos(double* addr, double v) {
               static_cast<unsigned long long>(__double_as_longlong(v)));
 }
 
+// the same, skipping the atomic when the accumulator already holds a value <= v (a plain
+// L2 read; a stale read only costs an unneeded atomic): for kernels with many small blocks,
+// whose atomics on one address would otherwise serialise
+__device__ __forceinline__ void atomic_min_pos_sparse(double* addr, double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (b < __ldcg(reinterpret_cast<const unsigned long long*>(addr)))
+        atomicMin(reinterpret_cast<unsigned long long*>(addr), b);
+}
+
 __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = smin(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -54,13 +54,22 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
                  "r"(bytes)
                  : "memory");
 }
+// (a wait that never completes -- e.g. a copy whose byte count disagrees with expect_tx --
+// traps after ~2^22 suspended tries instead of hanging the device)
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
         "{\n"
-        ".reg .pred P1;\n"
+        ".reg .pred P1, P2;\n"
+        ".reg .u32 n;\n"
+        "mov.u32 n, 0;\n"
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
+        "@P1 bra DONE_%=;\n"
+        "add.u32 n, n, 1;\n"
+        "setp.gt.u32 P2, n, 4194304;\n"
+        "@P2 trap;\n"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
@@ -83,6 +92,8 @@ __device__ __forceinline__ void cp_async_wait_all() {
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
+
+__device__ unsigned g_sm_ctr[256];
 
 template <bool O3, int TX, int TY>
 struct FusedShape {
@@ -379,6 +390,21 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                 eidx = l < TPW ? w * TPW + l
                                : (l < TPW + RPW ? TX * TY + w * RPW + (l - TPW) : S::NE + w);
             }
+        }
+    }
+    if (a.desync_ns | a.swap_mode) {
+        // co-resident CTAs alternate (per-SM arrival counter): a start offset and/or the ring
+        // warps on the other SMSP pair, so the two CTAs' light phases do not coincide
+        __shared__ int s_par;
+        if (tid == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            s_par = int(atomicAdd(&g_sm_ctr[smid & 255u], 1u) & 1u);
+        }
+        __syncthreads();
+        if (s_par) {
+            if (a.swap_mode && tid >= 128) eidx ^= 64;
+            if (a.desync_ns) __nanosleep(unsigned(a.desync_ns));
         }
     }
     double* part = red + 32 + eidx;         // [NV] stride TX*TY (owned threads only)

@@ -9,6 +9,9 @@
 #include <cstdlib>
 
 #include "fused_persist.cuh"
+#if HC_REASSOC
+#include "fused_seam.cuh"
+#endif
 
 namespace hc {
 namespace HC_FUSED_NS {
@@ -37,6 +40,16 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
         const char* v = std::getenv("HC_INTERLEAVE");
         return v ? std::atoi(v) : 0;
     }();
+    static const int desync = [] {
+        const char* v = std::getenv("HC_DESYNC");
+        return v ? std::atoi(v) : 0;
+    }();
+    static const int swap = [] {
+        const char* v = std::getenv("HC_SWAP");
+        return v ? std::atoi(v) : 0;
+    }();
+    b.desync_ns = desync;
+    b.swap_mode = (swap && S::NT == 256) ? 1 : 0;
     constexpr int NW = S::NT / 32;
     b.interleave = (inter && (TX * TY) % NW == 0 && (S::NE - TX * TY) % NW == 0) ? 1 : 0;
     dim3 grid((a.nx + TX - 1) / TX, (a.ny + TY - 1) / TY,
@@ -124,7 +137,68 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st, const 
     }
 }
 
+#if HC_REASSOC
+template <int ORD, int SOLVER, bool RK>
+static int seam_one(const FusedArgs& a, const SeamArgs& sa, cudaStream_t st, int* blocks_per_sm) {
+    using S = SeamShape<ORD>;
+    auto kern = seam_ader_kernel<ORD, SOLVER, RK>;
+    static unsigned long long configured = 0;  // per device, as launch_cfg
+    int dev = 0;
+    cudaError_t de = cudaGetDevice(&dev);
+    if (de != cudaSuccess) return cuda_fail(de, "cudaGetDevice");
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(__atomic_load_n(&configured, __ATOMIC_ACQUIRE) & bit)) {
+        cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(S::SMEM));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(seam)");
+        __atomic_fetch_or(&configured, bit, __ATOMIC_RELEASE);
+    }
+    if (blocks_per_sm) {
+        cudaError_t e =
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, kern, S::NT, S::SMEM);
+        return e == cudaSuccess ? HC_OK : cuda_fail(e, "occupancy(seam)");
+    }
+    const int nplanes = a.kz_last - a.kz_first;
+    if (nplanes <= 0) return HC_OK;
+    dim3 grid(unsigned(sa.ntx), unsigned(sa.nty), unsigned((nplanes + a.tz - 1) / a.tz));
+    kern<<<grid, S::NT, S::SMEM, st>>>(a, sa);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "seam_ader_kernel launch");
+    const unsigned nfx = unsigned(sa.ntx * sa.ny), nfy = unsigned(sa.nty * sa.nx);  // per plane
+    seam_fix_kernel<0, SOLVER, RK><<<dim3((nfx + 127) / 128, unsigned(nplanes)), 128, 0, st>>>(a, sa);
+    seam_fix_kernel<1, SOLVER, RK><<<dim3((nfy + 127) / 128, unsigned(nplanes)), 128, 0, st>>>(a, sa);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "seam_fix_kernel launch");
+}
+
+template <int ORD, bool RK>
+static int seam_solver(const FusedArgs& a, const SeamArgs& sa, int solver, cudaStream_t st,
+                       int* bps) {
+    switch (solver) {
+        case 0: return seam_one<ORD, 0, RK>(a, sa, st, bps);
+        case 1: return seam_one<ORD, 1, RK>(a, sa, st, bps);
+        case 2: return seam_one<ORD, 2, RK>(a, sa, st, bps);
+        default: return seam_one<ORD, 3, RK>(a, sa, st, bps);
+    }
+}
+#endif
+
 }  // namespace HC_FUSED_NS
+
+#if HC_REASSOC
+int launch_seam_fast(const FusedArgs& a, const SeamArgs& sa, int order, int solver, bool rk,
+                     cudaStream_t st, int* blocks_per_sm) {
+    using namespace HC_FUSED_NS;
+    if (rk) {
+        if (order == 2) return seam_solver<2, true>(a, sa, solver, st, blocks_per_sm);
+        return order == 3 ? seam_solver<3, true>(a, sa, solver, st, blocks_per_sm)
+                          : seam_solver<4, true>(a, sa, solver, st, blocks_per_sm);
+    }
+    if (order == 2) return seam_solver<2, false>(a, sa, solver, st, blocks_per_sm);
+    return order == 3 ? seam_solver<3, false>(a, sa, solver, st, blocks_per_sm)
+                      : seam_solver<4, false>(a, sa, solver, st, blocks_per_sm);
+}
+#endif
 
 int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st,
                       const PersistLaunch* pl, int* persist_blocks_per_sm) {

@@ -1,0 +1,449 @@
+// fused_seam.cuh -- the ring-free fused ADER step of the FMA build: the same update as
+// fused_ader.cuh (reconstruction -> ADER predictor -> face Riemann fluxes -> flux
+// differencing -> update -> CFL min; stepper.cpp:49-78, predictor.cpp:26-91,
+// corrector.cpp:15-125) with no redundant zone work and no waiting between CTAs.
+//
+//  * fused_ader.cuh re-runs reconstruction + predictor on a one-zone ring around each 16 x 12
+//    tile (the faces on the tile boundary need the outside zone's state: predictor.cpp:68-70's
+//    "active + one ring"), 1.29x the owned zones, ~20 % of the kernel's FP64 instructions.
+//    fused_persist.cuh removed the ring by exchanging boundary states between resident CTAs
+//    through L2 and measured 1.8x slower (waits, fences, long-scoreboard stalls).
+//  * Here every zone's face states are computed once, by its owner, and a CTA never waits on
+//    another: the faces ON a tile boundary ("seams") are left out of the fused kernel. Each
+//    tile publishes the face states of its edge zones (the -x state of column 0, the +x state
+//    of column 31, the -y / +y states of its first / last row) to a seam buffer, updates its
+//    edge zones provisionally -- their missing seam fluxes counted as zero -- and leaves their
+//    CFL estimate out. Two small kernels (seam_fix_kernel, x then y seams) solve each seam face from the
+//    two published states, adds the missing flux terms to the provisional edge zones and
+//    takes their CFL estimate. Both neighbours of a seam face solve it from the same two
+//    states with the same code, so the fluxes they apply are identical (conservation holds).
+//  * Tile = 32 columns x up to 8 rows, one warp per row: x neighbours are lanes of one warp
+//    (the -x side state and the east face flux travel by shuffles), y neighbours pass through
+//    one shared-memory array; planes arrive by TMA tensor copies (one box per plane, per-slot
+//    mbarrier), as in fused_persist.cuh.
+//
+// The provisional form U + (r_partial - cz (T - B)) followed by + cx W - cx E + cy S - cy N
+// re-associates the reference's rate (corrector.cpp:89-90), so this kernel belongs to the FMA
+// build only (tolerance-tested against the reference, like the FMA ring kernel). Periodic x
+// and y only (the zone across the mesh edge is the last tile's own edge zone); other meshes
+// and the bit-exact build run fused_ader.cuh.
+#pragma once
+
+#include "fused_persist.cuh"
+
+namespace hc {
+namespace HC_FUSED_NS {
+
+template <int ORD>
+struct SeamShape {
+    static constexpr bool O3 = ORD >= 3;
+    static constexpr int TX = SEAM_TX, TYM = SEAM_TYM;
+    static constexpr int R = O3 ? 2 : 1;
+    // planes p-R..p+R; the refill of p+R+1 (issued after the mid-plane barrier) takes the
+    // slot of p-R, which only the predict phase reads
+    static constexpr int NB = 2 * R + 1;
+    static constexpr int HX = O3 ? 3 : 2;  // x halo = storage ghosts (16-byte TMA box origin)
+    static constexpr int W = TX + 2 * HX;
+    static constexpr int H = TYM + 2 * R;
+    static constexpr int BOX = W * H * NV;
+    static constexpr int PLANE = (BOX + 15) / 16 * 16;  // 128-byte aligned slots
+    static constexpr int NT = TX * TYM;
+    static constexpr int YPF = TYM * TX * NV;  // +y states (rows 1..h-1) / south fluxes
+    // planes + YPF + one carried 5-vector per zone + 24 scalars: 109 KB at O3, two CTAs of
+    // eight warps per SM
+    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + YPF + NV * NT + 24);
+};
+
+// rows of tile row `by` when ny rows are split over nty tiles as evenly as possible
+__device__ __forceinline__ void seam_rows(int ny, int nty, int by, int& h, int& y0) {
+    const int base = ny / nty, rem = ny % nty;
+    h = base + (by < rem ? 1 : 0);
+    y0 = by * base + min(by, rem);
+}
+// inverse: the tile row of row ja, and whether ja is that tile's first or last row
+__device__ __forceinline__ bool seam_row_edge(int ny, int nty, int ja) {
+    const int base = ny / nty, rem = ny % nty, big = rem * (base + 1);
+    const int loc = ja < big ? ja % (base + 1) : (ja - big) % base;
+    const int h = ja < big ? base + 1 : base;
+    return loc == 0 || loc == h - 1;
+}
+
+// seam records, one component per row so a warp's accesses along the seam are contiguous:
+// SX [k][sx][side][q][ja] (x seam sx = the face at x = 32 sx; side 0 = the state of the zone
+// west of the face, 1 = east), SY [k][sy][side][q][ia]. Returns the q = 0 element; component
+// q is at + q * SEAM_STRIDE (the seam length).
+__device__ __forceinline__ double* seam_x(const SeamArgs& s, int k, int sx, int ja, int side) {
+    return s.sx + ((size_t(k) * s.ntx + sx) * 2 + side) * NV * s.ny + ja;
+}
+__device__ __forceinline__ double* seam_y(const SeamArgs& s, int k, int sy, int ia, int side) {
+    return s.sy + ((size_t(k) * s.nty + sy) * 2 + side) * NV * s.nx + ia;
+}
+
+// Per plane p (lp = -1 and nzc are the z-ring planes: predict and z face only):
+//  A  predict(p): face states in registers, +y states to YPF, edge-zone states to the seams
+//  B  z face at the bottom of p; finalise p-1 from its accumulator (U + rate_xy + cz B) and
+//     this top flux; the accumulator slot then parks the bottom flux of p
+//  C  x faces (lanes 1..31: the -x side state by shuffle) and the x term of the rate (the
+//     east flux by shuffle); y faces (rows 1..h-1) against YPF, south fluxes back to YPF
+//  D  the accumulator of p: (U + (x term - cy (N - S))) + cz B
+// Missing seam fluxes count as zero; seam_fix_x / seam_fix_y add them.
+template <int ORD, int SOLVER, bool RK>
+__global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
+    seam_ader_kernel(const __grid_constant__ FusedArgs a, const SeamArgs sa) {
+    using S = SeamShape<ORD>;
+    constexpr int R = S::R, NB = S::NB, W = S::W, TX = S::TX;
+    if (a.ctl->done) return;
+    __shared__ double* sbuf[3];
+    __shared__ const CUtensorMap* smap;
+    __shared__ unsigned long long mbar[NB];
+    __shared__ int s_tile[2];  // rows h, first row y0
+    if (threadIdx.x == 0) {
+        seam_rows(a.ny, sa.nty, blockIdx.y, s_tile[0], s_tile[1]);
+        const int cur = a.ctl->cur;
+        const int in = (cur + a.in_rel) % a.nbuf;
+        sbuf[0] = a.buf[in];
+        sbuf[1] = a.buf[(cur + a.out_rel) % a.nbuf];
+        sbuf[2] = a.buf[cur];
+        smap = sa.maps + in;
+    }
+    extern __shared__ __align__(128) double smem[];
+    double* planes = smem;                         // [NB][H][W][5]
+    double* YPF = planes + size_t(NB) * S::PLANE;  // [TYM][TX][5]: +y states / south fluxes
+    double* acc = YPF + S::YPF;                    // [5][NT] accumulator / parked z flux
+    double* red = acc + NV * S::NT;  // [24]: per-warp running CFL minimum [0, 8), dt & c [16, 20)
+
+    // coordinates are re-read from the special registers where used (cheap S2R) rather than
+    // held in registers across the predictor, which would spill
+    auto ci_ = [] { return int(threadIdx.x) & 31; };
+    auto cj_ = [] { return int(threadIdx.x) >> 5; };
+    auto ia_ = [] { return int(blockIdx.x) * TX + (int(threadIdx.x) & 31); };
+    auto ja_ = [&] { return s_tile[1] + (int(threadIdx.x) >> 5); };
+    const int tid = threadIdx.x;
+    const int x0 = blockIdx.x * TX;
+    const int kz0 = a.kz_first + blockIdx.z * a.tz;
+    const int nzc = min(a.tz, a.kz_last - kz0);
+    if (tid == 0) {
+        const double dt0 = a.ctl->dt;
+        red[16] = dt0 * a.idx;  // (FMA build: dt/dx as dt * (1/dx))
+        red[17] = dt0 * a.idy;
+        red[18] = dt0 * a.idz;
+        red[19] = dt0;
+    }
+    if (tid < S::TYM) red[tid] = 1.0e32;
+    const size_t plane_stride = size_t(a.my_pad) * a.pitch;
+    const int zfirst = kz0 - 1 - R;
+    constexpr unsigned PLANE_BYTES = S::BOX * sizeof(double);
+    auto load_plane = [&](int zact) {  // one TMA box per plane, issued by thread 0
+        if (tid != 0) return;
+        const int li = zact - zfirst;
+        fence_proxy_async();  // generic-proxy reads of the slot before the async writes
+        mbar_arrive_expect_tx(&mbar[li % NB], PLANE_BYTES);
+        tma_load_plane(planes + size_t(li % NB) * S::PLANE, smap, (x0 + a.gh - S::HX) * NV,
+                       s_tile[1] + a.gh - R, zact + a.gh, &mbar[li % NB]);
+    };
+    auto wait_plane = [&](int zact) {
+        const int li = zact - zfirst;
+        mbar_wait(&mbar[li % NB], unsigned(li / NB) & 1u);
+    };
+    auto P = [&](int zact) -> const double* {
+        return planes + size_t((zact - zfirst) % NB) * S::PLANE;
+    };
+    auto zoff_ = [&] { return ((cj_() + R) * W + (ci_() + S::HX)) * NV; };
+    if (tid == 0) {
+        for (int i = 0; i < NB; ++i) mbar_init(&mbar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    for (int z = kz0 - 1 - R; z <= kz0 - 1 + R; ++z) load_plane(z);
+
+    constexpr int CS = S::NT;
+    double zp_prev[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) zp_prev[q] = 0.0;
+
+    for (int lp = -1; lp <= nzc; ++lp) {
+        const int p = kz0 + lp;
+        __syncthreads();  // the previous plane's reads of YPF are done
+        for (int z = p - R; z <= p + R; ++z) wait_plane(z);
+        const bool real = lp >= 0 && lp < nzc;  // x/y faces of p exist (else a z-ring plane)
+        double st[6][NV];                       // face states incl. 0.5*tau: E, W, N, S, T, B
+        const int h = s_tile[0];
+        if (cj_() < h) {
+            // -------------------------------------------------------------- A: predict
+            {
+                const int zoff = zoff_();
+                const double* pc = P(p) + zoff;
+                const double* zm1 = P(p - 1) + zoff;
+                const double* zp1 = P(p + 1) + zoff;
+                const double* zm2 = S::O3 ? P(p - 2) + zoff : zm1;
+                const double* zp2 = S::O3 ? P(p + 2) + zoff : zp1;
+                Fault f;
+                f.clear();
+                zone_states<ORD, FM, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a, red[19], st, f);
+                if (f.redo()) {
+                    Careful c = zone_states_careful<ORD, RK>(pc, W * NV, zm2, zm1, zp1, zp2, a,
+                                                             red[19]);
+#pragma unroll
+                    for (int s = 0; s < 6; ++s)
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) st[s][q] = c.st.v[s][q];
+                    if (c.f.code) record_fault(a.eb, ST_PREDICT, c.f, ia_(), ja_(), p, 0);
+                }
+            }
+            if (real) {
+                const int ci = ci_(), cj = cj_();
+                if (cj < h - 1)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) YPF[((cj + 1) * TX + ci) * NV + q] = st[2][q];
+                // the edge zones' states at the seams (periodic: the last seam wraps to 0)
+                const int bx = blockIdx.x, by = blockIdx.y;
+                if (ci == 0) {
+                    double* r = seam_x(sa, p, bx, ja_(), 1);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) __stcg(r + q * a.ny, st[1][q]);
+                }
+                if (ci == TX - 1) {
+                    double* r = seam_x(sa, p, bx + 1 == sa.ntx ? 0 : bx + 1, ja_(), 0);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) __stcg(r + q * a.ny, st[0][q]);
+                }
+                if (cj == 0) {
+                    double* r = seam_y(sa, p, by, ia_(), 1);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) __stcg(r + q * a.nx, st[3][q]);
+                }
+                if (cj == h - 1) {
+                    double* r = seam_y(sa, p, by + 1 == sa.nty ? 0 : by + 1, ia_(), 0);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) __stcg(r + q * a.nx, st[2][q]);
+                }
+            }
+            // ---------------------------------------- B: z face, finalise plane p-1
+            if (lp >= 0) {
+                double fz[NV];
+                {
+                    Fault f2;
+                    f2.clear();
+                    face_flux<SOLVER, 2>(zp_prev, st[5], a.gamma, fz, f2);
+                    if (f2.code) record_fault(a.eb, ST_FLUX, f2, p, ia_(), ja_(), 2);
+                }
+                if (lp >= 1) {
+                    const int ci = ci_(), cj = cj_();
+                    const int ia = ia_(), ja = ja_();
+                    const size_t zi = size_t(p - 1 + a.gh) * plane_stride +
+                                      size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
+                    const double cz = red[18];
+                    double un[NV];
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        // edge zones: provisional (seam_fix_x / _y add their seam fluxes).
+                        // cz B and cz T are rounded products (no contraction): equal z fluxes
+                        // then cancel exactly, as T - B does in the reference's association, so
+                        // a z-invariant state stays z-invariant bit for bit (w = 0 stays 0)
+                        const double v = __dsub_rn(acc[q * CS + tid], __dmul_rn(cz, fz[q]));
+                        if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
+                            un[q] = a.rk_a * sbuf[2][zi + q] + a.rk_b * v;
+                        else
+                            un[q] = v;
+                    }
+                    double* dst = sbuf[1] + zi;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                    const bool edge = ci == 0 || ci == TX - 1 || cj == 0 || cj == h - 1;
+                    double dloc = 1.0e32;
+                    if ((!RK || a.want_dt) && !edge) {
+                        Fault f3;
+                        f3.clear();
+                        double d = eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
+                        if (f3.redo()) {
+                            V5 u5;
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) u5.v[q] = un[q];
+                            f3.clear();
+                            d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f3);
+                        }
+                        if (f3.code)
+                            record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f3, ia, ja, p - 1, 0);
+                        else
+                            dloc = d;
+                    }
+                    if (!RK || a.want_dt) {  // running CFL minimum per warp (exact)
+                        dloc = warp_min(dloc);
+                        if (ci == 0) red[cj] = smin(red[cj], dloc);
+                    }
+                }
+                if (real)
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) acc[q * CS + tid] = fz[q];  // parked for D
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];
+        }
+        __syncthreads();  // +y states in YPF; every thread is past its reads of plane p-R
+        if (lp <= nzc - 1) load_plane(p + R + 1);
+        if (!real) continue;
+        // ------------------------------------------------------------- C: faces
+        const int ci = ci_(), cj = cj_();
+        double xt[NV], fs[NV];
+        if (cj < h) {  // (whole warps: the shuffles need every lane)
+            double ul[NV], fw[NV];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) ul[q] = __shfl_up_sync(0xffffffffu, st[0][q], 1);
+            if (ci > 0) {  // x face at the west of this zone (lane 0's is a seam)
+                Fault f;
+                f.clear();
+                face_flux<SOLVER, 0>(ul, st[1], a.gamma, fw, f);
+                if (f.code) record_fault(a.eb, ST_FLUX, f, ia_(), ja_(), p, 0);
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) fw[q] = 0.0;
+            }
+            const double cx = red[16];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                double e = __shfl_down_sync(0xffffffffu, fw[q], 1);  // lane ci+1's west face
+                if (ci == TX - 1) e = 0.0;                           // (a seam)
+                xt[q] = -cx * (e - fw[q]);
+            }
+            if (cj > 0) {  // y face at the south of this zone (row 0's is a seam)
+                double us[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) us[q] = YPF[(cj * TX + ci) * NV + q];
+                Fault f;
+                f.clear();
+                face_flux<SOLVER, 1>(us, st[3], a.gamma, fs, f);
+                if (f.code) record_fault(a.eb, ST_FLUX, f, ja_(), ia_(), p, 1);
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) fs[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NV; ++q) YPF[(cj * TX + ci) * NV + q] = fs[q];
+        }
+        __syncthreads();  // south fluxes of every row in YPF
+        // ------------------------------------------------------ D: the accumulator of p
+        if (cj < h) {
+            const double cy = red[17], cz = red[18];
+            const double* u = P(p) + zoff_();
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                const double n = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
+                const double r = xt[q] - cy * (n - fs[q]);
+                acc[q * CS + tid] = __dadd_rn(u[q] + r, __dmul_rn(cz, acc[q * CS + tid]));
+            }
+        }
+    }
+
+    // ---- CFL minimum of the inner zones: block min -> one atomic per CTA
+    if (!RK || a.want_dt) {
+        __syncthreads();
+        if (tid < 32) {
+            double v = tid < S::TYM ? red[tid] : 1.0e32;
+            v = warp_min(v);
+            if (tid == 0) atomic_min_pos(&a.ctl->acc, v);
+        }
+    }
+}
+
+// The seam faces of planes [kz_first, kz_last), x seams first, then y seams (a corner zone
+// gets its x term, then its y term). One thread per seam face: the flux from the two
+// published states, subtracted from the zone on the low side and added to the zone on the
+// high side (times cx or cy, and b at an RK stage); the CFL estimate of every zone this pass
+// completes (seam_fix_x: edge columns outside the tile's first and last rows; seam_fix_y:
+// the first and last rows), min-reduced per block.
+template <int AXIS, int SOLVER, bool RK>
+__global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ FusedArgs a,
+                                                       const SeamArgs sa) {
+    if (a.ctl->done) return;
+    // grid (faces of one plane / 128, planes); along the seam fastest (ja for x seams, ia
+    // for y seams), then the seam index
+    const int along = AXIS == 0 ? a.ny : a.nx, nseam = AXIS == 0 ? sa.ntx : sa.nty;
+    const unsigned idx = blockIdx.x * 128u + threadIdx.x;
+    double dloc = 1.0e32;
+    if (idx < unsigned(nseam * along)) {
+        const int sidx = int(idx / unsigned(along));
+        const int l = int(idx - unsigned(sidx) * unsigned(along));
+        const int p = a.kz_first + int(blockIdx.y);
+        const int cur = a.ctl->cur;
+        double* out = a.buf[(cur + a.out_rel) % a.nbuf];
+        const double dt0 = a.ctl->dt;
+        const double c = AXIS == 0 ? dt0 * a.idx : dt0 * a.idy;
+        const double* rec = AXIS == 0 ? seam_x(sa, p, sidx, l, 0) : seam_y(sa, p, sidx, l, 0);
+        // the two zones: low side (west / south, wrapping at the mesh edge) and high side
+        int il, jl, ih, jh;
+        if (AXIS == 0) {
+            ih = sidx * SEAM_TX;
+            il = (sidx == 0 ? a.nx : ih) - 1;
+            jl = jh = l;
+        } else {
+            int h, y0;
+            seam_rows(a.ny, sa.nty, sidx, h, y0);
+            jh = y0;
+            jl = (sidx == 0 ? a.ny : y0) - 1;
+            il = ih = l;
+        }
+        auto zidx = [&](int i, int j) {
+            return (size_t(p + a.gh) * a.my_pad + size_t(j + a.gh)) * a.pitch +
+                   size_t(i + a.gh) * NV;
+        };
+        const size_t zl = zidx(il, jl), zh = zidx(ih, jh);
+        double ul[NV], ur[NV], f5[NV], vl[NV], vh[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            ul[q] = rec[q * along];             // side 0
+            ur[q] = rec[(NV + q) * along];      // side 1
+            vl[q] = out[zl + q];
+            vh[q] = out[zh + q];
+        }
+        Fault f;
+        f.clear();
+        face_flux<SOLVER, AXIS>(ul, ur, a.gamma, f5, f);
+        if (f.code) {
+            if (AXIS == 0) record_fault(a.eb, ST_FLUX, f, ih, jh, p, 0);
+            else record_fault(a.eb, ST_FLUX, f, jh, ih, p, 1);
+        }
+        const double cb = RK ? a.rk_b * c : c;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            vl[q] = vl[q] - cb * f5[q];  // its east / north face
+            vh[q] = vh[q] + cb * f5[q];  // its west / south face
+            out[zl + q] = vl[q];
+            out[zh + q] = vh[q];
+        }
+        // CFL of the zones completed here (x pass: not in a tile's first or last row)
+        if ((!RK || a.want_dt) && (AXIS == 1 || !seam_row_edge(a.ny, sa.nty, l))) {
+            double d[2];
+            const double* v[2] = {vl, vh};
+            const int zi[2] = {il, ih}, zj[2] = {jl, jh};
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+                Fault f3;
+                f3.clear();
+                d[s] = eval_tstep_inv<FM>(v[s], a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
+                if (f3.redo()) {
+                    V5 u5;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) u5.v[q] = v[s][q];
+                    f3.clear();
+                    d[s] = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f3);
+                }
+                if (f3.code) {
+                    record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f3, zi[s], zj[s], p, 0);
+                    d[s] = 1.0e32;
+                }
+            }
+            dloc = smin(d[0], d[1]);
+        }
+    }
+    if (RK && !a.want_dt) return;
+    __shared__ double red[4];
+    const int t = threadIdx.x;
+    dloc = warp_min(dloc);
+    if ((t & 31) == 0) red[t >> 5] = dloc;
+    __syncthreads();
+    if (t == 0)
+        atomic_min_pos_sparse(&a.ctl->acc, smin(smin(red[0], red[1]), smin(red[2], red[3])));
+}
+
+}  // namespace HC_FUSED_NS
+}  // namespace hc

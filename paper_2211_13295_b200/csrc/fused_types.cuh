@@ -28,6 +28,8 @@ struct FusedArgs {
     int want_dt;     // take the CFL estimate (ADER: always; RK: last stage)
     int bulk;        // plane loads by bulk copy (set by the launcher)
     int interleave;  // ring kernel: tile and ring E-columns mixed on every warp (launcher)
+    int desync_ns;   // experiment: every other CTA on an SM starts this late (launcher, env)
+    int swap_mode;   // experiment: every other CTA on an SM puts its ring warps on SMSPs 0-1
     double rk_a, rk_b;  // RK stage coefficients U' = a U0 + b (U + dt rate)
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width
@@ -95,6 +97,21 @@ struct PersistLaunch {
 // TMA box of one plane for the persistent kernel: (32 + 2 gh) zones x 5 doubles, 7 + 2R rows
 inline int px_box_w(int order) { return PX_TX + 2 * (order >= 3 ? 3 : 2); }
 inline int px_box_h(int order) { return PX_TYM + 2 * (order >= 3 ? 2 : 1); }
+
+// ---- the ring-free seam kernel (fused_seam.cuh, FMA build): 32 x <=8 tiles, tile-boundary
+// faces finished by seam_fix_kernel from the edge zones' published states
+constexpr int SEAM_TX = 32, SEAM_TYM = 8;
+struct SeamArgs {
+    const CUtensorMap* maps;  // [nbuf] in device memory: one TMA map per state buffer
+    double* sx;               // [nz][ntx][ny][2][5] states at the x seams (x = 32 sx)
+    double* sy;               // [nz][nty][nx][2][5] states at the y seams
+    int ntx, nty;             // tiles along x (nx / 32) and y (ceil(ny / 8), balanced rows)
+    int nx, ny;
+};
+// Both kernels of one seam step (or RK stage) over a.kz_first..a.kz_last; blocks_per_sm !=
+// nullptr: only report the fused kernel's resident CTAs per SM.
+int launch_seam_fast(const FusedArgs& a, const SeamArgs& s, int order, int solver, bool rk,
+                     cudaStream_t st, int* blocks_per_sm = nullptr);
 
 // pl == nullptr: the ring kernel (fused_ader.cuh); else the persistent ring-free kernel
 // (fused_persist.cuh) with these exchange buffers and tensor maps. persist_blocks_per_sm !=

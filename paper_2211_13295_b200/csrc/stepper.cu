@@ -137,6 +137,11 @@ struct hc_stepper {
     // the persistent ring-free kernel (fused_persist.cuh), when the mesh allows it
     bool persist = false;
     PersistLaunch pl{};
+    // the ring-free seam kernel pair (fused_seam.cuh; FMA build, x/y periodic, nx % 32 == 0)
+    bool seam = false;
+    SeamArgs sa{};
+    int seam_tz = 32;
+    CUtensorMap* maps = nullptr;  // device copies of the TMA maps (persist or seam)
 };
 
 namespace {
@@ -210,6 +215,8 @@ FusedArgs fused_args(const hc_stepper* s) {
 // recompute), nx a multiple of the 32-wide tile, 16-byte row pitch (TMA strides), and every
 // tile resident at once (nx/32 x nty CTAs within the occupancy). Opt-in (HC_PERSIST=1): it
 // is bit-identical to the ring kernel but measured 1.8x slower at 256^3.
+static int encode_maps(hc_stepper* s, int box_rows);
+
 static int setup_persist(hc_stepper* s) {
     const char* v = std::getenv("HC_PERSIST");
     if (!v || std::atoi(v) == 0) return HC_OK;
@@ -248,7 +255,18 @@ static int setup_persist(hc_stepper* s) {
     PersistHdr h0{};
     h0.epoch = 1;
     HC_CUDA(cudaMemcpyAsync(pa.hdr, &h0, sizeof h0, cudaMemcpyHostToDevice, s->st));
-    // one TMA tensor map per state buffer: dims (x * 5 doubles, y rows, z planes)
+    int rc2 = encode_maps(s, px_box_h(s->p.order));
+    if (rc2) return rc2;
+    pa.maps = s->maps;
+    s->persist = true;
+    return HC_OK;
+}
+
+// One TMA tensor map per state buffer, in device memory: dims (x * 5 doubles, y rows, z
+// planes), box (32 + 2 gh zones x 5, box_rows rows, 1 plane) -- the plane box of the
+// persistent (7 + 2R rows) or the seam (8 + 2R rows) kernel.
+static int encode_maps(hc_stepper* s, int box_rows) {
+    if (s->maps) return HC_OK;
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     HC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -262,7 +280,7 @@ static int setup_persist(hc_stepper* s) {
     const cuuint64_t strides[2] = {cuuint64_t(sg.pitch) * sizeof(double),
                                    cuuint64_t(sg.my_pad) * sg.pitch * sizeof(double)};
     const cuuint32_t box[3] = {cuuint32_t(px_box_w(s->p.order) * NV),
-                               cuuint32_t(px_box_h(s->p.order)), 1};
+                               cuuint32_t(box_rows), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap maps[3];
     std::memset(maps, 0, sizeof maps);
@@ -280,8 +298,42 @@ static int setup_persist(hc_stepper* s) {
     CUtensorMap* dmaps = nullptr;
     HC_CUDA(cudaMalloc(&dmaps, sizeof maps));
     HC_CUDA(cudaMemcpy(dmaps, maps, sizeof maps, cudaMemcpyHostToDevice));
-    pa.maps = dmaps;
-    s->persist = true;
+    s->maps = dmaps;
+    return HC_OK;
+}
+
+// Enables the ring-free seam kernel pair (fused_seam.cuh) for the FMA build when the mesh
+// allows it: x and y periodic (the zone across the mesh edge is the last tile's edge zone),
+// nx a multiple of 32, storage ghosts equal to the kernel's x halo and an even row pitch (TMA
+// box origins on 16-byte boundaries). HC_SEAM=0 keeps the ring kernel.
+static int setup_seam(hc_stepper* s) {
+    if (const char* v = std::getenv("HC_SEAM"))
+        if (std::atoi(v) == 0) return HC_OK;
+    const hc_geom& g = s->g;
+    if (s->o.exact || s->persist) return HC_OK;
+    if (s->o.bc[0] != HC_PERIODIC || s->o.bc[1] != HC_PERIODIC) return HC_OK;
+    if (g.nx % SEAM_TX || (s->sg.pitch & 1) || g.ghost != (s->p.order >= 3 ? 3 : 2)) return HC_OK;
+    const bool rk = s->o.integrator != 0;
+    int bps = 0, sms = 148;
+    SeamArgs& sa = s->sa;
+    sa.nx = g.nx;
+    sa.ny = g.ny;
+    sa.ntx = g.nx / SEAM_TX;
+    sa.nty = (g.ny + SEAM_TYM - 1) / SEAM_TYM;
+    int rc = launch_seam_fast(fused_args(s), sa, s->p.order, s->p.solver, rk, nullptr, &bps);
+    if (rc) return rc;
+    HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->o.device));
+    if (bps < 1) return HC_OK;
+    s->seam_tz = choose_tz(sa.ntx * sa.nty, g.nz, sms * bps);
+    if ((rc = encode_maps(s, SEAM_TYM + 2 * (s->p.order >= 3 ? 2 : 1)))) return rc;
+    sa.maps = s->maps;
+    const size_t nsx = size_t(g.nz) * sa.ntx * g.ny * 2 * NV;
+    const size_t nsy = size_t(g.nz) * sa.nty * g.nx * 2 * NV;
+    HC_CUDA(cudaMalloc(&sa.sx, nsx * sizeof(double)));
+    HC_CUDA(cudaMalloc(&sa.sy, nsy * sizeof(double)));
+    HC_CUDA(cudaMemsetAsync(sa.sx, 0, nsx * sizeof(double), s->st));
+    HC_CUDA(cudaMemsetAsync(sa.sy, 0, nsy * sizeof(double), s->st));
+    s->seam = true;
     return HC_OK;
 }
 
@@ -395,7 +447,8 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         hc_stepper_destroy(s);
         return rc;
     }
-    if ((rc = setup_persist(s)) || (rc = (cudaStreamSynchronize(s->st) == cudaSuccess
+    if ((rc = setup_persist(s)) || (rc = setup_seam(s)) ||
+        (rc = (cudaStreamSynchronize(s->st) == cudaSuccess
                                               ? HC_OK : cuda_fail(cudaGetLastError(),
                                                                   "persist setup")))) {
         hc_stepper_destroy(s);
@@ -418,7 +471,9 @@ int hc_stepper_destroy(hc_stepper* s) {
     cudaFree(s->pl.args.flag);
     cudaFree(s->pl.args.scr);
     cudaFree(s->pl.args.hdr);
-    cudaFree(const_cast<CUtensorMap*>(s->pl.args.maps));
+    cudaFree(s->sa.sx);
+    cudaFree(s->sa.sy);
+    cudaFree(s->maps);  // (the persistent kernel's maps are these)
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     if (s->graph) cudaGraphExecDestroy(s->graph);
     if (s->s_h2d) cudaStreamDestroy(s->s_h2d);
@@ -522,6 +577,24 @@ static const double kSsp3[3][2] = {{0.0, 1.0}, {0.75, 0.25}, {1.0 / 3.0, 2.0 / 3
 
 int hc_stepper_stages(hc_stepper* s) { return s->o.integrator == 0 ? 1 : s->o.integrator; }
 
+// The kernels of one step (or RK stage) over a.kz_first..a.kz_last on stream st: the seam
+// pair (main kernel + x and y seam fixes), the persistent kernel, or the ring kernel.
+static int launch_step(hc_stepper* s, FusedArgs a, bool rk, cudaStream_t st) {
+    int rc;
+    if (s->seam) {
+        a.tz = s->seam_tz;
+        if ((rc = launch_seam_fast(a, s->sa, s->p.order, s->p.solver, rk, st))) return rc;
+        s->launches += 3;
+        return HC_OK;
+    }
+    const PersistLaunch* pl = s->persist ? &s->pl : nullptr;
+    rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, st, pl)
+                    : launch_fused_fast(a, s->p.order, s->p.solver, rk, st, pl);
+    if (rc) return rc;
+    s->launches++;
+    return HC_OK;
+}
+
 // One fused launch: the ADER step, or the next Runge-Kutta stage.
 int hc_stepper_compute(hc_stepper* s) { return hc_stepper_compute_range(s, 0, s->g.nz, 1); }
 
@@ -552,11 +625,7 @@ int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last)
         a.want_dt = k == ns - 1;
     }
     if (kz_last > kz_first) {
-        const PersistLaunch* pl = s->persist ? &s->pl : nullptr;
-        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st, pl)
-                        : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st, pl);
-        if (rc) return rc;
-        s->launches++;
+        if ((rc = launch_step(s, a, rk, s->st))) return rc;
     }
     if (!last) return HC_OK;
     if (rk)
@@ -749,10 +818,7 @@ int hc_stepper_step_host(hc_stepper* s, const double* host_in, double* host_out,
         a.cfl = s->cfl;
         a.kz_first = c0;
         a.kz_last = c1;
-        rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, false, s->st)
-                        : launch_fused_fast(a, s->p.order, s->p.solver, false, s->st);
-        if (rc) return rc;
-        s->launches++;
+        if ((rc = launch_step(s, a, false, s->st))) return rc;
         HC_CUDA(cudaEventRecord(ev_comp[c], s->st));
         HC_CUDA(cudaStreamWaitEvent(s->s_d2h, ev_comp[c], 0));
         if ((rc = copy_active(s, out, host_out, g.gh + c0, g.gh + c1, false, s->s_d2h))) return rc;
@@ -790,8 +856,9 @@ int hc_stepper_sync(hc_stepper* s, double* t, double* dt, long* steps_done) {
 
 int hc_stepper_info(hc_stepper* s, int* kernel, int* ctas) {
     if (!s) return HC_INVALID;
-    if (kernel) *kernel = s->persist ? 1 : 0;
-    if (ctas) *ctas = s->persist ? s->pl.args.ntx * s->pl.args.nty : 0;
+    if (kernel) *kernel = s->persist ? 1 : (s->seam ? 2 : 0);
+    if (ctas) *ctas = s->persist ? s->pl.args.ntx * s->pl.args.nty
+                                 : (s->seam ? s->sa.ntx * s->sa.nty : 0);
     return HC_OK;
 }
 

@@ -399,10 +399,12 @@ class Stepper:
         return self.lib.hc_stepper_launches(self.h)
 
     def kernel_info(self):
-        """("persistent", ctas) for the ring-free persistent kernel, ("ring", 0) otherwise."""
+        """Which fused kernel steps this stepper: ("ring", 0), ("persistent", ctas) for the
+        opt-in persistent kernel, or ("seam", tiles) for the ring-free seam kernel pair (the
+        FMA build's default on x/y-periodic meshes with nx % 32 == 0)."""
         k, n = C.c_int(), C.c_int()
         _check(self.lib.hc_stepper_info(self.h, C.byref(k), C.byref(n)))
-        return ("persistent" if k.value else "ring"), n.value
+        return ("ring", "persistent", "seam")[k.value], n.value
 
 
 def fp64_peak(device: int = 0) -> float:

@@ -30,7 +30,8 @@ CASES = [
 
 @pytest.fixture
 def env():
-    saved = {k: os.environ.get(k) for k in ("HC_PERSIST", "HC_PERSIST_NTY")}
+    saved = {k: os.environ.get(k) for k in ("HC_PERSIST", "HC_PERSIST_NTY", "HC_SEAM")}
+    os.environ["HC_SEAM"] = "0"  # the FMA comparisons below are against the ring kernel
     os.environ["HC_PERSIST"] = "1"
     yield os.environ
     for k, v in saved.items():

@@ -81,11 +81,12 @@ __device__ __forceinline__ double* seam_y(const SeamArgs& s, int k, int sy, int 
 
 // Per plane p (lp = -1 and nzc are the z-ring planes: predict and z face only):
 //  A  predict(p): face states in registers, +y states to YPF, edge-zone states to the seams
-//  B  z face at the bottom of p; finalise p-1 from its accumulator (U + rate_xy + cz B) and
-//     this top flux; the accumulator slot then parks the bottom flux of p
-//  C  x faces (lanes 1..31: the -x side state by shuffle) and the x term of the rate (the
-//     east flux by shuffle); y faces (rows 1..h-1) against YPF, south fluxes back to YPF
-//  D  the accumulator of p: (U + (x term - cy (N - S))) + cz B
+//  B  z face at the bottom of p; finalise p-1 from its accumulator and this top flux (U_new =
+//     acc - cz T); the accumulator slot then parks the bottom flux of p for C
+//  C  x faces (lanes 1..31: the -x side state by shuffle), the accumulator of p =
+//     (U - cx (E - W)) + cz B (the east flux by shuffle); y faces (rows 1..h-1) against YPF,
+//     south fluxes back to YPF
+//  D  accumulator -= cy (N - S)
 // Missing seam fluxes count as zero; seam_fix_x / seam_fix_y add them.
 template <int ORD, int SOLVER, bool RK>
 __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
@@ -283,28 +284,35 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
         if (lp <= nzc - 1) load_plane(p + R + 1);
         if (!real) continue;
         // ------------------------------------------------------------- C: faces
+        // x face first; the x term goes straight into the accumulator, so nothing but the
+        // -y state stays live through the y face solve and nothing across the barrier
         const int ci = ci_(), cj = cj_();
-        double xt[NV], fs[NV];
         if (cj < h) {  // (whole warps: the shuffles need every lane)
-            double ul[NV], fw[NV];
+            {
+                double ul[NV], fw[NV];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) ul[q] = __shfl_up_sync(0xffffffffu, st[0][q], 1);
-            if (ci > 0) {  // x face at the west of this zone (lane 0's is a seam)
-                Fault f;
-                f.clear();
-                face_flux<SOLVER, 0>(ul, st[1], a.gamma, fw, f);
-                if (f.code) record_fault(a.eb, ST_FLUX, f, ia_(), ja_(), p, 0);
-            } else {
+                for (int q = 0; q < NV; ++q) ul[q] = __shfl_up_sync(0xffffffffu, st[0][q], 1);
+                if (ci > 0) {  // x face at the west of this zone (lane 0's is a seam)
+                    Fault f;
+                    f.clear();
+                    face_flux<SOLVER, 0>(ul, st[1], a.gamma, fw, f);
+                    if (f.code) record_fault(a.eb, ST_FLUX, f, ia_(), ja_(), p, 0);
+                } else {
 #pragma unroll
-                for (int q = 0; q < NV; ++q) fw[q] = 0.0;
+                    for (int q = 0; q < NV; ++q) fw[q] = 0.0;
+                }
+                const double cx = red[16], cz = red[18];
+                const double* u = P(p) + zoff_();
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    double e = __shfl_down_sync(0xffffffffu, fw[q], 1);  // lane ci+1's west
+                    if (ci == TX - 1) e = 0.0;                           // (a seam)
+                    const double xt = -cx * (e - fw[q]);
+                    // (cz B rounded, no contraction: see B)
+                    acc[q * CS + tid] = __dadd_rn(u[q] + xt, __dmul_rn(cz, acc[q * CS + tid]));
+                }
             }
-            const double cx = red[16];
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                double e = __shfl_down_sync(0xffffffffu, fw[q], 1);  // lane ci+1's west face
-                if (ci == TX - 1) e = 0.0;                           // (a seam)
-                xt[q] = -cx * (e - fw[q]);
-            }
+            double fs[NV];
             if (cj > 0) {  // y face at the south of this zone (row 0's is a seam)
                 double us[NV];
 #pragma unroll
@@ -321,15 +329,14 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
             for (int q = 0; q < NV; ++q) YPF[(cj * TX + ci) * NV + q] = fs[q];
         }
         __syncthreads();  // south fluxes of every row in YPF
-        // ------------------------------------------------------ D: the accumulator of p
+        // ---------------------------------------------- D: the y term of the accumulator
         if (cj < h) {
-            const double cy = red[17], cz = red[18];
-            const double* u = P(p) + zoff_();
+            const double cy = red[17];
 #pragma unroll
             for (int q = 0; q < NV; ++q) {
-                const double n = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
-                const double r = xt[q] - cy * (n - fs[q]);
-                acc[q * CS + tid] = __dadd_rn(u[q] + r, __dmul_rn(cz, acc[q * CS + tid]));
+                const double sf = YPF[(cj * TX + ci) * NV + q];
+                const double nf = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
+                acc[q * CS + tid] -= cy * (nf - sf);
             }
         }
     }

@@ -589,6 +589,12 @@ def main():
     max_mhz = clocks.max_mhz or pclk.max_mhz or 1965
     peak_fp64 = fp64_nominal_tflops(local, max_mhz)
     achieved = fpz * zones_local / (kern_ms * 1e-3) / 1e12
+    kind = dom.st.kernel_info()[0] if hasattr(dom, "st") else "ring"
+    kernel_desc = {
+        "seam": "seam_ader_kernel + seam_fix_kernel<x> + seam_fix_kernel<y>: the step's compute "
+                "launches (FMA build's ring-free pair; timed together, CUDA events around them)",
+        "persistent": "persist_ader_kernel (opt-in persistent ring-free kernel)",
+    }.get(kind, "fused_ader_kernel (ring kernel; CUDA events around the launch)")
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_achieved = BYTES_PER_ZONE * zones_local / (kern_ms * 1e-3) / 1e9
@@ -602,6 +608,7 @@ def main():
                        "source": "hc_fp64_peak: 16 DFMA chains per thread, 32 warps per SM, "
                                  "best of 10 launches, this process"},
         "flops_per_zone": fpz, "kernel_ms_per_launch": kern_ms,
+        "kernel": kernel_desc,
         "traffic": None,
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": hbm_achieved / hbm_peak, "bytes_per_zone": BYTES_PER_ZONE,

@@ -4,7 +4,7 @@
  * fluxes -> flux differencing -> conservative update + global CFL min.
  *
  * This is the drop-in boundary. The reference exposes its hot path as free C++ functions in
- * namespace hydro (proj/include/hydro/*.hpp, statically linked from libhydro.a); a
+ * namespace hydro (proj/include/hydro/ *.hpp, statically linked from libhydro.a); a
  * maintainer swaps proj/src/{fields,boundary,reconstruct,predictor,corrector,stepper}.cpp
  * for the thin C++ shim in paper_2211_13295_b200/shim/hydro_gpu_shim.cpp, which calls the
  * entry points below. Signatures carry plain pointers and sizes only.
@@ -234,6 +234,11 @@ int hc_stepper_stages(hc_stepper* s);
 long hc_stepper_launches(hc_stepper* s);
 /* Storage layout of the state buffers: rows per plane, doubles per row, planes. */
 int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz);
+/* The device state buffers (bufs[3]; unused entries NULL) and how many the integrator uses.
+ * Which one is current is decided on the device (hc_stepper_state); drivers that enqueue
+ * halo exchanges asynchronously track it as the steps flip it (ADER: every step; RK: never,
+ * stage k reads buffer (cur + k) % nbuf). */
+int hc_stepper_buffers(hc_stepper* s, double** bufs, int* nbuf);
 
 /* ------------------------------------------------ device-resident patch set
  * PatchSet (transfer.hpp:47-73) with the patches' states resident in HBM: px x py x pz
@@ -259,6 +264,52 @@ int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done);
  * uploads, downloads, scalar_uploads, scalar_downloads, uploads_active_only, steps */
 int hc_patchset_ledger(hc_patchset* ps, unsigned long long* counts6);
 long hc_patchset_launches(hc_patchset* ps);
+
+/* ------------------------------------------------ multi-GPU z-slab domain
+ * The reference's PatchSet split along z -- make_patch_set(global, 1, 1, world)
+ * (transfer.hpp:60-61, transfer.cpp:17-47) -- with every patch (slab) on its own GPU, and
+ * run_patch_step (transfer.hpp:73, transfer.cpp:152-216) as: x/y ghosts on each device; the
+ * z sweep of exchange_ghosts (transfer.cpp:131-149) as whole-plane halo messages straight
+ * into the neighbours' ghost planes (ncclSend/ncclRecv in one group, or peer copies for the
+ * slabs of one process); the fused step (every RK stage gets its own exchange,
+ * transfer.cpp:197-201); the global dt min (transfer.cpp:184) as an 8-byte ncclAllReduce(MIN)
+ * on the device; the t/dt hand-off on the device. No host round trip per step. Bit-identical
+ * to the single domain. NCCL is opened at run time (libnccl.so.2). */
+typedef struct hc_domain hc_domain;
+
+typedef enum { HC_XCHG_NCCL = 0, HC_XCHG_PEER = 1 } hc_exchange_kind;
+
+typedef struct {
+    int bc[3];       /* per axis HC_PERIODIC / HC_OUTFLOW (z: the global ends) */
+    int exact;       /* as hc_stepper_opts */
+    int integrator;  /* as hc_stepper_opts */
+    int device;      /* hc_domain_create: this rank's GPU */
+    int transport;   /* hc_exchange_kind; HC_XCHG_PEER only with hc_domain_create_local */
+} hc_domain_opts;
+
+/* An NCCL unique id for hc_domain_create (rank 0 makes it and shares it out of band);
+ * len >= 128 (NCCL_UNIQUE_ID_BYTES). */
+int hc_nccl_unique_id(unsigned char* id, size_t len);
+/* One process per GPU: this process owns slab `rank` of `world` (global.nz % world == 0). */
+int hc_domain_create(const hc_geom* global, const hc_params* p, const hc_domain_opts* o,
+                     int rank, int world, const unsigned char* nccl_id, hc_domain** out);
+/* One process driving `ngpu` GPUs (devices[ngpu]; ncclCommInitAll or peer copies). ngpu = 1
+ * with periodic z exchanges the slab's halos with itself through the same calls. */
+int hc_domain_create_local(const hc_geom* global, const hc_params* p, const hc_domain_opts* o,
+                           int ngpu, const int* devices, hc_domain** out);
+int hc_domain_destroy(hc_domain* d);
+/* scatter_to_patches / gather_from_patches (transfer.cpp:50-76) for the slabs this process
+ * drives: a global HOST SkinnyState [mz][my][mx][5]; only the slabs' active planes move. */
+int hc_domain_scatter(hc_domain* d, const double* global_skinny);
+int hc_domain_gather(hc_domain* d, double* global_skinny);
+int hc_domain_set_time(hc_domain* d, double t, double dt, double cfl, double t_final);
+/* run_patch_step x n, enqueued without host synchronisation */
+int hc_domain_step(hc_domain* d, int n);
+int hc_domain_sync(hc_domain* d, double* t, double* dt, long* steps_done);
+/* planes per slab, first global plane of this process's first slab, slabs in this process,
+ * which fused kernel steps them (hc_stepper_info) */
+int hc_domain_info(hc_domain* d, int* nz_local, int* z0, int* nslabs, int* kernel);
+long hc_domain_launches(hc_domain* d);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ SOURCES = {
     "peak.cu": ["--fmad=true"],
     "mhd.cu": ["--fmad=false"],
     "ced.cu": ["--fmad=false"],
+    "domain.cu": ["--fmad=false"],
 }
 
 
@@ -93,7 +94,7 @@ def build(verbose=True) -> str:
         return LIB
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-o", tmp] + ARCH + ["-ccbin", "/usr/bin/g++", "-Xcompiler",
-                                                 "-fopenmp"] + objs
+                                                 "-fopenmp"] + objs + ["-ldl"]
     subprocess.run(cmd, check=True)
     shutil.move(tmp, LIB)
     with open(stamp, "w") as f:

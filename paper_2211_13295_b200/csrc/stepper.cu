@@ -871,6 +871,14 @@ int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {
     return HC_OK;
 }
 
+int hc_stepper_buffers(hc_stepper* s, double** bufs, int* nbuf) {
+    if (!s) return HC_INVALID;
+    if (bufs)
+        for (int i = 0; i < 3; ++i) bufs[i] = s->buf[i];
+    if (nbuf) *nbuf = s->nbuf;
+    return HC_OK;
+}
+
 int hc_stepper_dt_ptrs(hc_stepper* s, double** dt_next_dev, double** dt_dev) {
     if (dt_next_dev) *dt_next_dev = &s->ctl->acc;
     if (dt_dev) *dt_dev = &s->ctl->dt;

@@ -160,6 +160,13 @@ def load_library(path: str = LIB_PATH):
     lib.hc_last_error.argtypes = [C.c_char_p, C.c_size_t]
     lib.hc_stepper_launches.restype = C.c_long
     lib.hc_stepper_launches.argtypes = [C.c_void_p]
+    lib.hc_domain_launches.restype = C.c_long
+    for name in ("hc_domain_launches", "hc_domain_destroy", "hc_domain_info",
+                 "hc_domain_scatter", "hc_domain_gather", "hc_domain_sync"):
+        getattr(lib, name).argtypes = None
+    lib.hc_domain_launches.argtypes = [C.c_void_p]
+    lib.hc_domain_destroy.argtypes = [C.c_void_p]
+    lib.hc_domain_step.argtypes = [C.c_void_p, C.c_int]
     for name in ("hc_stepper_destroy", "hc_stepper_step", "hc_stepper_fill_ghosts",
                  "hc_stepper_compute", "hc_stepper_advance", "hc_stepper_stages"):
         getattr(lib, name).argtypes = [C.c_void_p] + ([C.c_int] if name.endswith("_step")
@@ -405,6 +412,95 @@ class Stepper:
         k, n = C.c_int(), C.c_int()
         _check(self.lib.hc_stepper_info(self.h, C.byref(k), C.byref(n)))
         return ("ring", "persistent", "seam")[k.value], n.value
+
+
+class DomainOpts(C.Structure):
+    """hc_domain_opts (include/hydro_cuda.h)."""
+    _fields_ = [("bc", C.c_int * 3), ("exact", C.c_int), ("integrator", C.c_int),
+                ("device", C.c_int), ("transport", C.c_int)]
+
+
+XCHG_NCCL, XCHG_PEER = 0, 1  # hc_exchange_kind
+
+
+def nccl_unique_id() -> bytes:
+    """hc_nccl_unique_id: 128 bytes for Domain(..., rank, world, nccl_id) on every rank."""
+    buf = (C.c_ubyte * 128)()
+    _check(load_library().hc_nccl_unique_id(buf, C.c_size_t(128)))
+    return bytes(buf)
+
+
+class Domain:
+    """The multi-GPU z-slab domain of the C ABI (hc_domain_*, csrc/domain.cu): the reference's
+    PatchSet split along z (transfer.cpp:17-47) with one slab per GPU, run_patch_step
+    (transfer.cpp:152-216) as device x/y ghosts + whole-plane z halos (NCCL send/recv straight
+    into the ghost planes, or peer copies) + the fused step + an 8-byte all-reduce(MIN) of
+    dt_next, enqueued without host round trips.
+
+    devices: one process driving these GPUs (hc_domain_create_local); or rank / world /
+    nccl_id: one process per GPU (hc_domain_create, this rank's slab on ``device``)."""
+
+    def __init__(self, geom: Geom, params: Params, bc=(PERIODIC, PERIODIC, PERIODIC),
+                 exact=True, integrator=ADER, transport=XCHG_NCCL, devices=(0,), rank=None,
+                 world=None, nccl_id=None, device=0):
+        self.lib = load_library()
+        self.geom, self.params = geom, params
+        o = DomainOpts()
+        for a in range(3):
+            o.bc[a] = bc[a]
+        o.exact, o.integrator, o.device, o.transport = int(bool(exact)), integrator, device, \
+            transport
+        h = C.c_void_p()
+        if rank is None:
+            devs = (C.c_int * len(devices))(*devices)
+            _check(self.lib.hc_domain_create_local(C.byref(geom), C.byref(params), C.byref(o),
+                                                   len(devices), devs, C.byref(h)))
+        else:
+            idb = (C.c_ubyte * 128).from_buffer_copy(nccl_id) if nccl_id else None
+            _check(self.lib.hc_domain_create(C.byref(geom), C.byref(params), C.byref(o), rank,
+                                             world, idb, C.byref(h)))
+        self.h = h
+        nz, z0, ns, k = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(self.lib.hc_domain_info(self.h, C.byref(nz), C.byref(z0), C.byref(ns),
+                                       C.byref(k)))
+        self.nz_local, self.z0, self.nslabs = nz.value, z0.value, ns.value
+        self.kernel = ("ring", "persistent", "seam")[k.value]
+
+    def scatter(self, skinny: np.ndarray):
+        a = np.ascontiguousarray(skinny, dtype=np.float64)
+        _check(self.lib.hc_domain_scatter(self.h, a.ctypes.data_as(C.c_void_p)))
+
+    def gather(self, out: np.ndarray):
+        assert out.flags.c_contiguous and out.dtype == np.float64
+        _check(self.lib.hc_domain_gather(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def set_time(self, t, dt, cfl, t_final=0.0):
+        _check(self.lib.hc_domain_set_time(self.h, C.c_double(t), C.c_double(dt),
+                                           C.c_double(cfl), C.c_double(t_final)))
+
+    def step(self, n=1):
+        _check(self.lib.hc_domain_step(self.h, int(n)))
+
+    def sync(self):
+        t, dt, n = C.c_double(), C.c_double(), C.c_long()
+        _check(self.lib.hc_domain_sync(self.h, C.byref(t), C.byref(dt), C.byref(n)))
+        return t.value, dt.value, n.value
+
+    @property
+    def launches(self):
+        return self.lib.hc_domain_launches(self.h)
+
+    def close(self):
+        if self.h:
+            self.lib.hc_domain_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def fp64_peak(device: int = 0) -> float:

@@ -257,6 +257,10 @@ int hc_patchset_destroy(hc_patchset* ps);
  * SkinnyState [mz][my][mx][5] (active zones only) and the patches' device states */
 int hc_patchset_scatter(hc_patchset* ps, const double* global_skinny);
 int hc_patchset_gather(hc_patchset* ps, double* global_skinny);
+/* One patch's whole HOST SkinnyState [mz][my][mx][5] (its own ghosts included) to (upload = 1)
+ * or from (0) its device state: the per-patch residency moves of the C++ drop-in driver
+ * (shim/hydro_gpu_transfer.cpp), which keeps the reference's host Patch structures. */
+int hc_patchset_patch_io(hc_patchset* ps, int idx, double* host_skinny, int upload);
 int hc_patchset_set_time(hc_patchset* ps, double t, double dt, double cfl, double t_final);
 int hc_patchset_step(hc_patchset* ps, int n);
 int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done);

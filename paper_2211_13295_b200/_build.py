@@ -124,13 +124,24 @@ def build_shim(verbose=True):
     tests = sorted(os.path.join(REF, "tests", f) for f in os.listdir(os.path.join(REF, "tests"))
                    if f.endswith(".cpp") and f != "acceptance_main.cpp")
     inc = ["-I" + os.path.join(REF, "include"), "-I" + os.path.join(ROOT, "include"),
-           "-I" + os.path.join(ROOT, "oracle", "doctest_shim"), "-I" + os.path.join(REF, "tests")]
+           "-I" + os.path.join(ROOT, "oracle", "doctest_shim"), "-I" + os.path.join(REF, "tests"),
+           "-I" + os.path.join(PKG, "shim")]
     link = ["-L" + PKG, "-l:libhydro_cuda.so", "-Wl,-rpath,$ORIGIN/../../paper_2211_13295_b200"]
+    # the device-resident PatchSet driver replaces transfer.cpp too (hydro_gpu_transfer.cpp)
+    xfer = os.path.join(PKG, "shim", "hydro_gpu_transfer.cpp")
+    kept_res = [k for k in kept if not k.endswith("transfer.cpp")]
+    accept = os.path.join(REF, "tests", "acceptance_main.cpp")
     targets = {
         "unit_tests_gpu": tests + kept + [shim],
-        "acceptance_gpu": [os.path.join(REF, "tests", "acceptance_main.cpp")] + kept + [shim],
+        "acceptance_gpu": [accept] + kept + [shim],
+        "unit_tests_gpu_resident": tests + kept_res + [shim, xfer],
+        "acceptance_gpu_resident": [accept] + kept_res + [shim, xfer],
+        "run_benchmark_gpu": [os.path.join(PKG, "shim", "run_benchmark_gpu.cpp")] +
+                             [k for k in kept_res if not k.endswith("serial_ref.cpp")] +
+                             [shim, xfer],
     }
-    deps = [shim, LIB]
+    deps = [shim, xfer, os.path.join(PKG, "shim", "shim_resident.hpp"),
+            os.path.join(PKG, "shim", "run_benchmark_gpu.cpp"), LIB]
     for name, srcs in targets.items():
         exe = os.path.join(out_dir, name)
         if os.path.exists(exe) and os.path.getmtime(exe) >= max(os.path.getmtime(d) for d in deps):

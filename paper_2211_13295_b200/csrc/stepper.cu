@@ -1054,7 +1054,11 @@ int hc_patchset_create(const hc_geom* global, int px, int py, int pz, const hc_p
                 g.origin[0] = global->origin[0] + pi * lnx * global->dx;
                 g.origin[1] = global->origin[1] + pj * lny * global->dy;
                 g.origin[2] = global->origin[2] + pk * lnz * global->dz;
-                hc_stepper_opts o = {{-1, -1, -1}, exact, device, integrator};
+                // a single patch owns its boundaries (its ghost fill is exchange_ghosts for
+                // one patch, and the FMA build can take the ring-free seam kernel); several
+                // patches have every ghost filled by the exchange gather
+                const int b = px * py * pz == 1 ? boundary : -1;
+                hc_stepper_opts o = {{b, b, b}, exact, device, integrator};
                 hc_stepper* s = nullptr;
                 rc = hc_stepper_create(&g, p, &o, &s);
                 if (!rc) {
@@ -1136,6 +1140,16 @@ int hc_patchset_gather(hc_patchset* ps, double* global_skinny) {
     return ps_copy(ps, global_skinny, false);
 }
 
+int hc_patchset_patch_io(hc_patchset* ps, int idx, double* host_skinny, int upload) {
+    if (!ps || idx < 0 || idx >= int(ps->patches.size()) || !host_skinny) {
+        set_error(HC_INVALID, "hc_patchset_patch_io: bad patch index or buffer");
+        return HC_INVALID;
+    }
+    HC_CUDA(cudaSetDevice(ps->device));
+    return upload ? hc_stepper_upload(ps->patches[size_t(idx)], host_skinny)
+                  : hc_stepper_download(ps->patches[size_t(idx)], host_skinny);
+}
+
 int hc_patchset_set_time(hc_patchset* ps, double t, double dt, double cfl, double t_final) {
     for (hc_stepper* s : ps->patches) {
         int rc = hc_stepper_set_time(s, t, dt, cfl, t_final);
@@ -1153,7 +1167,8 @@ int hc_patchset_step(hc_patchset* ps, int n) {
     const int np = int(ps->patches.size());
     for (int it = 0; it < n; ++it) {
         for (int k = 0; k < ns; ++k) {
-            int rc = ps_exchange(ps, ps->integrator == 0 ? 0 : k);
+            int rc = np == 1 ? hc_stepper_fill_ghosts(ps->patches[0])
+                             : ps_exchange(ps, ps->integrator == 0 ? 0 : k);
             for (int p = 0; p < np && !rc; ++p) rc = hc_stepper_compute(ps->patches[p]);
             if (rc) return rc;
         }

@@ -21,6 +21,7 @@
 #include "hydro/reconstruct.hpp"
 #include "hydro/stepper.hpp"
 #include "hydro_cuda.h"
+#include "shim_resident.hpp"
 
 namespace hydro {
 
@@ -118,6 +119,10 @@ class CallTimer {
 
 }  // namespace
 
+// residency hook (shim_resident.hpp): no-op unless hydro_gpu_transfer.cpp is linked
+__attribute__((weak)) void shim_host_touch(const void*) {}
+#define TOUCH(x) shim_host_touch((x).v.data())
+
 // ------------------------------------------------------------------ fields.hpp:137-145
 
 void require_compatible(const SkinnyState& s, const ModalState& m) {
@@ -126,12 +131,16 @@ void require_compatible(const SkinnyState& s, const ModalState& m) {
 }
 
 void skinny_to_modal(const SkinnyState& skinny, ModalState& modal) {
+    TOUCH(skinny);
+    TOUCH(modal);
     require_compatible(skinny, modal);
     hc_geom g = shape_geom(modal.mx, modal.my, modal.mz);
     check(hc_skinny_to_modal(&g, modal.modes, skinny.v.data(), modal.v.data()));
 }
 
 void modal_to_skinny(const ModalState& modal, const PatchGeometry& g, SkinnyState& skinny) {
+    TOUCH(modal);
+    TOUCH(skinny);
     require_compatible(skinny, modal);
     hc_geom h = to_hc(g);
     check(hc_modal_to_skinny(&h, modal.modes, modal.v.data(), skinny.v.data()));
@@ -140,11 +149,13 @@ void modal_to_skinny(const ModalState& modal, const PatchGeometry& g, SkinnyStat
 // ---------------------------------------------------------------- boundary.hpp:10-15
 
 void apply_boundary(SkinnyState& skinny, const PatchGeometry& g, BoundaryKind k) {
+    TOUCH(skinny);
     hc_geom h = to_hc(g);
     check(hc_apply_boundary_skinny(&h, kind(k), skinny.v.data()));
 }
 
 void apply_boundary(ModalState& modal, const PatchGeometry& g, BoundaryKind k) {
+    TOUCH(modal);
     hc_geom h = to_hc(g);
     check(hc_apply_boundary_modal(&h, modal.modes, kind(k), modal.v.data()));
 }
@@ -152,12 +163,14 @@ void apply_boundary(ModalState& modal, const PatchGeometry& g, BoundaryKind k) {
 // ------------------------------------------------------------- reconstruct.hpp:85-97
 
 void limit_patch_o2(ModalState& modal, const PatchGeometry& g, const LimiterConfig& cfg) {
+    TOUCH(modal);
     hc_geom h = to_hc(g);
     hc_limiter l = to_hc(cfg);
     check(hc_limit_patch_o2(&h, modal.v.data(), &l));
 }
 
 void reconstruct_patch_o3(ModalState& modal, const PatchGeometry& g, const LimiterConfig& cfg) {
+    TOUCH(modal);
     hc_geom h = to_hc(g);
     hc_limiter l = to_hc(cfg);
     check(hc_reconstruct_patch_o3(&h, modal.v.data(), &l));
@@ -180,11 +193,13 @@ void predictor_ptwise(ZoneModal& zone, double dt, double dx, double dy, double d
 
 void predict_patch(ModalState& modal, const TimeState& time, const PatchGeometry& g,
                    const GasModel& gas) {
+    TOUCH(modal);
     hc_geom h = to_hc(g);
     check(hc_predict_patch(&h, modal.modes, modal.v.data(), time.dt, gas.gamma));
 }
 
 void zero_temporal_mode(ModalState& modal) {
+    TOUCH(modal);
     hc_geom g = shape_geom(modal.mx, modal.my, modal.mz);
     check(hc_zero_temporal_mode(&g, modal.modes, modal.v.data()));
 }
@@ -193,6 +208,8 @@ void zero_temporal_mode(ModalState& modal) {
 
 void make_flux_axis(const ModalState& modal, Axis axis, const PatchGeometry& g,
                     const GasModel& gas, SolverChoice solver, FaceFlux& out) {
+    TOUCH(modal);
+    TOUCH(out);
     hc_geom h = to_hc(g);
     int rc = hc_make_flux_axis(&h, modal.modes, modal.v.data(), int(axis), gas.gamma,
                                solver == SolverChoice::rusanov ? HC_RUSANOV : HC_HLL,
@@ -204,6 +221,8 @@ void make_flux_axis(const ModalState& modal, Axis axis, const PatchGeometry& g,
 
 void make_du_dt(const FluxSet& fluxes, const TimeState& time, const PatchGeometry& g,
                 RateField& rate) {
+    TOUCH(fluxes.fx);
+    TOUCH(rate);
     hc_geom h = to_hc(g);
     check(hc_make_du_dt(&h, fluxes.fx.v.data(), fluxes.fy.v.data(), fluxes.fz.v.data(),
                         time.dt, rate.v.data()));
@@ -211,6 +230,9 @@ void make_du_dt(const FluxSet& fluxes, const TimeState& time, const PatchGeometr
 
 void update_u_timestep(ModalState& modal, SkinnyState& skinny, const RateField& rate,
                        TimeState& time, const PatchGeometry& g, const GasModel& gas) {
+    TOUCH(modal);
+    TOUCH(skinny);
+    TOUCH(rate);
     hc_geom h = to_hc(g);
     double dtn = 0.0;
     check(hc_update_u_timestep(&h, modal.modes, modal.v.data(), skinny.v.data(), rate.v.data(),
@@ -222,6 +244,7 @@ void update_u_timestep(ModalState& modal, SkinnyState& skinny, const RateField& 
 
 double compute_dt_next(const ModalState& modal, const PatchGeometry& g, const GasModel& gas,
                        double cfl) {
+    TOUCH(modal);
     hc_geom h = to_hc(g);
     double dtn = 0.0;
     check(hc_compute_dt_next(&h, modal.modes, modal.v.data(), gas.gamma, cfl, &dtn));
@@ -230,6 +253,9 @@ double compute_dt_next(const ModalState& modal, const PatchGeometry& g, const Ga
 
 void ader_step(ModalState& modal, SkinnyState& skinny, TimeState& time, const PatchGeometry& g,
                const StepParams& par, StepScratch& scratch, StageProfile* prof) {
+    TOUCH(modal);
+    TOUCH(skinny);
+    TOUCH(scratch.rate);
     hc_geom h = to_hc(g);
     hc_params p = to_hc(par);
     double dtn = 0.0, stage[6] = {0, 0, 0, 0, 0, 0};
@@ -257,12 +283,17 @@ const std::vector<RkStage>& rk_stages(IntegratorChoice k) {
 }
 
 void rk_save_u0(const SkinnyState& skinny, const PatchGeometry& g, StepScratch& scratch) {
+    TOUCH(skinny);
+    TOUCH(scratch.stage_u0);
     hc_geom h = to_hc(g);
     check(hc_rk_save_u0(&h, skinny.v.data(), scratch.stage_u0.v.data()));
 }
 
 void rk_stage(ModalState& modal, SkinnyState& skinny, TimeState& time, const PatchGeometry& g,
               const StepParams& par, StepScratch& scratch, RkStage stage, StageProfile* prof) {
+    TOUCH(modal);
+    TOUCH(skinny);
+    TOUCH(scratch.stage_u0);
     hc_geom h = to_hc(g);
     hc_params p = to_hc(par);
     double s[6] = {0, 0, 0, 0, 0, 0};

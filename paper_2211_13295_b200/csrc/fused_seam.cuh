@@ -51,7 +51,8 @@ struct SeamShape {
     static constexpr int YPF = TYM * TX * NV;  // +y states (rows 1..h-1) / south fluxes
     // planes + YPF + one carried 5-vector per zone + 24 scalars: 109 KB at O3, two CTAs of
     // eight warps per SM
-    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + YPF + NV * NT + 24);
+    static constexpr size_t SMEM = sizeof(double) * (size_t(NB) * PLANE + YPF + NV * NT + 24 + TYM);
+    static constexpr int MINB = NT <= 256 ? 2 : 1;  // CTAs per SM the 128 registers allow
 };
 
 // rows of tile row `by` when ny rows are split over nty tiles as evenly as possible
@@ -89,7 +90,7 @@ __device__ __forceinline__ double* seam_y(const SeamArgs& s, int k, int sy, int 
 //  D  accumulator -= cy (N - S)
 // Missing seam fluxes count as zero; seam_fix_x / seam_fix_y add them.
 template <int ORD, int SOLVER, bool RK>
-__global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
+__global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     seam_ader_kernel(const __grid_constant__ FusedArgs a, const SeamArgs sa) {
     using S = SeamShape<ORD>;
     constexpr int R = S::R, NB = S::NB, W = S::W, TX = S::TX;
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
     double* planes = smem;                         // [NB][H][W][5]
     double* YPF = planes + size_t(NB) * S::PLANE;  // [TYM][TX][5]: +y states / south fluxes
     double* acc = YPF + S::YPF;                    // [5][NT] accumulator / parked z flux
-    double* red = acc + NV * S::NT;  // [24]: per-warp running CFL minimum [0, 8), dt & c [16, 20)
+    double* red = acc + NV * S::NT;  // [24 + TYM]: dt & c at [16, 20), per-warp CFL minimum at [24, 24 + TYM)
 
     // coordinates are re-read from the special registers where used (cheap S2R) rather than
     // held in registers across the predictor, which would spill
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
         red[18] = dt0 * a.idz;
         red[19] = dt0;
     }
-    if (tid < S::TYM) red[tid] = 1.0e32;
+    if (tid < S::TYM) red[24 + tid] = 1.0e32;
     const size_t plane_stride = size_t(a.my_pad) * a.pitch;
     const int zfirst = kz0 - 1 - R;
     constexpr unsigned PLANE_BYTES = S::BOX * sizeof(double);
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
                     }
                     if (!RK || a.want_dt) {  // running CFL minimum per warp (exact)
                         dloc = warp_min(dloc);
-                        if (ci == 0) red[cj] = smin(red[cj], dloc);
+                        if (ci == 0) red[24 + cj] = smin(red[24 + cj], dloc);
                     }
                 }
                 if (real)
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, 2)
     if (!RK || a.want_dt) {
         __syncthreads();
         if (tid < 32) {
-            double v = tid < S::TYM ? red[tid] : 1.0e32;
+            double v = tid < S::TYM ? red[24 + tid] : 1.0e32;
             v = warp_min(v);
             if (tid == 0) atomic_min_pos(&a.ctl->acc, v);
         }

@@ -164,9 +164,10 @@ static int seam_one(const FusedArgs& a, const SeamArgs& sa, cudaStream_t st, int
     kern<<<grid, S::NT, S::SMEM, st>>>(a, sa);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "seam_ader_kernel launch");
-    const unsigned nfx = unsigned(sa.ntx * sa.ny), nfy = unsigned(sa.nty * sa.nx);  // per plane
-    seam_fix_kernel<0, SOLVER, RK><<<dim3((nfx + 127) / 128, unsigned(nplanes)), 128, 0, st>>>(a, sa);
-    seam_fix_kernel<1, SOLVER, RK><<<dim3((nfy + 127) / 128, unsigned(nplanes)), 128, 0, st>>>(a, sa);
+    // per plane: y-seam faces, x-seam faces, tile-corner zones (one launch, disjoint zones)
+    const unsigned nby = unsigned(sa.nty * sa.nx + 127) / 128, nbx = unsigned(sa.ntx * sa.ny + 127) / 128,
+                   nbc = unsigned(4 * sa.ntx * sa.nty + 127) / 128;
+    seam_fix_kernel<SOLVER, RK><<<dim3(nby + nbx + nbc, unsigned(nplanes)), 128, 0, st>>>(a, sa);
     e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "seam_fix_kernel launch");
 }

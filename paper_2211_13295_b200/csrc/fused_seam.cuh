@@ -13,7 +13,7 @@
 //    tile publishes the face states of its edge zones (the -x state of column 0, the +x state
 //    of column 31, the -y / +y states of its first / last row) to a seam buffer, updates its
 //    edge zones provisionally -- their missing seam fluxes counted as zero -- and leaves their
-//    CFL estimate out. Two small kernels (seam_fix_kernel, x then y seams) solve each seam face from the
+//    CFL estimate out. A second, small kernel (seam_fix_kernel) solves each seam face from the
 //    two published states, adds the missing flux terms to the provisional edge zones and
 //    takes their CFL estimate. Both neighbours of a seam face solve it from the same two
 //    states with the same code, so the fluxes they apply are identical (conservation holds).
@@ -353,95 +353,135 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     }
 }
 
-// The seam faces of planes [kz_first, kz_last), x seams first, then y seams (a corner zone
-// gets its x term, then its y term). One thread per seam face: the flux from the two
-// published states, subtracted from the zone on the low side and added to the zone on the
-// high side (times cx or cy, and b at an RK stage); the CFL estimate of every zone this pass
-// completes (seam_fix_x: edge columns outside the tile's first and last rows; seam_fix_y:
-// the first and last rows), min-reduced per block.
-template <int AXIS, int SOLVER, bool RK>
+// The seam faces of planes [kz_first, kz_last), in ONE launch: the edge zones split into three
+// disjoint groups, so no zone is written by two threads and no ordering is needed --
+//   Y: the y seam faces whose two zones are not tile corners (lanes 1..30): one thread per face
+//   X: the x seam faces in rows that are not a tile's first or last: one thread per face
+//   C: the tile-corner zones (lane 0 / 31 of a tile's first / last row): one thread per zone,
+//      solving its own x and y seam faces (each corner face is solved by both of its zones,
+//      from the same two published states, so both apply the same flux)
+// A face's flux is subtracted from the zone on its low side and added to the zone on its high
+// side (times cx or cy, and b at an RK stage); every thread then takes the CFL estimate of the
+// zones it completed; min-reduced per block. Grid (blocks of the three groups, planes).
+template <int SOLVER, bool RK>
 __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ FusedArgs a,
                                                        const SeamArgs sa) {
     if (a.ctl->done) return;
-    // grid (faces of one plane / 128, planes); along the seam fastest (ja for x seams, ia
-    // for y seams), then the seam index
-    const int along = AXIS == 0 ? a.ny : a.nx, nseam = AXIS == 0 ? sa.ntx : sa.nty;
-    const unsigned idx = blockIdx.x * 128u + threadIdx.x;
-    double dloc = 1.0e32;
-    if (idx < unsigned(nseam * along)) {
-        const int sidx = int(idx / unsigned(along));
-        const int l = int(idx - unsigned(sidx) * unsigned(along));
-        const int p = a.kz_first + int(blockIdx.y);
-        const int cur = a.ctl->cur;
-        double* out = a.buf[(cur + a.out_rel) % a.nbuf];
-        const double dt0 = a.ctl->dt;
-        const double c = AXIS == 0 ? dt0 * a.idx : dt0 * a.idy;
-        const double* rec = AXIS == 0 ? seam_x(sa, p, sidx, l, 0) : seam_y(sa, p, sidx, l, 0);
-        // the two zones: low side (west / south, wrapping at the mesh edge) and high side
-        int il, jl, ih, jh;
-        if (AXIS == 0) {
-            ih = sidx * SEAM_TX;
-            il = (sidx == 0 ? a.nx : ih) - 1;
-            jl = jh = l;
-        } else {
-            int h, y0;
-            seam_rows(a.ny, sa.nty, sidx, h, y0);
-            jh = y0;
-            jl = (sidx == 0 ? a.ny : y0) - 1;
-            il = ih = l;
-        }
-        auto zidx = [&](int i, int j) {
-            return (size_t(p + a.gh) * a.my_pad + size_t(j + a.gh)) * a.pitch +
-                   size_t(i + a.gh) * NV;
-        };
-        const size_t zl = zidx(il, jl), zh = zidx(ih, jh);
-        double ul[NV], ur[NV], f5[NV], vl[NV], vh[NV];
+    const int p = a.kz_first + int(blockIdx.y);
+    const int nby = (sa.nty * a.nx + 127) / 128, nbx = (sa.ntx * a.ny + 127) / 128;
+    const int bid = int(blockIdx.x);
+    const int grp = bid < nby ? 0 : (bid < nby + nbx ? 1 : 2);  // Y, X, C
+    const unsigned idx = unsigned(bid - (grp == 0 ? 0 : (grp == 1 ? nby : nby + nbx))) * 128u +
+                         threadIdx.x;
+    const int cur = a.ctl->cur;
+    double* out = a.buf[(cur + a.out_rel) % a.nbuf];
+    const double dt0 = a.ctl->dt;
+    const double cx = RK ? a.rk_b * (dt0 * a.idx) : dt0 * a.idx;
+    const double cy = RK ? a.rk_b * (dt0 * a.idy) : dt0 * a.idy;
+    auto zidx = [&](int i, int j) {
+        return (size_t(p + a.gh) * a.my_pad + size_t(j + a.gh)) * a.pitch + size_t(i + a.gh) * NV;
+    };
+    // the flux of the seam face whose records start at rec (SoA, `along` apart per component)
+    auto solve = [&](const double* rec, int along, int axis, int fa, int fb, double* f5) {
+        double ul[NV], ur[NV];
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-            ul[q] = rec[q * along];             // side 0
-            ur[q] = rec[(NV + q) * along];      // side 1
-            vl[q] = out[zl + q];
-            vh[q] = out[zh + q];
+            ul[q] = rec[q * along];         // side 0: the low zone's state
+            ur[q] = rec[(NV + q) * along];  // side 1: the high zone's state
         }
         Fault f;
         f.clear();
-        face_flux<SOLVER, AXIS>(ul, ur, a.gamma, f5, f);
-        if (f.code) {
-            if (AXIS == 0) record_fault(a.eb, ST_FLUX, f, ih, jh, p, 0);
-            else record_fault(a.eb, ST_FLUX, f, jh, ih, p, 1);
+        if (axis == 0)
+            face_flux<SOLVER, 0>(ul, ur, a.gamma, f5, f);
+        else
+            face_flux<SOLVER, 1>(ul, ur, a.gamma, f5, f);
+        if (f.code) record_fault(a.eb, ST_FLUX, f, fa, fb, p, axis);
+    };
+    auto cfl = [&](const double* v, int i, int j) {
+        if (RK && !a.want_dt) return 1.0e32;
+        Fault f3;
+        f3.clear();
+        double d = eval_tstep_inv<FM>(v, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
+        if (f3.redo()) {
+            V5 u5;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) u5.v[q] = v[q];
+            f3.clear();
+            d = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f3);
         }
-        const double cb = RK ? a.rk_b * c : c;
+        if (f3.code) {
+            record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f3, i, j, p, 0);
+            return 1.0e32;
+        }
+        return d;
+    };
+    double dloc = 1.0e32;
+    if (grp < 2) {  // one face, two zones
+        const int along = grp == 0 ? a.nx : a.ny, nseam = grp == 0 ? sa.nty : sa.ntx;
+        if (idx < unsigned(nseam * along)) {
+            const int sidx = int(idx / unsigned(along));
+            const int l = int(idx - unsigned(sidx) * unsigned(along));
+            // corner zones belong to group C
+            const bool skip = grp == 0 ? ((l & (SEAM_TX - 1)) == 0 || (l & (SEAM_TX - 1)) == SEAM_TX - 1)
+                                       : seam_row_edge(a.ny, sa.nty, l);
+            if (!skip) {
+                int il, jl, ih, jh;
+                if (grp == 1) {
+                    ih = sidx * SEAM_TX;
+                    il = (sidx == 0 ? a.nx : ih) - 1;
+                    jl = jh = l;
+                } else {
+                    int h, y0;
+                    seam_rows(a.ny, sa.nty, sidx, h, y0);
+                    jh = y0;
+                    jl = (sidx == 0 ? a.ny : y0) - 1;
+                    il = ih = l;
+                }
+                const size_t zl = zidx(il, jl), zh = zidx(ih, jh);
+                double vl[NV], vh[NV], f5[NV];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    vl[q] = out[zl + q];
+                    vh[q] = out[zh + q];
+                }
+                if (grp == 1)
+                    solve(seam_x(sa, p, sidx, l, 0), a.ny, 0, ih, jh, f5);
+                else
+                    solve(seam_y(sa, p, sidx, l, 0), a.nx, 1, jh, ih, f5);
+                const double c = grp == 1 ? cx : cy;
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    vl[q] = vl[q] - c * f5[q];  // its east / north face
+                    vh[q] = vh[q] + c * f5[q];  // its west / south face
+                    out[zl + q] = vl[q];
+                    out[zh + q] = vh[q];
+                }
+                dloc = smin(cfl(vl, il, jl), cfl(vh, ih, jh));
+            }
+        }
+    } else if (idx < unsigned(4 * sa.ntx * sa.nty)) {  // a tile-corner zone
+        const int tile = int(idx >> 2), corner = int(idx & 3u);
+        const int bx = tile % sa.ntx, by = tile / sa.ntx;
+        int h, y0;
+        seam_rows(a.ny, sa.nty, by, h, y0);
+        const bool east = corner & 1, north = corner & 2;
+        const int i = bx * SEAM_TX + (east ? SEAM_TX - 1 : 0);
+        const int j = y0 + (north ? h - 1 : 0);
+        const size_t z = zidx(i, j);
+        double v[NV], fx[NV], fy[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = out[z + q];
+        const int sx = east ? (bx + 1 == sa.ntx ? 0 : bx + 1) : bx;
+        const int sy = north ? (by + 1 == sa.nty ? 0 : by + 1) : by;
+        solve(seam_x(sa, p, sx, j, 0), a.ny, 0, east ? i + 1 : i, j, fx);
+        solve(seam_y(sa, p, sy, i, 0), a.nx, 1, north ? j + 1 : j, i, fy);
+        const double sxs = east ? -cx : cx, sys = north ? -cy : cy;
 #pragma unroll
         for (int q = 0; q < NV; ++q) {
-            vl[q] = vl[q] - cb * f5[q];  // its east / north face
-            vh[q] = vh[q] + cb * f5[q];  // its west / south face
-            out[zl + q] = vl[q];
-            out[zh + q] = vh[q];
+            v[q] = (v[q] + sxs * fx[q]) + sys * fy[q];
+            out[z + q] = v[q];
         }
-        // CFL of the zones completed here (x pass: not in a tile's first or last row)
-        if ((!RK || a.want_dt) && (AXIS == 1 || !seam_row_edge(a.ny, sa.nty, l))) {
-            double d[2];
-            const double* v[2] = {vl, vh};
-            const int zi[2] = {il, ih}, zj[2] = {jl, jh};
-#pragma unroll
-            for (int s = 0; s < 2; ++s) {
-                Fault f3;
-                f3.clear();
-                d[s] = eval_tstep_inv<FM>(v[s], a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
-                if (f3.redo()) {
-                    V5 u5;
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) u5.v[q] = v[s][q];
-                    f3.clear();
-                    d[s] = eval_tstep_careful(u5, a.cfl, a.dx, a.dy, a.dz, a.gamma, &f3);
-                }
-                if (f3.code) {
-                    record_fault(a.eb, RK ? ST_DT : ST_UPDATE, f3, zi[s], zj[s], p, 0);
-                    d[s] = 1.0e32;
-                }
-            }
-            dloc = smin(d[0], d[1]);
-        }
+        dloc = cfl(v, i, j);
     }
     if (RK && !a.want_dt) return;
     __shared__ double red[4];

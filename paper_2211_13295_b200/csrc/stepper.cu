@@ -584,7 +584,7 @@ static int launch_step(hc_stepper* s, FusedArgs a, bool rk, cudaStream_t st) {
     if (s->seam) {
         a.tz = s->seam_tz;
         if ((rc = launch_seam_fast(a, s->sa, s->p.order, s->p.solver, rk, st))) return rc;
-        s->launches += 3;
+        s->launches += 2;
         return HC_OK;
     }
     const PersistLaunch* pl = s->persist ? &s->pl : nullptr;

@@ -93,8 +93,6 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-__device__ unsigned g_sm_ctr[256];
-
 template <bool O3, int TX, int TY>
 struct FusedShape {
     static constexpr int R = O3 ? 2 : 1;   // reconstruction stencil radius
@@ -390,21 +388,6 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                 eidx = l < TPW ? w * TPW + l
                                : (l < TPW + RPW ? TX * TY + w * RPW + (l - TPW) : S::NE + w);
             }
-        }
-    }
-    if (a.desync_ns | a.swap_mode) {
-        // co-resident CTAs alternate (per-SM arrival counter): a start offset and/or the ring
-        // warps on the other SMSP pair, so the two CTAs' light phases do not coincide
-        __shared__ int s_par;
-        if (tid == 0) {
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            s_par = int(atomicAdd(&g_sm_ctr[smid & 255u], 1u) & 1u);
-        }
-        __syncthreads();
-        if (s_par) {
-            if (a.swap_mode && tid >= 128) eidx ^= 64;
-            if (a.desync_ns) __nanosleep(unsigned(a.desync_ns));
         }
     }
     double* part = red + 32 + eidx;         // [NV] stride TX*TY (owned threads only)

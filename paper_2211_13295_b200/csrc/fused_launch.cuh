@@ -40,16 +40,6 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
         const char* v = std::getenv("HC_INTERLEAVE");
         return v ? std::atoi(v) : 0;
     }();
-    static const int desync = [] {
-        const char* v = std::getenv("HC_DESYNC");
-        return v ? std::atoi(v) : 0;
-    }();
-    static const int swap = [] {
-        const char* v = std::getenv("HC_SWAP");
-        return v ? std::atoi(v) : 0;
-    }();
-    b.desync_ns = desync;
-    b.swap_mode = (swap && S::NT == 256) ? 1 : 0;
     constexpr int NW = S::NT / 32;
     b.interleave = (inter && (TX * TY) % NW == 0 && (S::NE - TX * TY) % NW == 0) ? 1 : 0;
     dim3 grid((a.nx + TX - 1) / TX, (a.ny + TY - 1) / TY,

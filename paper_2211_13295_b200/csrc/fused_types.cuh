@@ -28,8 +28,6 @@ struct FusedArgs {
     int want_dt;     // take the CFL estimate (ADER: always; RK: last stage)
     int bulk;        // plane loads by bulk copy (set by the launcher)
     int interleave;  // ring kernel: tile and ring E-columns mixed on every warp (launcher)
-    int desync_ns;   // experiment: every other CTA on an SM starts this late (launcher, env)
-    int swap_mode;   // experiment: every other CTA on an SM puts its ring warps on SMSPs 0-1
     double rk_a, rk_b;  // RK stage coefficients U' = a U0 + b (U + dt rate)
     int nx, ny, nz;  // active zones of this patch / slab
     int gh;          // storage ghost width

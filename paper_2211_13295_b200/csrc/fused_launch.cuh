@@ -42,6 +42,9 @@ static int launch_cfg(const FusedArgs& a, cudaStream_t st) {
     }();
     constexpr int NW = S::NT / 32;
     b.interleave = (inter && (TX * TY) % NW == 0 && (S::NE - TX * TY) % NW == 0) ? 1 : 0;
+    // an empty plane range only configures the kernel (loads its module, sets the shared-
+    // memory opt-in): the stepper does this at creation, outside any timed loop
+    if (a.kz_last <= a.kz_first) return HC_OK;
     dim3 grid((a.nx + TX - 1) / TX, (a.ny + TY - 1) / TY,
               (a.kz_last - a.kz_first + a.tz - 1) / a.tz);
     kern<<<grid, S::NT, S::SMEM, st>>>(b);

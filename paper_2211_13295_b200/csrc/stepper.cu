@@ -337,6 +337,18 @@ static int setup_seam(hc_stepper* s) {
     return HC_OK;
 }
 
+// Configures the fused kernels this stepper will launch (module load, shared-memory opt-in)
+// at creation, so the first timed step does not pay for them (the seam kernels are configured
+// by setup_seam's occupancy query).
+static int preload_kernels(hc_stepper* s) {
+    if (s->seam || s->persist) return HC_OK;
+    FusedArgs a = fused_args(s);
+    a.kz_last = a.kz_first;  // empty range: configure only
+    const bool rk = s->o.integrator != 0;
+    return s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, s->st)
+                      : launch_fused_fast(a, s->p.order, s->p.solver, rk, s->st);
+}
+
 static size_t state_bytes(const hc_stepper* s) {
     return size_t(s->sg.mz) * s->sg.my * s->sg.mx * NV * sizeof(double);
 }
@@ -447,7 +459,7 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         hc_stepper_destroy(s);
         return rc;
     }
-    if ((rc = setup_persist(s)) || (rc = setup_seam(s)) ||
+    if ((rc = setup_persist(s)) || (rc = setup_seam(s)) || (rc = preload_kernels(s)) ||
         (rc = (cudaStreamSynchronize(s->st) == cudaSuccess
                                               ? HC_OK : cuda_fail(cudaGetLastError(),
                                                                   "persist setup")))) {

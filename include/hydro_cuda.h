@@ -289,6 +289,9 @@ typedef struct {
     int integrator;  /* as hc_stepper_opts */
     int device;      /* hc_domain_create: this rank's GPU */
     int transport;   /* hc_exchange_kind; HC_XCHG_PEER only with hc_domain_create_local */
+    int overlap;     /* 1: the halo exchange runs on a second stream while the interior planes
+                      * (whose stencils never reach a z ghost) are updated; then the two
+                      * boundary ranges. 0: exchange, then the whole slab. Same bits. */
 } hc_domain_opts;
 
 /* An NCCL unique id for hc_domain_create (rank 0 makes it and shares it out of band);

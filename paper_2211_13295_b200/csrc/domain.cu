@@ -106,6 +106,9 @@ struct Slab {
     ncclComm_t comm = nullptr;
     double* buf[3] = {nullptr, nullptr, nullptr};
     int nbuf = 2;
+    // overlap: the halo exchange runs on xstream while the interior planes are computed
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
 };
 
 }  // namespace
@@ -179,6 +182,11 @@ int make_slab(hc_domain* d, Slab& x) {
     if ((rc = hc_stepper_create(&g, &d->p, &so, &x.st))) return rc;
     HC_CUDA(cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking));
     if ((rc = hc_stepper_set_stream(x.st, x.stream))) return rc;
+    if (d->o.overlap) {
+        HC_CUDA(cudaStreamCreateWithFlags(&x.xstream, cudaStreamNonBlocking));
+        HC_CUDA(cudaEventCreateWithFlags(&x.ev_ready, cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&x.ev_done, cudaEventDisableTiming));
+    }
     if ((rc = hc_stepper_buffers(x.st, x.buf, &x.nbuf))) return rc;
     int my_pad = 0, pitch = 0, mz = 0;
     hc_stepper_layout(x.st, &my_pad, &pitch, &mz);
@@ -202,8 +210,10 @@ int common_init(hc_domain* d, const hc_geom* g, const hc_params* p, const hc_dom
 
 // z halos of every local slab, buffer b: NCCL group (send down, receive from above, send up,
 // receive from below -- the posting order that keeps the k-th send to a peer matched with
-// that peer's k-th receive even when, at world 2, below == above), or peer copies.
-int exchange(hc_domain* d, int b) {
+// that peer's k-th receive even when, at world 2, below == above), or peer copies. xs: on the
+// slabs' exchange streams (overlap; the caller orders the compute streams after them).
+int exchange(hc_domain* d, int b, bool xs) {
+    auto S = [&](const Slab& x) { return xs ? x.xstream : x.stream; };
     const int gh = d->gh, nl = d->nloc, W = d->world;
     const bool periodic = d->o.bc[2] == HC_PERIODIC;
     const size_t cnt = size_t(gh) * d->plane;  // doubles per message
@@ -219,12 +229,12 @@ int exchange(hc_domain* d, int b) {
             double* hi_act = plane_ptr(d, x, b, nl);
             double* lo_gh = plane_ptr(d, x, b, 0);
             double* hi_gh = plane_ptr(d, x, b, gh + nl);
-            if (lo >= 0) HC_NCCL(N.Send(lo_act, cnt, ncclFloat64, lo, x.comm, x.stream));
+            if (lo >= 0) HC_NCCL(N.Send(lo_act, cnt, ncclFloat64, lo, x.comm, S(x)));
             if (hi >= 0) {
-                HC_NCCL(N.Recv(hi_gh, cnt, ncclFloat64, hi, x.comm, x.stream));
-                HC_NCCL(N.Send(hi_act, cnt, ncclFloat64, hi, x.comm, x.stream));
+                HC_NCCL(N.Recv(hi_gh, cnt, ncclFloat64, hi, x.comm, S(x)));
+                HC_NCCL(N.Send(hi_act, cnt, ncclFloat64, hi, x.comm, S(x)));
             }
-            if (lo >= 0) HC_NCCL(N.Recv(lo_gh, cnt, ncclFloat64, lo, x.comm, x.stream));
+            if (lo >= 0) HC_NCCL(N.Recv(lo_gh, cnt, ncclFloat64, lo, x.comm, S(x)));
         }
         HC_NCCL(N.GroupEnd());
     } else {  // peer copies: every slab in this process; each pulls its two halos
@@ -233,31 +243,35 @@ int exchange(hc_domain* d, int b) {
         for (size_t i = 0; i < d->s.size(); ++i) {
             HC_CUDA(cudaSetDevice(d->s[i].device));
             HC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
-            HC_CUDA(cudaEventRecord(ev[i], d->s[i].stream));
+            HC_CUDA(cudaEventRecord(ev[i], S(d->s[i])));
         }
         for (Slab& x : d->s) {
             HC_CUDA(cudaSetDevice(x.device));
-            for (size_t i = 0; i < d->s.size(); ++i) HC_CUDA(cudaStreamWaitEvent(x.stream, ev[i], 0));
+            for (size_t i = 0; i < d->s.size(); ++i) HC_CUDA(cudaStreamWaitEvent(S(x), ev[i], 0));
             const int lo = below(x.rank), hi = above(x.rank);
             if (hi >= 0) {
                 const Slab& y = d->s[size_t(hi)];
                 HC_CUDA(cudaMemcpyPeerAsync(plane_ptr(d, x, b, gh + nl), x.device,
-                                            plane_ptr(d, y, b, gh), y.device, bytes, x.stream));
+                                            plane_ptr(d, y, b, gh), y.device, bytes, S(x)));
             }
             if (lo >= 0) {
                 const Slab& y = d->s[size_t(lo)];
                 HC_CUDA(cudaMemcpyPeerAsync(plane_ptr(d, x, b, 0), x.device,
-                                            plane_ptr(d, y, b, nl), y.device, bytes, x.stream));
+                                            plane_ptr(d, y, b, nl), y.device, bytes, S(x)));
             }
         }
-        // the next stage overwrites the sources: order every slab after every copy
-        for (size_t i = 0; i < d->s.size(); ++i) {
-            HC_CUDA(cudaSetDevice(d->s[i].device));
-            HC_CUDA(cudaEventRecord(ev[i], d->s[i].stream));
-        }
-        for (Slab& x : d->s) {
-            HC_CUDA(cudaSetDevice(x.device));
-            for (size_t i = 0; i < d->s.size(); ++i) HC_CUDA(cudaStreamWaitEvent(x.stream, ev[i], 0));
+        // the next stage overwrites the sources: order every slab after every copy (with
+        // overlap the caller orders the compute streams after every exchange stream)
+        if (!xs) {
+            for (size_t i = 0; i < d->s.size(); ++i) {
+                HC_CUDA(cudaSetDevice(d->s[i].device));
+                HC_CUDA(cudaEventRecord(ev[i], d->s[i].stream));
+            }
+            for (Slab& x : d->s) {
+                HC_CUDA(cudaSetDevice(x.device));
+                for (size_t i = 0; i < d->s.size(); ++i)
+                    HC_CUDA(cudaStreamWaitEvent(x.stream, ev[i], 0));
+            }
         }
         for (size_t i = 0; i < d->s.size(); ++i) cudaEventDestroy(ev[i]);
     }
@@ -269,12 +283,12 @@ int exchange(hc_domain* d, int b) {
                 if (x.rank == 0)
                     HC_CUDA(cudaMemcpyAsync(plane_ptr(d, x, b, k), plane_ptr(d, x, b, gh),
                                             d->plane * sizeof(double), cudaMemcpyDeviceToDevice,
-                                            x.stream));
+                                            S(x)));
                 if (x.rank == W - 1)
                     HC_CUDA(cudaMemcpyAsync(plane_ptr(d, x, b, gh + nl + k),
                                             plane_ptr(d, x, b, gh + nl - 1),
                                             d->plane * sizeof(double), cudaMemcpyDeviceToDevice,
-                                            x.stream));
+                                            S(x)));
             }
         }
     }
@@ -325,9 +339,34 @@ int one_step(hc_domain* d) {
             if ((rc = set_dev(x.device)) || (rc = hc_stepper_fill_ghosts(x.st))) return rc;
         }
         // the buffer this stage reads: cur (ADER, RK stage 0) or the previous stage's result
-        if ((rc = exchange(d, (d->cur + (d->o.integrator ? k : 0)) % nbuf))) return rc;
+        const int b = (d->cur + (d->o.integrator ? k : 0)) % nbuf;
+        const int G = d->gh;  // planes whose stencils reach a z ghost plane, on each side
+        if (!d->o.overlap || d->nloc <= 2 * G) {
+            if ((rc = exchange(d, b, false))) return rc;
+            for (Slab& x : d->s) {
+                if ((rc = set_dev(x.device)) || (rc = hc_stepper_compute(x.st))) return rc;
+            }
+            continue;
+        }
+        // overlap: the exchange on the side streams while the interior planes [G, nloc - G)
+        // -- whose stencils never reach a z ghost -- are updated, then the two boundary ranges
         for (Slab& x : d->s) {
-            if ((rc = set_dev(x.device)) || (rc = hc_stepper_compute(x.st))) return rc;
+            if ((rc = set_dev(x.device))) return rc;
+            HC_CUDA(cudaEventRecord(x.ev_ready, x.stream));
+            HC_CUDA(cudaStreamWaitEvent(x.xstream, x.ev_ready, 0));
+        }
+        if ((rc = exchange(d, b, true))) return rc;
+        for (Slab& x : d->s) {
+            if ((rc = set_dev(x.device))) return rc;
+            HC_CUDA(cudaEventRecord(x.ev_done, x.xstream));
+            if ((rc = hc_stepper_compute_range(x.st, G, d->nloc - G, 0))) return rc;
+        }
+        for (Slab& x : d->s) {
+            if ((rc = set_dev(x.device))) return rc;
+            for (Slab& y : d->s) HC_CUDA(cudaStreamWaitEvent(x.stream, y.ev_done, 0));
+            if ((rc = hc_stepper_compute_range(x.st, 0, G, 0)) ||
+                (rc = hc_stepper_compute_range(x.st, d->nloc - G, d->nloc, 1)))
+                return rc;
         }
     }
     // global dt min (transfer.cpp:184): one 8-byte all-reduce on the device accumulators
@@ -485,6 +524,12 @@ int hc_domain_destroy(hc_domain* d) {
         if (x.comm && d->nccl_owned) nccl().CommDestroy(x.comm);
         if (x.st) hc_stepper_destroy(x.st);
         if (x.stream) cudaStreamDestroy(x.stream);
+        if (x.xstream) {
+            cudaStreamSynchronize(x.xstream);
+            cudaStreamDestroy(x.xstream);
+        }
+        if (x.ev_ready) cudaEventDestroy(x.ev_ready);
+        if (x.ev_done) cudaEventDestroy(x.ev_done);
     }
     delete d;
     return HC_OK;

@@ -417,7 +417,7 @@ class Stepper:
 class DomainOpts(C.Structure):
     """hc_domain_opts (include/hydro_cuda.h)."""
     _fields_ = [("bc", C.c_int * 3), ("exact", C.c_int), ("integrator", C.c_int),
-                ("device", C.c_int), ("transport", C.c_int)]
+                ("device", C.c_int), ("transport", C.c_int), ("overlap", C.c_int)]
 
 
 XCHG_NCCL, XCHG_PEER = 0, 1  # hc_exchange_kind
@@ -442,7 +442,7 @@ class Domain:
 
     def __init__(self, geom: Geom, params: Params, bc=(PERIODIC, PERIODIC, PERIODIC),
                  exact=True, integrator=ADER, transport=XCHG_NCCL, devices=(0,), rank=None,
-                 world=None, nccl_id=None, device=0):
+                 world=None, nccl_id=None, device=0, overlap=False):
         self.lib = load_library()
         self.geom, self.params = geom, params
         o = DomainOpts()
@@ -450,6 +450,7 @@ class Domain:
             o.bc[a] = bc[a]
         o.exact, o.integrator, o.device, o.transport = int(bool(exact)), integrator, device, \
             transport
+        o.overlap = int(bool(overlap))
         h = C.c_void_p()
         if rank is None:
             devs = (C.c_int * len(devices))(*devices)

@@ -84,7 +84,7 @@ static int run_case(int exact, int integrator, int mode) {
 
     /* the domain */
     hc_domain_opts o = {{HC_PERIODIC, HC_PERIODIC, HC_PERIODIC}, exact, integrator, 0,
-                        mode == 2 ? HC_XCHG_PEER : HC_XCHG_NCCL};
+                        mode == 2 ? HC_XCHG_PEER : HC_XCHG_NCCL, mode == 1};
     hc_domain* d = NULL;
     if (mode == 1) {
         unsigned char id[128];

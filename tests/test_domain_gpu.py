@@ -32,8 +32,9 @@ def _single(g, params, s0, dt0, cfl, steps, exact, integ, bc):
 
 @pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("integ", [hydro.ADER, hydro.RK3])
-@pytest.mark.parametrize("transport", [hydro.XCHG_NCCL, hydro.XCHG_PEER])
-def test_domain_self_exchange_bitwise(exact, integ, transport):
+@pytest.mark.parametrize("transport,overlap", [(hydro.XCHG_NCCL, False), (hydro.XCHG_PEER, False),
+                                               (hydro.XCHG_NCCL, True), (hydro.XCHG_PEER, True)])
+def test_domain_self_exchange_bitwise(exact, integ, transport, overlap):
     order, shape, steps = 3, (64, 14, 12), 4
     api = hydro.HostApi()
     g = hydro.make_geometry(*shape, order)
@@ -42,7 +43,8 @@ def test_domain_self_exchange_bitwise(exact, integ, transport):
     dt0 = api.initial_dt(g, s0, 0.4)
     bc = (hydro.PERIODIC,) * 3
     want, t1, dt1, n1, kind = _single(g, params, s0, dt0, 0.4, steps, exact, integ, bc)
-    d = hydro.Domain(g, params, bc=bc, exact=exact, integrator=integ, transport=transport)
+    d = hydro.Domain(g, params, bc=bc, exact=exact, integrator=integ, transport=transport,
+                     overlap=overlap)
     assert d.nslabs == 1 and d.nz_local == shape[2] and d.kernel == kind
     d.scatter(s0)
     d.set_time(0.0, dt0, 0.4)

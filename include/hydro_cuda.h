@@ -269,6 +269,25 @@ int hc_patchset_sync(hc_patchset* ps, double* t, double* dt, long* steps_done);
 int hc_patchset_ledger(hc_patchset* ps, unsigned long long* counts6);
 long hc_patchset_launches(hc_patchset* ps);
 
+/* ------------------------------------------------ fourth-order ADER (extension)
+ * NOT in the reference (orders 2-3 only, geometry.hpp:13-27). The reference's ADER structure
+ * (one face state per face, the zone mean's tau at the midpoint: predictor.cpp:26-60,
+ * corrector.cpp:30-33) is second order in time, whatever the reconstruction order; this step
+ * is formally fourth order: a degree-3 WENO-AO + cross-term reconstruction, a local space-time
+ * predictor (Picard iterations on 4 x 4 x 4 x 4 Gauss-Legendre space-time nodes), fluxes at the
+ * 2 x 2 face x 2 time Gauss points (csrc/ader4.cu). Skinny layout, ghost width 3, the same
+ * vortex ICs and time-control semantics as hc_stepper; boundary = HC_PERIODIC / HC_OUTFLOW. */
+typedef struct hc_ader4 hc_ader4;
+int hc_ader4_create(const hc_geom* g, const hc_params* p, int boundary, int device,
+                    hc_ader4** out);
+int hc_ader4_destroy(hc_ader4* s);
+int hc_ader4_upload(hc_ader4* s, const double* host_skinny);
+int hc_ader4_download(hc_ader4* s, double* host_skinny);
+int hc_ader4_set_time(hc_ader4* s, double t, double dt, double cfl, double t_final);
+int hc_ader4_step(hc_ader4* s, int n);
+int hc_ader4_sync(hc_ader4* s, double* t, double* dt, long* steps_done);
+long hc_ader4_launches(hc_ader4* s);
+
 /* ------------------------------------------------ multi-GPU z-slab domain
  * The reference's PatchSet split along z -- make_patch_set(global, 1, 1, world)
  * (transfer.hpp:60-61, transfer.cpp:17-47) -- with every patch (slab) on its own GPU, and

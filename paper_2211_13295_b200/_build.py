@@ -32,6 +32,7 @@ SOURCES = {
     "mhd.cu": ["--fmad=false"],
     "ced.cu": ["--fmad=false"],
     "domain.cu": ["--fmad=false"],
+    "ader4.cu": ["--fmad=true"],
 }
 
 

@@ -161,6 +161,9 @@ def load_library(path: str = LIB_PATH):
     lib.hc_stepper_launches.restype = C.c_long
     lib.hc_stepper_launches.argtypes = [C.c_void_p]
     lib.hc_domain_launches.restype = C.c_long
+    lib.hc_ader4_launches.restype = C.c_long
+    lib.hc_ader4_destroy.argtypes = [C.c_void_p]
+    lib.hc_ader4_step.argtypes = [C.c_void_p, C.c_int]
     for name in ("hc_domain_launches", "hc_domain_destroy", "hc_domain_info",
                  "hc_domain_scatter", "hc_domain_gather", "hc_domain_sync"):
         getattr(lib, name).argtypes = None
@@ -412,6 +415,54 @@ class Stepper:
         k, n = C.c_int(), C.c_int()
         _check(self.lib.hc_stepper_info(self.h, C.byref(k), C.byref(n)))
         return ("ring", "persistent", "seam")[k.value], n.value
+
+
+class Ader4Stepper:
+    """The formally fourth-order ADER step of csrc/ader4.cu (hc_ader4_*; an extension: the
+    reference's ADER structure is second order in time): degree-3 WENO-AO + cross-term
+    reconstruction, local space-time predictor, Gauss-point face and time quadrature."""
+
+    def __init__(self, geom: Geom, params: Params, boundary=PERIODIC, device=0):
+        self.lib = load_library()
+        self.geom = geom
+        h = C.c_void_p()
+        _check(self.lib.hc_ader4_create(C.byref(geom), C.byref(params), boundary, device,
+                                        C.byref(h)))
+        self.h = h
+
+    def upload(self, skinny: np.ndarray):
+        a = np.ascontiguousarray(skinny, dtype=np.float64)
+        _check(self.lib.hc_ader4_upload(self.h, a.ctypes.data_as(C.c_void_p)))
+
+    def download(self, out: np.ndarray | None = None):
+        g = self.geom
+        if out is None:
+            out = np.empty((g.nz + 2 * g.ghost, g.ny + 2 * g.ghost, g.nx + 2 * g.ghost, 5))
+        _check(self.lib.hc_ader4_download(self.h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def set_time(self, t, dt, cfl, t_final=0.0):
+        _check(self.lib.hc_ader4_set_time(self.h, C.c_double(t), C.c_double(dt),
+                                          C.c_double(cfl), C.c_double(t_final)))
+
+    def step(self, n=1):
+        _check(self.lib.hc_ader4_step(self.h, int(n)))
+
+    def sync(self):
+        t, dt, n = C.c_double(), C.c_double(), C.c_long()
+        _check(self.lib.hc_ader4_sync(self.h, C.byref(t), C.byref(dt), C.byref(n)))
+        return t.value, dt.value, n.value
+
+    def close(self):
+        if self.h:
+            self.lib.hc_ader4_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DomainOpts(C.Structure):

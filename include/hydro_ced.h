@@ -34,7 +34,11 @@ extern "C" {
 #define HC_CED_NVAR 6
 
 typedef struct {
-    int order;      /* 2 (MC) or 3 (WENO3 + cross terms) */
+    int order;      /* 2 (MC), 3 (WENO3 + cross terms) -- the reference's ADER structure, second
+                     * order in time -- or 4: the local space-time predictor with the conduction
+                     * source implicit inside it (Radau IIA collocation, one 4 x 4 block
+                     * inversion per zone) and edge E, H at space-time Gauss points (formally
+                     * fourth order; ced.cu k_ced4_*) */
     double eps, mu; /* uniform permittivity and permeability; c = 1/sqrt(eps mu) */
     hc_limiter lim;
     int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis */

@@ -321,6 +321,382 @@ __global__ void k_ced_update(CArgs a) {
     }
 }
 
+// ============================================================ order 4 (space-time ADER)
+// The O2/O3 kernels above keep the reference's ADER structure (face state + the zone's tau/2),
+// second order in time. Order 4 is the scheme of the paper's CED runs: a
+// local space-time predictor with the stiff conduction source solved IMPLICITLY inside it by
+// small block inversions, then edge E and H integrated at space-time Gauss points:
+//   k_ced4_predict  one CTA per ring zone, one thread per space-time node (4 x 4 x 4 Gauss-
+//                   Legendre points x 4 Radau IIA times in [t, t + dt]): the degree-3 polynomial
+//                   of the six cell fields (WENO-AO pure terms, central mixed terms, as
+//                   ader4.cu), then Picard iterations of the collocation system
+//                     q(tau_m) = P - dt sum_l A_ml (div F(q(tau_l)) + s q_D(tau_l)),  s = sigma/eps
+//                   with the source implicit: per spatial node the 4 x 4 system
+//                   (I + s dt A) q_D = P - dt A div F_D, inverted once per zone; Radau IIA is
+//                   L-stable, so sigma dt >> 1 relaxes D instead of ringing
+//   outputs         the fields at the 2 Gauss points along each of the 12 zone edges at the 2
+//                   Gauss times ([48][6][N] in `states`)
+//   k_ced4_edge<C>  E_C and H_C from the four corner states at each of the 2 x 2 space-time
+//                   Gauss points (the O3 upwind formula and its asymptotic-preserving scaling),
+//                   averaged: the edge- and time-averaged EMFs
+//   k_ced4_update   B -= dt curl E (CT); D: the exponential conduction step of the O3 path
+//                   (exact for frozen curl H, L-stable) with the space-time averaged curl H
+struct CedBasis {
+    double xi[4], D[4][4];   // Gauss-Legendre nodes on [-1/2, 1/2] and d/dxi of their Lagrange basis
+    double A[4][4];          // Radau IIA: int_0^{c_m} L_l(s) ds, c on [0, 1]
+    double LF[2][4];         // L_l(+1/2), L_l(-1/2)
+    double LG[2][4];         // L_l(-+1/(2 sqrt 3))
+    double LT[2][4];         // Radau time basis at the Gauss times 1/2 -+ 1/(2 sqrt 3)
+};
+__constant__ CedBasis c_cb;
+constexpr int C4_NT = 256, C4_EDGE = 48, C4_NCOEF = 23;
+
+__device__ __forceinline__ void psi4(double s, double* p) {
+    const double s2 = s * s;
+    p[0] = s;
+    p[1] = s2 - 1.0 / 12.0;
+    p[2] = s * (s2 - 3.0 / 20.0);
+    p[3] = s2 * s2 - (3.0 / 14.0) * s2 + 3.0 / 560.0;
+}
+
+__global__ void __launch_bounds__(C4_NT) k_ced4_predict(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    __shared__ double coef[NF][C4_NCOEF];
+    __shared__ double minv[4][4];
+    extern __shared__ double sm4[];
+    double* Q = sm4;                // [256][6] nodal fields
+    double* FL = Q + C4_NT * NF;    // [3][256][6] flux components
+    double* DV = FL + 3 * C4_NT * NF;  // [256][6] divergence
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const int zr = blockIdx.x;
+    const int i = zr % rx - 1 + b.gh, j = (zr / rx) % ry - 1 + b.gh, k = zr / (rx * ry) - 1 + b.gh;
+    const size_t o = at(b, k, j, i);
+    const size_t st3[3] = {stride(b, 0), stride(b, 1), stride(b, 2)};
+    const size_t N = b.N;
+    const int t = threadIdx.x;
+    const double dt = a.ctl->dt;
+    auto W = [&](int q, long long off) { return __ldg(a.w + size_t(q) * N + size_t((long long)o + off)); };
+    auto offs = [&](int ax, int s1) { return (long long)s1 * (long long)st3[ax]; };
+    // -- reconstruction (see ader4.cu): [0] mean, [1..4] x, [5..8] y, [9..12] z, [13..22] mixed
+    if (t < 18) {
+        const int q = t / 3, ax = t % 3;
+        double m[4];
+        Fault f;
+        f.clear();
+        weno_ao<0>(W(q, offs(ax, -2)), W(q, offs(ax, -1)), W(q, 0), W(q, offs(ax, 1)),
+                   W(q, offs(ax, 2)), a.lim, m, f);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
+        if (ax == 0) coef[q][0] = W(q, 0);
+    } else if (t < 18 + NF * 10) {
+        const int q = (t - 18) / 10, term = (t - 18) % 10;
+        auto val = [&](int p1, int s1, int p2, int s2) { return W(q, offs(p1, s1) + offs(p2, s2)); };
+        double v;
+        if (term < 3) {
+            const int p1 = term, r = (term + 1) % 3;
+            v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) - (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
+        } else if (term < 9) {
+            const int pair = (term - 3) / 2, sw = (term - 3) % 2;
+            const int a1 = pair, a2 = (pair + 1) % 3;
+            const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
+            auto d2 = [&](int sg) { return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg); };
+            v = 0.25 * (d2(1) - d2(-1));
+        } else {
+            double acc = 0.0;
+            for (int cc = -1; cc <= 1; cc += 2)
+                for (int bb = -1; bb <= 1; bb += 2)
+                    for (int aa = -1; aa <= 1; aa += 2)
+                        acc += double(aa * bb * cc) * W(q, offs(0, aa) + offs(1, bb) + offs(2, cc));
+            v = 0.125 * acc;
+        }
+        coef[q][13 + term] = v;
+    } else if (t == 255) {
+        // (I + z A)^-1, z = dt sigma / eps (Gauss-Jordan on 4 x 4; the system is diagonally
+        // dominant for z >= 0, no pivoting needed)
+        const double z = dt * a.sigma[o] / a.eps;
+        double m[4][8];
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) {
+                m[r][c] = (r == c ? 1.0 : 0.0) + z * c_cb.A[r][c];
+                m[r][4 + c] = r == c ? 1.0 : 0.0;
+            }
+        for (int c = 0; c < 4; ++c) {
+            const double ip = 1.0 / m[c][c];
+            for (int cc = 0; cc < 8; ++cc) m[c][cc] *= ip;
+            for (int r = 0; r < 4; ++r)
+                if (r != c) {
+                    const double fct = m[r][c];
+                    for (int cc = 0; cc < 8; ++cc) m[r][cc] -= fct * m[c][cc];
+                }
+        }
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) minv[r][c] = m[r][4 + c];
+    }
+    __syncthreads();
+    const int ni = t & 3, nj = (t >> 2) & 3, nk = (t >> 4) & 3, nm = t >> 6;
+    double p0[NF];
+    {
+        double px[4], py[4], pz[4];
+        psi4(c_cb.xi[ni], px);
+        psi4(c_cb.xi[nj], py);
+        psi4(c_cb.xi[nk], pz);
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+            const double* c = coef[q];
+            double v = c[0];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) v += c[1 + l] * px[l] + c[5 + l] * py[l] + c[9 + l] * pz[l];
+            v += c[13] * px[0] * py[0] + c[14] * py[0] * pz[0] + c[15] * pz[0] * px[0];
+            v += c[16] * px[1] * py[0] + c[17] * px[0] * py[1];
+            v += c[18] * py[1] * pz[0] + c[19] * py[0] * pz[1];
+            v += c[20] * pz[1] * px[0] + c[21] * pz[0] * px[1];
+            v += c[22] * px[0] * py[0] * pz[0];
+            p0[q] = v;
+            Q[t * NF + q] = v;
+        }
+    }
+    __syncthreads();
+    const double ie = 1.0 / a.eps, im = 1.0 / a.mu;
+    double* RH = FL;  // right-hand sides reuse the flux storage after the divergence
+    for (int it = 0; it < 4; ++it) {
+        {
+            double u[NF], f[NF];
+#pragma unroll
+            for (int q = 0; q < NF; ++q) u[q] = Q[t * NF + q];
+            maxwell_flux<0>(u, ie, im, f);
+#pragma unroll
+            for (int q = 0; q < NF; ++q) FL[(0 * C4_NT + t) * NF + q] = f[q];
+            maxwell_flux<1>(u, ie, im, f);
+#pragma unroll
+            for (int q = 0; q < NF; ++q) FL[(1 * C4_NT + t) * NF + q] = f[q];
+            maxwell_flux<2>(u, ie, im, f);
+#pragma unroll
+            for (int q = 0; q < NF; ++q) FL[(2 * C4_NT + t) * NF + q] = f[q];
+        }
+        __syncthreads();
+        {
+            double dv[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
+                const double wx = c_cb.D[ni][l] * a.id[0], wy = c_cb.D[nj][l] * a.id[1],
+                             wz = c_cb.D[nk][l] * a.id[2];
+#pragma unroll
+                for (int q = 0; q < NF; ++q)
+                    dv[q] += wx * FL[(0 * C4_NT + tx) * NF + q] + wy * FL[(1 * C4_NT + ty) * NF + q] +
+                             wz * FL[(2 * C4_NT + tz) * NF + q];
+            }
+#pragma unroll
+            for (int q = 0; q < NF; ++q) DV[t * NF + q] = dv[q];
+        }
+        __syncthreads();
+        {  // right-hand sides P - dt sum_l A_ml div_l
+            double r[NF];
+#pragma unroll
+            for (int q = 0; q < NF; ++q) r[q] = p0[q];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int tl = (t & 63) | (l << 6);
+                const double w = dt * c_cb.A[nm][l];
+#pragma unroll
+                for (int q = 0; q < NF; ++q) r[q] -= w * DV[tl * NF + q];
+            }
+#pragma unroll
+            for (int q = 0; q < NF; ++q) RH[t * NF + q] = r[q];
+        }
+        __syncthreads();
+        {  // D: the implicit source over the time nodes of this spatial node; B: explicit
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                double v = 0.0;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) v += minv[nm][l] * RH[((t & 63) | (l << 6)) * NF + q];
+                Q[t * NF + q] = v;
+            }
+#pragma unroll
+            for (int q = 3; q < NF; ++q) Q[t * NF + q] = RH[t * NF + q];
+        }
+        __syncthreads();
+    }
+    // -- outputs, contracted one dimension at a time: (1) time -> the 2 Gauss times
+    double* T = FL;
+    if (t < 128) {
+        const int tg = t >> 6, node = t & 63;
+        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double w = c_cb.LT[tg][m];
+#pragma unroll
+            for (int q = 0; q < NF; ++q) v[q] += w * Q[((m << 6) | node) * NF + q];
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) T[t * NF + q] = v[q];
+    }
+    __syncthreads();
+    // (2) the edge points: edge axis C, corner (la, lb) in the (C+1, C+2) plane at +-1/2, the
+    //     Gauss point g along C, the Gauss time tg: e = ((C * 4 + 2 lb + la) * 2 + g) * 2 + tg
+    if (t < C4_EDGE) {
+        const int tg = t & 1, g = (t >> 1) & 1, corner = (t >> 2) & 3, C = t >> 4;
+        const int la = corner & 1, lb = corner >> 1;
+        const int AA = (C + 1) % 3, BB = (C + 2) % 3;
+        double w[3][4];
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            w[C][l] = c_cb.LG[g][l];
+            w[AA][l] = c_cb.LF[la][l];  // la = 0: +1/2
+            w[BB][l] = c_cb.LF[lb][l];
+        }
+        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int kk = 0; kk < 4; ++kk)
+            for (int jj = 0; jj < 4; ++jj)
+                for (int ii = 0; ii < 4; ++ii) {
+                    const double ww = w[2][kk] * w[1][jj] * w[0][ii];
+                    const int node = (kk * 4 + jj) * 4 + ii;
+#pragma unroll
+                    for (int q = 0; q < NF; ++q) v[q] += ww * T[((tg << 6) | node) * NF + q];
+                }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) __stcs(a.states + (size_t(t) * NF + q) * N + o, v[q]);
+    }
+}
+
+template <int C>
+__global__ void __launch_bounds__(128) k_ced4_edge(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
+    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = b.n[2] + (C != 2);
+    const size_t cnt = size_t(ex) * ey * ez;
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int c0 = int(r % ex), c1 = int((r / ex) % ey), c2 = int(r / (size_t(ex) * ey));
+    const size_t o = at(b, c2 + b.gh, c1 + b.gh, c0 + b.gh);
+    const size_t sa = stride(b, AA), sb = stride(b, BB), N = b.N;
+    double sg = 0.0;
+#pragma unroll
+    for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+        for (int la = 0; la < 2; ++la) sg = sg + a.sigma[o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0)];
+    sg = 0.25 * sg;
+    const double ta = 1.0 / (1.0 + sg * a.d[AA] / (2.0 * a.c * a.eps));
+    const double tb = 1.0 / (1.0 + sg * a.d[BB] / (2.0 * a.c * a.eps));
+    const double hc = 0.5 * a.c;
+    double E = 0.0, H = 0.0;
+    for (int gp = 0; gp < 4; ++gp) {  // (g, tg): the 2 x 2 space-time Gauss points, weight 1/4
+        double e = 0.0, h = 0.0, dbp = 0.0, dbm = 0.0, dap = 0.0, dam = 0.0;
+        double bbp = 0.0, bbm = 0.0, bap = 0.0, bam = 0.0;
+#pragma unroll
+        for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+            for (int la = 0; la < 2; ++la) {
+                const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
+                const int eidx = (C * 4 + 2 * lb + la) * 4 + gp;
+                double u[NF];
+#pragma unroll
+                for (int q = 0; q < NF; ++q) u[q] = __ldg(a.states + (size_t(eidx) * NF + q) * N + z);
+                e = e + u[C];
+                h = h + u[3 + C];
+                if (la) { dbp = dbp + u[BB]; bbp = bbp + u[3 + BB]; }
+                else { dbm = dbm + u[BB]; bbm = bbm + u[3 + BB]; }
+                if (lb) { dap = dap + u[AA]; bap = bap + u[3 + AA]; }
+                else { dam = dam + u[AA]; bam = bam + u[3 + AA]; }
+            }
+        E += 0.25 * (0.25 * e / a.eps + hc * ta * (0.5 * bbp - 0.5 * bbm) -
+                     hc * tb * (0.5 * bap - 0.5 * bam));
+        H += 0.25 * (0.25 * h / a.mu - hc * ta * (0.5 * dbp - 0.5 * dbm) +
+                     hc * tb * (0.5 * dap - 0.5 * dam));
+    }
+    a.emf[size_t(C) * N + o] = E;
+    a.hmf[size_t(C) * N + o] = H;
+}
+
+__global__ void k_ced4_update(CArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    const int px = b.n[0] + 1, py = b.n[1] + 1;
+    const size_t cnt = size_t(px) * py * (b.n[2] + 1);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= cnt) return;
+    const int i = int(r % px), j = int((r / px) % py), k = int(r / (size_t(px) * py));
+    const bool ci = i < b.n[0], cj = j < b.n[1], ck = k < b.n[2];
+    const size_t o = at(b, k + b.gh, j + b.gh, i + b.gh);
+    const size_t N = b.N, sx = 1, sy = b.P, sz = size_t(b.P) * b.Q;
+    const double dt = a.ctl->dt;
+    const double cx = dt / a.d[0], cy = dt / a.d[1], cz = dt / a.d[2];
+    const double *ex = a.emf, *ey = a.emf + N, *ez = a.emf + 2 * N;
+    const double *hx = a.hmf, *hy = a.hmf + N, *hz = a.hmf + 2 * N;
+    double* s = a.s;
+    // D on the low A face of zone o: the exponential conduction step with the space-time
+    // averaged curl H of the edges, D = exp(-z) D + phi(z) dt <curl H>, z = s_f dt -- exact for
+    // sigma = 0 (the fourth-order flux integral) and for frozen curl H, L-stable for z >> 1.
+    // (An explicit corrector source -dt s <D>_f from the zones' predictors would multiply the
+    // face-vs-reconstruction mismatch by s dt and blows up in a good conductor.)
+    const double ie = 1.0 / a.eps;
+    auto dstep = [&](int A, size_t so, double curl) {
+        double e_, p_;
+        decay(0.5 * (a.sigma[o] + a.sigma[o - so]) * ie * dt, e_, p_);
+        s[A * N + o] = e_ * s[A * N + o] + p_ * curl;
+    };
+    if (cj && ck) {
+        s[3 * N + o] = s[3 * N + o] - (cy * (ez[o + sy] - ez[o]) - cz * (ey[o + sz] - ey[o]));
+        dstep(0, sx, cy * (hz[o + sy] - hz[o]) - cz * (hy[o + sz] - hy[o]));
+    }
+    if (ci && ck) {
+        s[4 * N + o] = s[4 * N + o] - (cz * (ex[o + sz] - ex[o]) - cx * (ez[o + 1] - ez[o]));
+        dstep(1, sy, cz * (hx[o + sz] - hx[o]) - cx * (hz[o + 1] - hz[o]));
+    }
+    if (ci && cj) {
+        s[5 * N + o] = s[5 * N + o] - (cx * (ey[o + 1] - ey[o]) - cy * (ex[o + sy] - ex[o]));
+        dstep(2, sz, cx * (hy[o + 1] - hy[o]) - cy * (hx[o + sy] - hx[o]));
+    }
+}
+
+// host: Gauss-Legendre space basis, Radau IIA time basis
+CedBasis make_ced_basis() {
+    CedBasis bs;
+    const double gl[4] = {-0.8611363115940526, -0.3399810435848563, 0.3399810435848563,
+                          0.8611363115940526};
+    const double gw[4] = {0.3478548451374538, 0.6521451548625461, 0.6521451548625461,
+                          0.3478548451374538};
+    const double rc[4] = {0.08858795951270395, 0.4094668644407347, 0.7876594617608471, 1.0};
+    for (int l = 0; l < 4; ++l) bs.xi[l] = 0.5 * gl[l];
+    auto lag = [](const double* n, int l, double x) {
+        double v = 1.0;
+        for (int m = 0; m < 4; ++m)
+            if (m != l) v *= (x - n[m]) / (n[l] - n[m]);
+        return v;
+    };
+    auto dlag = [](const double* n, int l, double x) {
+        double sum = 0.0;
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk == l) continue;
+            double v = 1.0 / (n[l] - n[kk]);
+            for (int m = 0; m < 4; ++m)
+                if (m != l && m != kk) v *= (x - n[m]) / (n[l] - n[m]);
+            sum += v;
+        }
+        return sum;
+    };
+    const double g2 = 0.5 / std::sqrt(3.0);
+    for (int r = 0; r < 4; ++r)
+        for (int l = 0; l < 4; ++l) {
+            bs.D[r][l] = dlag(bs.xi, l, bs.xi[r]);
+            double sum = 0.0;  // int_0^{c_r} L_l (cubic): 4-point Gauss on [0, c_r]
+            for (int g = 0; g < 4; ++g) sum += 0.5 * rc[r] * gw[g] * lag(rc, l, 0.5 * rc[r] * (gl[g] + 1.0));
+            bs.A[r][l] = sum;
+        }
+    for (int l = 0; l < 4; ++l) {
+        bs.LF[0][l] = lag(bs.xi, l, 0.5);
+        bs.LF[1][l] = lag(bs.xi, l, -0.5);
+        bs.LG[0][l] = lag(bs.xi, l, -g2);
+        bs.LG[1][l] = lag(bs.xi, l, g2);
+        bs.LT[0][l] = lag(rc, l, 0.5 - g2);
+        bs.LT[1][l] = lag(rc, l, 0.5 + g2);
+    }
+    return bs;
+}
+
 __global__ void k_ced_div(CArgs a, double* out) {
     const Box& b = a.b;
     const size_t cnt = size_t(b.n[0]) * b.n[1] * b.n[2];
@@ -405,7 +781,32 @@ CArgs cargs(const hc_ced* m) {
     return a;
 }
 
+constexpr size_t kCed4Smem = sizeof(double) * 5 * C4_NT * NF;
+
+int launch_step4(hc_ced* m) {
+    CArgs a = cargs(m);
+    const Box& b = m->b;
+    cudaStream_t st = m->st;
+    k_ced_ghosts<<<blocks(shell_count(b), 256), 256, 0, st>>>(a, 0);
+    k_ced_cell<true><<<blocks(b.N, 256), 256, 0, st>>>(a);
+    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
+    k_ced4_predict<<<unsigned(ring), C4_NT, kCed4Smem, st>>>(a);
+    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (b.n[2] + 1);
+    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (b.n[2] + 1);
+    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * b.n[2];
+    k_ced4_edge<0><<<blocks(ex, 128), 128, 0, st>>>(a);
+    k_ced4_edge<1><<<blocks(ey, 128), 128, 0, st>>>(a);
+    k_ced4_edge<2><<<blocks(ez, 128), 128, 0, st>>>(a);
+    const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
+    k_ced4_update<<<blocks(up, 256), 256, 0, st>>>(a);
+    k_ced_advance<<<1, 1, 0, st>>>(m->ctl);
+    m->launches += 8;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "ced order-4 step launch");
+}
+
 int launch_step(hc_ced* m) {
+    if (m->p.order == 4) return launch_step4(m);
     CArgs a = cargs(m);
     const Box& b = m->b;
     const bool o3 = m->p.order == 3;
@@ -445,10 +846,14 @@ int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
         set_error(HC_INVALID, "null argument");
         return HC_INVALID;
     }
-    int rc = validate_geom(g, p->order);
+    int rc = validate_geom(g, p->order == 4 ? 3 : p->order);  // (order 4: the same stencils)
     if (rc) return rc;
-    if (g->ghost < (p->order == 3 ? 4 : 2)) {
-        set_error(HC_INVALID, "ced: order 3 needs a ghost width of at least 4");
+    if (p->order < 2 || p->order > 4) {
+        set_error(HC_INVALID, "ced: order must be 2, 3 or 4");
+        return HC_INVALID;
+    }
+    if (g->ghost < (p->order >= 3 ? 4 : 2)) {
+        set_error(HC_INVALID, "ced: orders 3 and 4 need a ghost width of at least 4");
         return HC_INVALID;
     }
     if (!(p->eps > 0.0) || !(p->mu > 0.0)) {
@@ -481,7 +886,7 @@ int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
     if (e == cudaSuccess) e = cudaMalloc(&m->s, NF * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->sigma, B);
     if (e == cudaSuccess) e = cudaMalloc(&m->w, NF * B);
-    if (e == cudaSuccess) e = cudaMalloc(&m->states, size_t(12) * NF * B);
+    if (e == cudaSuccess) e = cudaMalloc(&m->states, size_t(p->order == 4 ? C4_EDGE : 12) * NF * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->ht, NF * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, 3 * B);
     if (e == cudaSuccess) e = cudaMalloc(&m->hmf, 3 * B);
@@ -495,6 +900,13 @@ int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
     if (e == cudaSuccess) {
         StepCtl c{};
         e = cudaMemcpy(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && p->order == 4) {
+        CedBasis bs = make_ced_basis();
+        e = cudaMemcpyToSymbol(c_cb, &bs, sizeof bs);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_ced4_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kCed4Smem));
     }
     if (e != cudaSuccess) {
         hc_ced_destroy(m);

@@ -34,7 +34,10 @@ extern "C" {
 #define HC_MHD_NVAR 8
 
 typedef struct {
-    int order;      /* 2 (MC slopes) or 3 (WENO3 + cross terms) */
+    int order;      /* 2 (MC slopes) or 3 (WENO3 + cross terms) in the reference's ADER
+                     * structure (second order in time), or 4: the local space-time predictor with
+                     * face fluxes and edge EMFs at space-time Gauss points (formally fourth order,
+                     * smooth flows: no positivity fallback; mhd.cu k_mhd4_*) */
     double gamma;
     hc_limiter lim; /* as the Euler path: MC factors, WENO3 eps and linear weights */
     int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis; bc[2] = -1: z ghosts caller-filled */

@@ -603,6 +603,361 @@ __global__ void k_mhd_dt(MArgs a, double cfl, double* out, int stage) {
     }
 }
 
+// ============================================================ order 4 (space-time ADER)
+// The O2/O3 kernels keep the reference's ADER structure (face state + the zone's tau/2), second
+// order in time. Order 4 (smooth flows; no positivity fallback):
+//   k_mhd4_predict  one CTA per ring zone, one thread per space-time node (4 x 4 x 4 Gauss-
+//                   Legendre points x 4 Gauss times): the degree-3 polynomial of the 8 cell
+//                   variables (fluid averages, fourth-order cell B from k_mhd_cellb; WENO-AO pure
+//                   terms, central mixed terms, as ader4.cu), four Picard iterations of the local
+//                   space-time predictor with the MHD flux; outputs the states at the 2 x 2 Gauss
+//                   points of the 6 faces and at the 2 Gauss points along the 12 zone edges, each
+//                   at the 2 Gauss times ([96][8][N] in `states`: faces 0..47, edges 48..95)
+//   k_mhd4_flux<A>  HLL at the 2 x 2 x 2 space-time Gauss points of each face (single-valued
+//                   normal B with the energy shift of k_mhd_flux), averaged
+//   k_mhd4_emf<C>   the 2D HLL EMF of k_mhd_emf at the 2 x 2 points along the edge and in time,
+//                   averaged: the edge- and time-averaged EMF of constrained transport
+// then k_mhd_update / k_mhd_dt as at O2/O3 (div B stays at round-off).
+struct MhdBasis {
+    double xi[4], D[4][4], IT[4][4], LF[2][4], LG[2][4], LT[2][4];
+};
+__constant__ MhdBasis c_mb;
+constexpr int M4_NT = 256, M4_OUT = 96, M4_NCOEF = 23;
+
+__device__ __forceinline__ void psi4m(double s, double* p) {
+    const double s2 = s * s;
+    p[0] = s;
+    p[1] = s2 - 1.0 / 12.0;
+    p[2] = s * (s2 - 3.0 / 20.0);
+    p[3] = s2 * s2 - (3.0 / 14.0) * s2 + 3.0 / 560.0;
+}
+
+__global__ void __launch_bounds__(M4_NT) k_mhd4_predict(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    __shared__ double coef[NM][M4_NCOEF];
+    extern __shared__ double smm[];
+    double* Q = smm;                  // [256][8]
+    double* FL = Q + M4_NT * NM;      // [3][256][8]
+    double* DV = FL + 3 * M4_NT * NM; // [256][8]
+    const int rx = b.n[0] + 2, ry = b.n[1] + 2;
+    const int zr = blockIdx.x;
+    const int i = zr % rx - 1 + b.gh, j = (zr / rx) % ry - 1 + b.gh,
+              k = zr / (rx * ry) - 1 + a.zlo + b.gh;
+    const size_t o = at(b, k, j, i);
+    const long long st3[3] = {(long long)stride(b, 0), (long long)stride(b, 1), (long long)stride(b, 2)};
+    const size_t N = b.N;
+    const int t = threadIdx.x;
+    const double dt = a.ctl->dt;
+    auto Wv = [&](int q, long long off) { return wvar(a, q, size_t((long long)o + off)); };
+    if (t < 24) {
+        const int q = t / 3, ax = t % 3;
+        double m[4];
+        Fault f;
+        f.clear();
+        weno_ao<0>(Wv(q, -2 * st3[ax]), Wv(q, -st3[ax]), Wv(q, 0), Wv(q, st3[ax]), Wv(q, 2 * st3[ax]),
+                   a.lim, m, f);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
+        if (ax == 0) coef[q][0] = Wv(q, 0);
+    } else if (t < 24 + NM * 10) {
+        const int q = (t - 24) / 10, term = (t - 24) % 10;
+        auto val = [&](int p1, int s1, int p2, int s2) { return Wv(q, s1 * st3[p1] + s2 * st3[p2]); };
+        double v;
+        if (term < 3) {
+            const int p1 = term, r = (term + 1) % 3;
+            v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) - (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
+        } else if (term < 9) {
+            const int pair = (term - 3) / 2, sw = (term - 3) % 2;
+            const int a1 = pair, a2 = (pair + 1) % 3;
+            const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
+            auto d2 = [&](int sg) { return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg); };
+            v = 0.25 * (d2(1) - d2(-1));
+        } else {
+            double acc = 0.0;
+            for (int cc = -1; cc <= 1; cc += 2)
+                for (int bb = -1; bb <= 1; bb += 2)
+                    for (int aa = -1; aa <= 1; aa += 2)
+                        acc += double(aa * bb * cc) * Wv(q, aa * st3[0] + bb * st3[1] + cc * st3[2]);
+            v = 0.125 * acc;
+        }
+        coef[q][13 + term] = v;
+    }
+    __syncthreads();
+    const int ni = t & 3, nj = (t >> 2) & 3, nk = (t >> 4) & 3, nm = t >> 6;
+    double p0[NM];
+    {
+        double px[4], py[4], pz[4];
+        psi4m(c_mb.xi[ni], px);
+        psi4m(c_mb.xi[nj], py);
+        psi4m(c_mb.xi[nk], pz);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            const double* c = coef[q];
+            double v = c[0];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) v += c[1 + l] * px[l] + c[5 + l] * py[l] + c[9 + l] * pz[l];
+            v += c[13] * px[0] * py[0] + c[14] * py[0] * pz[0] + c[15] * pz[0] * px[0];
+            v += c[16] * px[1] * py[0] + c[17] * px[0] * py[1];
+            v += c[18] * py[1] * pz[0] + c[19] * py[0] * pz[1];
+            v += c[20] * pz[1] * px[0] + c[21] * pz[0] * px[1];
+            v += c[22] * px[0] * py[0] * pz[0];
+            p0[q] = v;
+            Q[t * NM + q] = v;
+        }
+    }
+    __syncthreads();
+    Fault f;
+    f.clear();
+    for (int it = 0; it < 4; ++it) {
+        {
+            double u[NM], fl[NM];
+#pragma unroll
+            for (int q = 0; q < NM; ++q) u[q] = Q[t * NM + q];
+            const MPrim pr = mhd_prim<0>(u, a.gamma, f);
+            mhd_flux<0>(u, pr, fl);
+#pragma unroll
+            for (int q = 0; q < NM; ++q) FL[(0 * M4_NT + t) * NM + q] = fl[q];
+            mhd_flux<1>(u, pr, fl);
+#pragma unroll
+            for (int q = 0; q < NM; ++q) FL[(1 * M4_NT + t) * NM + q] = fl[q];
+            mhd_flux<2>(u, pr, fl);
+#pragma unroll
+            for (int q = 0; q < NM; ++q) FL[(2 * M4_NT + t) * NM + q] = fl[q];
+        }
+        __syncthreads();
+        {
+            double dv[NM];
+#pragma unroll
+            for (int q = 0; q < NM; ++q) dv[q] = 0.0;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
+                const double wx = c_mb.D[ni][l] * a.id[0], wy = c_mb.D[nj][l] * a.id[1],
+                             wz = c_mb.D[nk][l] * a.id[2];
+#pragma unroll
+                for (int q = 0; q < NM; ++q)
+                    dv[q] += wx * FL[(0 * M4_NT + tx) * NM + q] + wy * FL[(1 * M4_NT + ty) * NM + q] +
+                             wz * FL[(2 * M4_NT + tz) * NM + q];
+            }
+#pragma unroll
+            for (int q = 0; q < NM; ++q) DV[t * NM + q] = dv[q];
+        }
+        __syncthreads();
+        {
+            double qn[NM];
+#pragma unroll
+            for (int q = 0; q < NM; ++q) qn[q] = p0[q];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int tl = (t & 63) | (l << 6);
+                const double w = dt * c_mb.IT[nm][l];
+#pragma unroll
+                for (int q = 0; q < NM; ++q) qn[q] -= w * DV[tl * NM + q];
+            }
+#pragma unroll
+            for (int q = 0; q < NM; ++q) Q[t * NM + q] = qn[q];
+        }
+        __syncthreads();
+    }
+    if (f.code) record_fault(a.eb, ST_PREDICT, f, i - b.gh, j - b.gh, k - b.gh, 0);
+    // outputs: (1) time -> the 2 Gauss times, T[tg][node][8] (in FL)
+    double* T = FL;
+    if (t < 128) {
+        const int tg = t >> 6, node = t & 63;
+        double v[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double w = c_mb.LT[tg][m];
+#pragma unroll
+            for (int q = 0; q < NM; ++q) v[q] += w * Q[((m << 6) | node) * NM + q];
+        }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) T[t * NM + q] = v[q];
+    }
+    __syncthreads();
+    // (2) the points: faces e < 48: ((face * 4 + g1 * 2 + g2) * 2 + tg), face = 2A + side;
+    //     edges e - 48 < 48: ((C * 4 + 2 lb + la) * 2 + g) * 2 + tg (corner la, lb at +-1/2 in
+    //     the (C+1, C+2) plane, la = 0: +1/2; g along C)
+    if (t < M4_OUT) {
+        double w[3][4];
+        int tg;
+        if (t < 48) {
+            tg = t & 1;
+            const int g = (t >> 1) & 3, face = t >> 3, A = face >> 1, side = face & 1;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                w[A][l] = c_mb.LF[side][l];
+                w[(A + 1) % 3][l] = c_mb.LG[g >> 1][l];
+                w[(A + 2) % 3][l] = c_mb.LG[g & 1][l];
+            }
+        } else {
+            const int e = t - 48;
+            tg = e & 1;
+            const int g = (e >> 1) & 1, corner = (e >> 2) & 3, C = e >> 4;
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                w[C][l] = c_mb.LG[g][l];
+                w[(C + 1) % 3][l] = c_mb.LF[corner & 1][l];
+                w[(C + 2) % 3][l] = c_mb.LF[corner >> 1][l];
+            }
+        }
+        double v[NM];
+#pragma unroll
+        for (int q = 0; q < NM; ++q) v[q] = 0.0;
+        for (int kk = 0; kk < 4; ++kk)
+            for (int jj = 0; jj < 4; ++jj)
+                for (int ii = 0; ii < 4; ++ii) {
+                    const double ww = w[2][kk] * w[1][jj] * w[0][ii];
+                    const int node = (kk * 4 + jj) * 4 + ii;
+#pragma unroll
+                    for (int q = 0; q < NM; ++q) v[q] += ww * T[((tg << 6) | node) * NM + q];
+                }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) __stcs(a.states + (size_t(t) * NM + q) * N + o, v[q]);
+    }
+}
+
+template <int A>
+__global__ void __launch_bounds__(128) k_mhd4_flux(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int B1 = (A + 1) % 3, B2 = (A + 2) % 3;
+    const int ex = b.n[0] + (A == 0), ey = b.n[1] + (A == 1), ez = a.zhi - a.zlo + (A == 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= size_t(ex) * ey * ez) return;
+    int c[3];
+    c[0] = int(r % ex);
+    c[1] = int((r / ex) % ey);
+    c[2] = a.zlo + int(r / (size_t(ex) * ey));
+    const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
+    const size_t ol = o - stride(b, A), N = b.N;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    Fault f;
+    f.clear();
+    for (int p = 0; p < 8; ++p) {  // (g1, g2, tg) of the face
+        double ul[NM], ur[NM], f5[5];
+        const int el = (2 * A) * 8 + p, er = (2 * A + 1) * 8 + p;
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            ul[q] = __ldg(a.states + (size_t(el) * NM + q) * N + ol);
+            ur[q] = __ldg(a.states + (size_t(er) * NM + q) * N + o);
+        }
+        const double bn = 0.5 * (ul[5 + A] + ur[5 + A]);
+        ul[4] = ul[4] + 0.5 * (bn * bn - ul[5 + A] * ul[5 + A]);
+        ur[4] = ur[4] + 0.5 * (bn * bn - ur[5 + A] * ur[5 + A]);
+        ul[5 + A] = bn;
+        ur[5 + A] = bn;
+        mhd_hll<A>(ul, ur, a.gamma, f5, f);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) acc[q] += 0.125 * f5[q];
+    }
+    if (f.code) record_fault(a.eb, ST_FLUX, f, c[A], c[B1], c[B2], A);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) a.flux[(size_t(A) * 5 + q) * N + o] = acc[q];
+}
+
+template <int C>
+__global__ void __launch_bounds__(128) k_mhd4_emf(MArgs a) {
+    if (a.ctl->done) return;
+    const Box& b = a.b;
+    constexpr int AA = (C + 1) % 3, BB = (C + 2) % 3;
+    const int ex = b.n[0] + (C != 0), ey = b.n[1] + (C != 1), ez = a.zhi - a.zlo + (C != 2);
+    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    if (r >= size_t(ex) * ey * ez) return;
+    int c[3];
+    c[0] = int(r % ex);
+    c[1] = int((r / ex) % ey);
+    c[2] = a.zlo + int(r / (size_t(ex) * ey));
+    const size_t o = at(b, c[2] + b.gh, c[1] + b.gh, c[0] + b.gh);
+    const size_t sa = stride(b, AA), sb = stride(b, BB), N = b.N;
+    Fault f;
+    f.clear();
+    double E = 0.0;
+    for (int p = 0; p < 4; ++p) {  // (g along C, tg)
+        double ec[2][2], ba[2][2], bb[2][2];
+        double apa = 0.0, ama = 0.0, apb = 0.0, amb = 0.0;
+#pragma unroll
+        for (int lb = 0; lb < 2; ++lb)
+#pragma unroll
+            for (int la = 0; la < 2; ++la) {
+                const size_t z = o - (la == 0 ? sa : 0) - (lb == 0 ? sb : 0);
+                const int e = 48 + (C * 4 + 2 * lb + la) * 4 + p;
+                double u[NM];
+#pragma unroll
+                for (int q = 0; q < NM; ++q) u[q] = __ldg(a.states + (size_t(e) * NM + q) * N + z);
+                const MPrim pr = mhd_prim(u, a.gamma, f);
+                ec[la][lb] = pr.u[BB] * u[5 + AA] - pr.u[AA] * u[5 + BB];
+                ba[la][lb] = u[5 + AA];
+                bb[la][lb] = u[5 + BB];
+                const double cfa = fast_speed<AA>(u, pr, a.gamma);
+                const double cfb = fast_speed<BB>(u, pr, a.gamma);
+                apa = smax(apa, pr.u[AA] + cfa);
+                ama = smax(ama, cfa - pr.u[AA]);
+                apb = smax(apb, pr.u[BB] + cfb);
+                amb = smax(amb, cfb - pr.u[BB]);
+            }
+        const double ia = 1.0 / (apa + ama), ib = 1.0 / (apb + amb);
+        const double wa[2] = {apa * ia, ama * ia}, wb[2] = {apb * ib, amb * ib};
+        const double e = wa[0] * wb[0] * ec[0][0] + wa[1] * wb[0] * ec[1][0] +
+                         wa[0] * wb[1] * ec[0][1] + wa[1] * wb[1] * ec[1][1];
+        const double jb = 0.5 * (bb[1][0] + bb[1][1]) - 0.5 * (bb[0][0] + bb[0][1]);
+        const double ja = 0.5 * (ba[0][1] + ba[1][1]) - 0.5 * (ba[0][0] + ba[1][0]);
+        E += 0.25 * (e + apa * ama * ia * jb - apb * amb * ib * ja);
+    }
+    if (f.code) record_fault(a.eb, ST_FLUX, f, c[0], c[1], c[2], 3 + C);
+    a.emf[size_t(C) * N + o] = E;
+}
+
+MhdBasis make_mhd_basis() {
+    MhdBasis bs;
+    const double gl[4] = {-0.8611363115940526, -0.3399810435848563, 0.3399810435848563,
+                          0.8611363115940526};
+    const double gw[4] = {0.3478548451374538, 0.6521451548625461, 0.6521451548625461,
+                          0.3478548451374538};
+    double tau[4];
+    for (int l = 0; l < 4; ++l) {
+        bs.xi[l] = 0.5 * gl[l];
+        tau[l] = 0.5 * (gl[l] + 1.0);
+    }
+    auto lag = [](const double* n, int l, double x) {
+        double v = 1.0;
+        for (int m = 0; m < 4; ++m)
+            if (m != l) v *= (x - n[m]) / (n[l] - n[m]);
+        return v;
+    };
+    auto dlag = [](const double* n, int l, double x) {
+        double sum = 0.0;
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk == l) continue;
+            double v = 1.0 / (n[l] - n[kk]);
+            for (int m = 0; m < 4; ++m)
+                if (m != l && m != kk) v *= (x - n[m]) / (n[l] - n[m]);
+            sum += v;
+        }
+        return sum;
+    };
+    const double g2 = 0.5 / std::sqrt(3.0);
+    for (int r = 0; r < 4; ++r)
+        for (int l = 0; l < 4; ++l) {
+            bs.D[r][l] = dlag(bs.xi, l, bs.xi[r]);
+            double sum = 0.0;
+            for (int g = 0; g < 4; ++g) sum += 0.5 * tau[r] * gw[g] * lag(tau, l, 0.5 * tau[r] * (gl[g] + 1.0));
+            bs.IT[r][l] = sum;
+        }
+    for (int l = 0; l < 4; ++l) {
+        bs.LF[0][l] = lag(bs.xi, l, 0.5);
+        bs.LF[1][l] = lag(bs.xi, l, -0.5);
+        bs.LG[0][l] = lag(bs.xi, l, -g2);
+        bs.LG[1][l] = lag(bs.xi, l, g2);
+        bs.LT[0][l] = lag(tau, l, 0.5 - g2);
+        bs.LT[1][l] = lag(tau, l, 0.5 + g2);
+    }
+    return bs;
+}
+
 __global__ void k_mhd_divb(MArgs a, double* out) {
     const Box& b = a.b;
     const size_t cnt = size_t(b.n[0]) * b.n[1] * b.n[2];
@@ -711,7 +1066,37 @@ int launch_ghosts(hc_mhd* m) {
 
 // the front kernels of a step for the active z range [zlo, zhi): cell B, predictor, face
 // fluxes and edge EMFs of every face/edge the update of those zones reads
+constexpr size_t kMhd4Smem = sizeof(double) * 5 * M4_NT * NM;
+
+int launch_front4(hc_mhd* m, int zlo, int zhi) {
+    MArgs a = margs(m);
+    a.zlo = zlo;
+    a.zhi = zhi;
+    const Box& b = m->b;
+    const int nz = zhi - zlo;
+    const size_t cb = size_t(b.P) * b.Q * (nz + 6);
+    const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (nz + 2);
+    k_mhd_cellb<true><<<blocks(cb, 256), 256, 0, m->st>>>(a);
+    k_mhd4_predict<<<unsigned(ring), M4_NT, kMhd4Smem, m->st>>>(a);
+    const size_t fx = size_t(b.n[0] + 1) * b.n[1] * nz;
+    const size_t fy = size_t(b.n[0]) * (b.n[1] + 1) * nz;
+    const size_t fz = size_t(b.n[0]) * b.n[1] * (nz + 1);
+    const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (nz + 1);
+    const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (nz + 1);
+    const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * nz;
+    k_mhd4_flux<0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+    k_mhd4_flux<1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+    k_mhd4_flux<2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    k_mhd4_emf<0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
+    k_mhd4_emf<1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
+    k_mhd4_emf<2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
+    m->launches += 8;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd order-4 step launch");
+}
+
 int launch_front(hc_mhd* m, int zlo, int zhi) {
+    if (m->p.order == 4) return launch_front4(m, zlo, zhi);
     MArgs a = margs(m);
     a.zlo = zlo;
     a.zhi = zhi;
@@ -754,7 +1139,7 @@ int launch_front(hc_mhd* m, int zlo, int zhi) {
 int launch_finish(hc_mhd* m) {
     MArgs a = margs(m);
     const Box& b = m->b;
-    const bool o3 = m->p.order == 3;
+    const bool o3 = m->p.order >= 3;
     const size_t up = size_t(b.n[0] + 1) * (b.n[1] + 1) * (b.n[2] + 1);
     k_mhd_update<<<blocks(up, 256), 256, 0, m->st>>>(a);
     const size_t act = size_t(b.n[0]) * b.n[1] * b.n[2];
@@ -794,10 +1179,14 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
         set_error(HC_INVALID, "null argument");
         return HC_INVALID;
     }
-    int rc = validate_geom(g, p->order);
+    if (p->order < 2 || p->order > 4) {
+        set_error(HC_INVALID, "mhd: order must be 2, 3 or 4");
+        return HC_INVALID;
+    }
+    int rc = validate_geom(g, p->order == 4 ? 3 : p->order);  // (order 4: the same stencils)
     if (rc) return rc;
-    if (g->ghost < (p->order == 3 ? 4 : 2)) {  // WENO radius 2 + ring + B cell average
-        set_error(HC_INVALID, "mhd: order 3 needs a ghost width of at least 4");
+    if (g->ghost < (p->order >= 3 ? 4 : 2)) {  // WENO radius 2 + ring + B cell average
+        set_error(HC_INVALID, "mhd: orders 3 and 4 need a ghost width of at least 4");
         return HC_INVALID;
     }
     for (int d = 0; d < 3; ++d)
@@ -823,7 +1212,8 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
     b.N = size_t(b.P) * b.Q * b.R;
     cudaError_t e = cudaSetDevice(p->device);
     if (e == cudaSuccess) e = cudaMalloc(&m->s, sizeof(double) * NM * b.N);
-    if (e == cudaSuccess) e = cudaMalloc(&m->states, sizeof(double) * size_t(NST) * NM * b.N);
+    if (e == cudaSuccess)
+        e = cudaMalloc(&m->states, sizeof(double) * size_t(p->order == 4 ? M4_OUT : NST) * NM * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->ht, sizeof(double) * NM * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->flux, sizeof(double) * 15 * b.N);
     if (e == cudaSuccess) e = cudaMalloc(&m->emf, sizeof(double) * 3 * b.N);
@@ -842,6 +1232,13 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
         StepCtl c{};
         c.acc = 1.0e32;
         e = cudaMemcpy(m->ctl, &c, sizeof c, cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && p->order == 4) {
+        MhdBasis bs = make_mhd_basis();
+        e = cudaMemcpyToSymbol(c_mb, &bs, sizeof bs);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_mhd4_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kMhd4Smem));
     }
     if (e != cudaSuccess) {
         hc_mhd_destroy(m);
@@ -927,7 +1324,7 @@ int hc_mhd_cfl_dt(hc_mhd* m, double cfl, double* dt) {
     HC_CUDA(cudaMemcpyAsync(m->scratch, &seed, sizeof seed, cudaMemcpyHostToDevice, m->st));
     HC_CUDA(cudaMemsetAsync(m->eb, 0, sizeof(ErrBlock), m->st));
     const size_t act = size_t(m->b.n[0]) * m->b.n[1] * m->b.n[2];
-    if (m->p.order == 3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, cfl, m->scratch, ST_DT);
+    if (m->p.order >= 3) k_mhd_dt<true><<<blocks(act, 256), 256, 0, m->st>>>(a, cfl, m->scratch, ST_DT);
     else k_mhd_dt<false><<<blocks(act, 256), 256, 0, m->st>>>(a, cfl, m->scratch, ST_DT);
     m->launches += 1;
     ErrBlock eb;

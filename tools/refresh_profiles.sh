@@ -7,7 +7,7 @@
 set -e
 mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_o3_256.json 2> gpurun_out/bench.err
-ncu --set full --import-source on --clock-control none -k regex:seam_ -s 9 -c 3 \
+ncu --set full --import-source on --clock-control none -k regex:seam_ -s 8 -c 2 \
     -o /tmp/fused_o3_256_fma -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     --only-timed > gpurun_out/ncu_fma.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:fused_ader -s 3 -c 1 \

@@ -33,6 +33,10 @@ extern "C" {
 
 #define HC_MHD_NVAR 8
 
+/* face Riemann solver of the fluid fluxes (the edge EMFs are the 2D HLL solver either way) */
+#define HC_MHD_HLL 0  /* HLL with Davis speeds (fast magnetosonic) */
+#define HC_MHD_HLLD 1 /* HLLD, Miyoshi & Kusano 2005: fast, Alfven and entropy waves */
+
 typedef struct {
     int order;      /* 2 (MC slopes) or 3 (WENO3 + cross terms) in the reference's ADER
                      * structure (second order in time), or 4: the local space-time predictor with
@@ -42,6 +46,7 @@ typedef struct {
     hc_limiter lim; /* as the Euler path: MC factors, WENO3 eps and linear weights */
     int bc[3];      /* HC_PERIODIC / HC_OUTFLOW per axis; bc[2] = -1: z ghosts caller-filled */
     int device;
+    int face_solver; /* HC_MHD_HLL (0) or HC_MHD_HLLD */
 } hc_mhd_params;
 
 typedef struct hc_mhd hc_mhd;
@@ -53,8 +58,8 @@ int hc_mhd_upload(hc_mhd* m, const double* host_state);
 int hc_mhd_download(hc_mhd* m, double* host_state);
 /* t, dt of the next step, cfl, t_final (<= 0: fixed step count) */
 int hc_mhd_set_time(hc_mhd* m, double t, double dt, double cfl, double t_final);
-/* Enqueue n ADER-CT steps: ghost fill, reconstruction + predictor, face fluxes (HLL, 3
- * axes), edge EMFs (2D HLL, 3 axes), conservative + CT update, CFL min, dt hand-off. */
+/* Enqueue n ADER-CT steps: ghost fill, reconstruction + predictor, face fluxes (HLL or HLLD,
+ * 3 axes), edge EMFs (2D HLL, 3 axes), conservative + CT update, CFL min, dt hand-off. */
 int hc_mhd_step(hc_mhd* m, int n);
 int hc_mhd_sync(hc_mhd* m, double* t, double* dt, long* steps_done);
 /* CFL time step of the current device state: cfl / max(sum_a (|v_a| + c_f,a) / d_a) */

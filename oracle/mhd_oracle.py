@@ -46,8 +46,8 @@ class Geom:
 
 class Params:
     def __init__(self, order, gamma=5.0 / 3.0, cfac_rho=2.0, cfac_other=1.5, eps=1e-12,
-                 w=(0.25, 0.5, 0.25), bc=(PERIODIC, PERIODIC, PERIODIC)):
-        self.order, self.gamma = order, gamma
+                 w=(0.25, 0.5, 0.25), bc=(PERIODIC, PERIODIC, PERIODIC), face_solver=0):
+        self.order, self.gamma, self.face_solver = order, gamma, face_solver
         self.cfac_rho, self.cfac_other, self.eps, self.w = cfac_rho, cfac_other, eps, w
         self.bc = bc
 
@@ -325,6 +325,84 @@ def predict(s, g: Geom, par: Params, dt):
     return m
 
 
+def _hlld_star(u, q, s, d, sm, pts, pt, bn, A):
+    """mhd.cu hlld_star: the star state of one side (rho, v[3], b[3], e)"""
+    T1, T2 = (A + 1) % 3, (A + 2) % 3
+    rho = d / (s - sm)
+    den = d * (s - sm) - bn * bn
+    degen = np.abs(den) < 1e-8 * pts
+    iden = 1.0 / den
+    fv = bn * (sm - q[1][A]) * iden
+    fb = (d * (s - q[1][A]) - bn * bn) * iden
+    v, b = [None] * 3, [None] * 3
+    v[A], b[A] = sm, bn
+    for T in (T1, T2):
+        v[T] = np.where(degen, q[1][T], q[1][T] - u[5 + T] * fv)
+        b[T] = np.where(degen, u[5 + T], u[5 + T] * fb)
+    vb = q[1][0] * u[5] + q[1][1] * u[6] + q[1][2] * u[7]
+    vbs = v[0] * b[0] + v[1] * b[1] + v[2] * b[2]
+    e = ((s - q[1][A]) * u[4] - pt * q[1][A] + pts * sm + bn * (vb - vbs)) / (s - sm)
+    return rho, v, b, e
+
+
+def hlld(ul, ur, ql, qr, cl, cr, A):
+    """mhd.cu mhd_hlld<A> (Miyoshi & Kusano 2005), vectorised over faces: fluid fluxes"""
+    T1, T2 = (A + 1) % 3, (A + 2) % 3
+    with np.errstate(divide="ignore", invalid="ignore"):
+        bn = ul[5 + A]
+        cm = smax(cl, cr)
+        sl = smin(ql[1][A], qr[1][A]) - cm
+        sr = smax(ql[1][A], qr[1][A]) + cm
+        fl, fr = mhd_flux(ul, ql, A), mhd_flux(ur, qr, A)
+        ptl = ql[2] + 0.5 * ql[3]
+        ptr = qr[2] + 0.5 * qr[3]
+        dl = (sl - ql[1][A]) * ul[0]
+        dr = (sr - qr[1][A]) * ur[0]
+        idn = 1.0 / (dr - dl)
+        sm = (dr * qr[1][A] - dl * ql[1][A] - ptr + ptl) * idn
+        pts = (dr * ptl - dl * ptr + dl * dr * (qr[1][A] - ql[1][A])) * idn
+        L = _hlld_star(ul, ql, sl, dl, sm, pts, ptl, bn, A)
+        R = _hlld_star(ur, qr, sr, dr, sm, pts, ptr, bn, A)
+        rl, rr = np.sqrt(L[0]), np.sqrt(R[0])
+        sal = sm - np.abs(bn) / rl
+        sar = sm + np.abs(bn) / rr
+        left = sm >= 0.0
+
+        def pick(a, b):
+            return np.where(left, a, b)
+        Srho, Se = pick(L[0], R[0]), pick(L[3], R[3])
+        Sv = [pick(L[1][d], R[1][d]) for d in range(3)]
+        Sb = [pick(L[2][d], R[2][d]) for d in range(3)]
+        u = [pick(ul[q], ur[q]) for q in range(5)]
+        f = [pick(fl[q], fr[q]) for q in range(5)]
+        s = pick(sl, sr)
+        fs = [None] * 5
+        fs[0] = f[0] + s * (Srho - u[0])
+        for d in range(3):
+            fs[1 + d] = f[1 + d] + s * (Srho * Sv[d] - u[1 + d])
+        fs[4] = f[4] + s * (Se - u[4])
+        # double-star states
+        degen = 0.5 * bn * bn < 1e-8 * pts
+        sg = np.where(bn > 0.0, 1.0, -1.0)
+        inv = 1.0 / (rl + rr)
+        u2, b2 = [None] * 3, [None] * 3
+        u2[A], b2[A] = sm, bn
+        for T in (T1, T2):
+            u2[T] = (rl * L[1][T] + rr * R[1][T] + (R[2][T] - L[2][T]) * sg) * inv
+            b2[T] = (rl * R[2][T] + rr * L[2][T] + rl * rr * (R[1][T] - L[1][T]) * sg) * inv
+        vb2 = u2[0] * b2[0] + u2[1] * b2[1] + u2[2] * b2[2]
+        vbs = Sv[0] * Sb[0] + Sv[1] * Sb[1] + Sv[2] * Sb[2]
+        e2 = np.where(left, Se - rl * (vbs - vb2) * sg, Se + rr * (vbs - vb2) * sg)
+        u2 = [np.where(degen, Sv[d], u2[d]) for d in range(3)]
+        e2 = np.where(degen, Se, e2)
+        sa = pick(sal, sar)
+        dstar = (left & (sal <= 0.0)) | (~left & (sar >= 0.0))
+        for d in range(3):
+            fs[1 + d] = np.where(dstar, fs[1 + d] + sa * (Srho * u2[d] - Srho * Sv[d]), fs[1 + d])
+        fs[4] = np.where(dstar, fs[4] + sa * (e2 - Se), fs[4])
+        return [np.where(sl >= 0.0, fl[q], np.where(sr <= 0.0, fr[q], fs[q])) for q in range(5)]
+
+
 def face_fluxes(m, g: Geom, par: Params, A):
     """k_mhd_flux<A>: fluid fluxes of the A faces, stored at the zone right of the face;
     valid at faces 0..n_A, active transverse."""
@@ -346,6 +424,12 @@ def face_fluxes(m, g: Geom, par: Params, A):
     ur = [x[sel] for x in ur]
     ql, qr = prim(ul, par.gamma), prim(ur, par.gamma)
     cl, cr = fast_speed(ul, ql, par.gamma, A), fast_speed(ur, qr, par.gamma, A)
+    if par.face_solver == 1:
+        out = np.zeros((5,) + g.shape)
+        f5 = hlld(ul, ur, ql, qr, cl, cr, A)
+        for q in range(5):
+            out[q][sel] = f5[q]
+        return out
     sl = smin(ql[1][A] - cl, qr[1][A] - cr)
     sr = smax(ql[1][A] + cl, qr[1][A] + cr)
     fl, fr = mhd_flux(ul, ql, A), mhd_flux(ur, qr, A)

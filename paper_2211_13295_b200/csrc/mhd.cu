@@ -11,8 +11,9 @@
 //   k_mhd_predict<O3> ring zones: reconstruction of the 8 variables, the 18 states the
 //                     face and edge solvers read (6 face averages, 12 edge midpoints, without
 //                     the temporal part), ADER predictor; writes those states and tau/2
-//   k_mhd_flux<A>     HLL (Davis speeds with the fast magnetosonic speed) on the A faces;
-//                     the normal field is the mean of the two reconstructed values
+//   k_mhd_flux<A>     HLL (Davis speeds with the fast magnetosonic speed) or HLLD (Miyoshi &
+//                     Kusano 2005; hc_mhd_params.face_solver) on the A faces; the normal
+//                     field is the mean of the two reconstructed values
 //   k_mhd_emf<C>      edge EMF E_C from the four zones around the edge: the two-dimensional
 //                     HLL Riemann solver (UCT-HLL, Londrillo & Del Zanna 2004; the HLL limit
 //                     of Balsara's MHLLE 2010): HLL-weighted corner EMFs plus the upwind
@@ -150,6 +151,133 @@ __device__ __forceinline__ void mhd_hll(const double* ul, const double* ur, doub
         for (int q = 0; q < 5; ++q)
             f5[q] = (sr * fl[q] - sl * fr[q] + sl * sr * (ur[q] - ul[q])) * inv;
     }
+}
+
+// HLLD (Miyoshi & Kusano 2005, J. Comput. Phys. 208:315): five waves -- the fast pair
+// S_L, S_R (the HLL bounds above, Davis-Einfeldt form min/max(u) -/+ max(c_f)), the Alfven
+// pair S*_L = S_M - |B_n|/sqrt(rho*_L), S*_R = S_M + |B_n|/sqrt(rho*_R) and the entropy wave
+// S_M -- with the total pressure and the normal velocity constant across the Riemann fan.
+// Resolves isolated contacts, tangential and rotational discontinuities exactly (HLL
+// smears them). Fluid components only (the CT edges carry the field); the caller has made
+// the normal field single-valued. Degenerate cases as in Miyoshi & Kusano section 4
+// (S_M -> S_L,R with B_n^2 -> rho (S - u)^2: the tangential fields/velocities pass through
+// unchanged; B_n -> 0: the double-star states collapse onto the star states).
+struct HlldSide {
+    double rho, v[3], b[3], e;  // star state (v[A] = S_M, b[A] = B_n)
+};
+
+template <int A>
+__device__ __forceinline__ void hlld_star(const double* u, const MPrim& q, double s, double d,
+                                          double sm, double pts, double pt, double bn,
+                                          HlldSide& o) {
+    constexpr int T1 = (A + 1) % 3, T2 = (A + 2) % 3;
+    o.rho = d / (s - sm);  // d = rho (S - u)
+    const double den = d * (s - sm) - bn * bn;
+    o.v[A] = sm;
+    o.b[A] = bn;
+    if (fabs(den) < 1e-8 * pts) {
+        o.v[T1] = q.u[T1];
+        o.v[T2] = q.u[T2];
+        o.b[T1] = u[5 + T1];
+        o.b[T2] = u[5 + T2];
+    } else {
+        const double iden = 1.0 / den;
+        const double fv = bn * (sm - q.u[A]) * iden;
+        const double fb = (d * (s - q.u[A]) - bn * bn) * iden;
+        o.v[T1] = q.u[T1] - u[5 + T1] * fv;
+        o.v[T2] = q.u[T2] - u[5 + T2] * fv;
+        o.b[T1] = u[5 + T1] * fb;
+        o.b[T2] = u[5 + T2] * fb;
+    }
+    const double vb = q.u[0] * u[5] + q.u[1] * u[6] + q.u[2] * u[7];
+    const double vbs = o.v[0] * o.b[0] + o.v[1] * o.b[1] + o.v[2] * o.b[2];
+    o.e = ((s - q.u[A]) * u[4] - pt * q.u[A] + pts * sm + bn * (vb - vbs)) / (s - sm);
+}
+
+template <int A>
+__device__ __forceinline__ void mhd_hlld(const double* ul, const double* ur, double gamma,
+                                         double* f5, Fault& flt) {
+    constexpr int T1 = (A + 1) % 3, T2 = (A + 2) % 3;
+    MPrim ql = mhd_prim(ul, gamma, flt);
+    MPrim qr = mhd_prim(ur, gamma, flt);
+    const double bn = ul[5 + A];
+    const double cl = fast_speed<A>(ul, ql, gamma);
+    const double cr = fast_speed<A>(ur, qr, gamma);
+    const double cm = smax(cl, cr);
+    const double sl = smin(ql.u[A], qr.u[A]) - cm;
+    const double sr = smax(ql.u[A], qr.u[A]) + cm;
+    double fl[NM], fr[NM];
+    mhd_flux<A>(ul, ql, fl);
+    mhd_flux<A>(ur, qr, fr);
+    if (sl >= 0.0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) f5[q] = fl[q];
+        return;
+    }
+    if (sr <= 0.0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) f5[q] = fr[q];
+        return;
+    }
+    const double ptl = ql.p + 0.5 * ql.b2, ptr = qr.p + 0.5 * qr.b2;
+    const double dl = (sl - ql.u[A]) * ul[0], dr = (sr - qr.u[A]) * ur[0];
+    const double idn = 1.0 / (dr - dl);
+    const double sm = (dr * qr.u[A] - dl * ql.u[A] - ptr + ptl) * idn;
+    const double pts = (dr * ptl - dl * ptr + dl * dr * (qr.u[A] - ql.u[A])) * idn;
+    HlldSide L, R;
+    hlld_star<A>(ul, ql, sl, dl, sm, pts, ptl, bn, L);
+    hlld_star<A>(ur, qr, sr, dr, sm, pts, ptr, bn, R);
+    const double rl = sqrt(L.rho), rr = sqrt(R.rho);
+    const double sal = sm - fabs(bn) / rl, sar = sm + fabs(bn) / rr;
+    const bool left = sm >= 0.0;
+    const HlldSide& S = left ? L : R;
+    const double* u = left ? ul : ur;
+    const double* f = left ? fl : fr;
+    const double s = left ? sl : sr;
+    // star flux F* = F + S (U* - U)
+    double fs[5];
+    fs[0] = f[0] + s * (S.rho - u[0]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) fs[1 + d] = f[1 + d] + s * (S.rho * S.v[d] - u[1 + d]);
+    fs[4] = f[4] + s * (S.e - u[4]);
+    if ((left && sal <= 0.0) || (!left && sar >= 0.0)) {
+        // double-star region: F** = F* + S*_side (U** - U*)
+        double u2[3], e2;
+        if (0.5 * bn * bn < 1e-8 * pts) {
+            u2[0] = S.v[0];
+            u2[1] = S.v[1];
+            u2[2] = S.v[2];
+            e2 = S.e;
+        } else {
+            const double sg = bn > 0.0 ? 1.0 : -1.0;
+            const double inv = 1.0 / (rl + rr);
+            double b2[3];
+            u2[A] = sm;
+            b2[A] = bn;
+            u2[T1] = (rl * L.v[T1] + rr * R.v[T1] + (R.b[T1] - L.b[T1]) * sg) * inv;
+            u2[T2] = (rl * L.v[T2] + rr * R.v[T2] + (R.b[T2] - L.b[T2]) * sg) * inv;
+            b2[T1] = (rl * R.b[T1] + rr * L.b[T1] + rl * rr * (R.v[T1] - L.v[T1]) * sg) * inv;
+            b2[T2] = (rl * R.b[T2] + rr * L.b[T2] + rl * rr * (R.v[T2] - L.v[T2]) * sg) * inv;
+            const double vb2 = u2[0] * b2[0] + u2[1] * b2[1] + u2[2] * b2[2];
+            const double vbs = S.v[0] * S.b[0] + S.v[1] * S.b[1] + S.v[2] * S.b[2];
+            e2 = left ? S.e - rl * (vbs - vb2) * sg : S.e + rr * (vbs - vb2) * sg;
+        }
+        const double sa = left ? sal : sar;
+        // rho** = rho*: the mass flux is the star one
+#pragma unroll
+        for (int d = 0; d < 3; ++d) fs[1 + d] = fs[1 + d] + sa * (S.rho * u2[d] - S.rho * S.v[d]);
+        fs[4] = fs[4] + sa * (e2 - S.e);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) f5[q] = fs[q];
+}
+
+// the face solver of the step (hc_mhd_params.face_solver)
+template <int A, int S>
+__device__ __forceinline__ void mhd_face(const double* ul, const double* ur, double gamma,
+                                         double* f5, Fault& flt) {
+    if (S == HC_MHD_HLLD) mhd_hlld<A>(ul, ur, gamma, f5, flt);
+    else mhd_hll<A>(ul, ur, gamma, f5, flt);
 }
 
 // the six face states of a zone, (+x,-x,+y,-y,+z,-z) x 8 variables, in shared memory (one
@@ -402,7 +530,7 @@ __device__ __forceinline__ void positive_or_average(const MArgs& a, size_t o, do
     for (int q = 0; q < NM; ++q) u[q] = cellvar<false>(a, q, o);  // (mean B: see k_mhd_dt)
 }
 
-template <bool O3, int A>
+template <bool O3, int A, int S>
 __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
@@ -432,7 +560,7 @@ __global__ void __launch_bounds__(128) k_mhd_flux(MArgs a) {
     ur[5 + A] = bn;
     Fault f;
     f.clear();
-    mhd_hll<A>(ul, ur, a.gamma, f5, f);
+    mhd_face<A, S>(ul, ur, a.gamma, f5, f);
     if (f.code) record_fault(a.eb, ST_FLUX, f, c[A], c[B1], c[B2], A);
 #pragma unroll
     for (int q = 0; q < 5; ++q) a.flux[(size_t(A) * 5 + q) * b.N + o] = f5[q];
@@ -820,7 +948,7 @@ __global__ void __launch_bounds__(M4_NT) k_mhd4_predict(MArgs a) {
     }
 }
 
-template <int A>
+template <int A, int S>
 __global__ void __launch_bounds__(128) k_mhd4_flux(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
@@ -850,7 +978,7 @@ __global__ void __launch_bounds__(128) k_mhd4_flux(MArgs a) {
         ur[4] = ur[4] + 0.5 * (bn * bn - ur[5 + A] * ur[5 + A]);
         ul[5 + A] = bn;
         ur[5 + A] = bn;
-        mhd_hll<A>(ul, ur, a.gamma, f5, f);
+        mhd_face<A, S>(ul, ur, a.gamma, f5, f);
 #pragma unroll
         for (int q = 0; q < 5; ++q) acc[q] += 0.125 * f5[q];
     }
@@ -1084,15 +1212,34 @@ int launch_front4(hc_mhd* m, int zlo, int zhi) {
     const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (nz + 1);
     const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (nz + 1);
     const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * nz;
-    k_mhd4_flux<0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
-    k_mhd4_flux<1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
-    k_mhd4_flux<2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    if (m->p.face_solver == HC_MHD_HLLD) {
+        k_mhd4_flux<0, HC_MHD_HLLD><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd4_flux<1, HC_MHD_HLLD><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd4_flux<2, HC_MHD_HLLD><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    } else {
+        k_mhd4_flux<0, HC_MHD_HLL><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd4_flux<1, HC_MHD_HLL><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd4_flux<2, HC_MHD_HLL><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    }
     k_mhd4_emf<0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
     k_mhd4_emf<1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
     k_mhd4_emf<2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
     m->launches += 8;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "mhd order-4 step launch");
+}
+
+template <bool O3>
+void launch_faces(hc_mhd* m, const MArgs& a, size_t fx, size_t fy, size_t fz) {
+    if (m->p.face_solver == HC_MHD_HLLD) {
+        k_mhd_flux<O3, 0, HC_MHD_HLLD><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<O3, 1, HC_MHD_HLLD><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<O3, 2, HC_MHD_HLLD><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    } else {
+        k_mhd_flux<O3, 0, HC_MHD_HLL><<<blocks(fx, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<O3, 1, HC_MHD_HLL><<<blocks(fy, 128), 128, 0, m->st>>>(a);
+        k_mhd_flux<O3, 2, HC_MHD_HLL><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+    }
 }
 
 int launch_front(hc_mhd* m, int zlo, int zhi) {
@@ -1116,16 +1263,12 @@ int launch_front(hc_mhd* m, int zlo, int zhi) {
     const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (nz + 1);
     const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * nz;
     if (o3) {
-        k_mhd_flux<true, 0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
-        k_mhd_flux<true, 1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
-        k_mhd_flux<true, 2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+        launch_faces<true>(m, a, fx, fy, fz);
         k_mhd_emf<true, 0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
         k_mhd_emf<true, 1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
         k_mhd_emf<true, 2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
     } else {
-        k_mhd_flux<false, 0><<<blocks(fx, 128), 128, 0, m->st>>>(a);
-        k_mhd_flux<false, 1><<<blocks(fy, 128), 128, 0, m->st>>>(a);
-        k_mhd_flux<false, 2><<<blocks(fz, 128), 128, 0, m->st>>>(a);
+        launch_faces<false>(m, a, fx, fy, fz);
         k_mhd_emf<false, 0><<<blocks(ex, 128), 128, 0, m->st>>>(a);
         k_mhd_emf<false, 1><<<blocks(ey, 128), 128, 0, m->st>>>(a);
         k_mhd_emf<false, 2><<<blocks(ez, 128), 128, 0, m->st>>>(a);
@@ -1181,6 +1324,10 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
     }
     if (p->order < 2 || p->order > 4) {
         set_error(HC_INVALID, "mhd: order must be 2, 3 or 4");
+        return HC_INVALID;
+    }
+    if (p->face_solver != HC_MHD_HLL && p->face_solver != HC_MHD_HLLD) {
+        set_error(HC_INVALID, "mhd: face_solver must be HC_MHD_HLL or HC_MHD_HLLD");
         return HC_INVALID;
     }
     int rc = validate_geom(g, p->order == 4 ? 3 : p->order);  // (order 4: the same stencils)

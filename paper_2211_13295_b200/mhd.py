@@ -29,12 +29,16 @@ PERIODIC, OUTFLOW = hydro.PERIODIC, hydro.OUTFLOW
 
 class MhdParams(C.Structure):
     _fields_ = [("order", C.c_int), ("gamma", C.c_double), ("lim", Limiter),
-                ("bc", C.c_int * 3), ("device", C.c_int)]
+                ("bc", C.c_int * 3), ("device", C.c_int), ("face_solver", C.c_int)]
 
 
-def make_params(order, gamma=5.0 / 3.0, bc=(PERIODIC,) * 3, device=0, limiter=None):
+HLL, HLLD = 0, 1  # HC_MHD_HLL / HC_MHD_HLLD: face solver of the fluid fluxes
+
+
+def make_params(order, gamma=5.0 / 3.0, bc=(PERIODIC,) * 3, device=0, limiter=None,
+                face_solver=HLL):
     p = MhdParams()
-    p.order, p.gamma, p.device = order, gamma, device
+    p.order, p.gamma, p.device, p.face_solver = order, gamma, device, face_solver
     p.lim = limiter or default_limiter()
     for d in range(3):
         p.bc[d] = bc[d]

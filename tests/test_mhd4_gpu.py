@@ -16,10 +16,10 @@ def active(s, g):
     return s[:, gh:gh + g.nz, gh:gh + g.ny, gh:gh + g.nx]
 
 
-def _vortex(n, order, t_final=1.0):
+def _vortex(n, order, t_final=1.0, solver=mhd.HLL):
     g = mhd.make_geometry(n, n, 4, order, (-5, -5, -5 * 4 / n), (5, 5, 5 * 4 / n))
     s0 = mhd.mhd_vortex(g, order)
-    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st = mhd.MhdStepper(g, mhd.make_params(order, face_solver=solver))
     st.upload(s0)
     t, dt, done = st.run(0.4, t_final=t_final)
     s = st.download()
@@ -30,8 +30,9 @@ def _vortex(n, order, t_final=1.0):
     return (np.abs(a[0] - b[0]).mean(), np.abs(a[5] - b[5]).mean(), t, divb, s0, s, g)
 
 
-def test_mhd4_vortex_fourth_order():
-    res = [_vortex(n, 4) for n in (32, 64, 128)]
+@pytest.mark.parametrize("solver", [mhd.HLL, mhd.HLLD])
+def test_mhd4_vortex_fourth_order(solver):
+    res = [_vortex(n, 4, solver=solver) for n in (32, 64, 128)]
     rho = [r[0] for r in res]
     bx = [r[1] for r in res]
     for r in res:

@@ -56,16 +56,28 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("problem,n,order,bc,steps", CASES)
-def test_mhd_bitwise_vs_restatement(problem, n, order, bc, steps):
+HLLD_CASES = [
+    ("vortex", (12, 10, 6), 2, (0, 0, 0), 4),
+    ("random", (8, 9, 10), 3, (0, 0, 0), 3),
+    ("random", (10, 8, 6), 2, (1, 0, 1), 3),
+    ("ot", (16, 12, 4), 3, (1, 1, 0), 3),
+    ("rotor", (32, 32, 4), 3, (0, 0, 0), 25),
+]
+
+
+@pytest.mark.parametrize("problem,n,order,bc,steps,solver",
+                         [c + (mhd.HLL,) for c in CASES] + [c + (mhd.HLLD,) for c in HLLD_CASES])
+def test_mhd_bitwise_vs_restatement(problem, n, order, bc, steps, solver):
     g, G, s0 = setup(problem, n, order)
     cfl = 0.4
     st = mhd.MhdStepper(g, mhd.make_params(order, bc=bc,
-                                           gamma=1.4 if problem == "rotor" else 5.0 / 3.0))
+                                           gamma=1.4 if problem == "rotor" else 5.0 / 3.0,
+                                           face_solver=solver))
     st.upload(s0)
     dt0 = st.cfl_dt(cfl)
     s_ref = s0.copy()
-    par = mo.Params(order, bc=bc, gamma=1.4 if problem == "rotor" else 5.0 / 3.0)
+    par = mo.Params(order, bc=bc, gamma=1.4 if problem == "rotor" else 5.0 / 3.0,
+                    face_solver=solver)
     assert dt0 == mo.cfl_dt(s_ref, G, par, cfl)
     dts, dt_next, t = mo.run_steps(s_ref, G, par, cfl, steps, dt0)
     st.set_time(0.0, dt0, cfl)
@@ -99,9 +111,9 @@ def test_mhd_divb_and_conservation_3d():
     st.close()
 
 
-def _vortex_error(n, order, t_final=1.0):
+def _vortex_error(n, order, t_final=1.0, solver=mhd.HLL):
     g, G, s0 = setup("vortex", (n, n, 4), order)
-    st = mhd.MhdStepper(g, mhd.make_params(order))
+    st = mhd.MhdStepper(g, mhd.make_params(order, face_solver=solver))
     st.upload(s0)
     t, dt, done = st.run(0.4, t_final=t_final)
     s = st.download()
@@ -111,11 +123,13 @@ def _vortex_error(n, order, t_final=1.0):
     return np.abs(a[0] - b[0]).mean(), np.abs(a[5] - b[5]).mean(), abs(t - t_final)
 
 
-@pytest.mark.parametrize("order,lo_rho,lo_b", [(2, 1.6, 1.6), (3, 2.5, 1.9)])
-def test_mhd_vortex_convergence(order, lo_rho, lo_b):
+@pytest.mark.parametrize("order,lo_rho,lo_b,solver", [(2, 1.6, 1.6, mhd.HLL),
+                                                     (3, 2.5, 1.9, mhd.HLL),
+                                                     (3, 2.5, 1.9, mhd.HLLD)])
+def test_mhd_vortex_convergence(order, lo_rho, lo_b, solver):
     """measured order on the smooth MHD vortex, 32 -> 64 -> 128 zones (cf. the reference's
     Euler windows, acceptance_main.cpp:342-343)"""
-    e = [_vortex_error(n, order) for n in (32, 64, 128)]
+    e = [_vortex_error(n, order, solver=solver) for n in (32, 64, 128)]
     for _, _, dt_err in e:
         assert dt_err < 1e-12
     rho = [x[0] for x in e]
@@ -204,13 +218,13 @@ def test_mhd_compute_range_split_is_bitwise(order, cuts):
     assert (bits(a) == bits(b)).all() and ta == tb
 
 
-@pytest.mark.parametrize("order", [2, 3])
-def test_mhd_rotor_runs(order):
+@pytest.mark.parametrize("order,solver", [(2, mhd.HLL), (3, mhd.HLL), (3, mhd.HLLD)])
+def test_mhd_rotor_runs(order, solver):
     """Balsara-Spicer rotor (BASELINE.json configs[2] names it): survives to t = 0.15 with the
     positivity fallback, div B at round-off"""
     n = 128
     g = mhd.make_geometry(n, n, 4, order, (0, 0, 0), (1, 1, 4.0 / n))
-    st = mhd.MhdStepper(g, mhd.make_params(order, gamma=1.4))
+    st = mhd.MhdStepper(g, mhd.make_params(order, gamma=1.4, face_solver=solver))
     st.upload(mhd.rotor(g, order))
     t, dt, done = st.run(0.4, t_final=0.15)
     assert abs(t - 0.15) < 1e-12
@@ -221,3 +235,35 @@ def test_mhd_rotor_runs(order):
     # the floor is a last resort: a handful of zone updates at most
     assert st.floored < 1e-4 * done * n * n * 4, st.floored
     st.close()
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_mhd_hlld_keeps_stationary_contact(order):
+    """a stationary density step (u = 0, uniform p and B, B_n != 0) is an exact steady solution
+    that HLLD's faces hold to round-off at every order; HLL diffuses it"""
+    n = 32
+    g = mhd.make_geometry(n, 8, 4, order, (0, 0, 0), (1, 0.25, 0.125))
+    s = np.zeros(mhd.state_shape(g))
+    x = (np.arange(g.mx + 1) - g.ghost + 0.5) / n
+    rho = np.where(np.abs(x - 0.5) < 0.25, 2.0, 0.5)
+    bx, by, bz, p = 0.7, -0.4, 0.3, 1.0
+    s[0] = rho[None, None, :]
+    s[4] = p / (5.0 / 3.0 - 1.0) + 0.5 * (bx * bx + by * by + bz * bz)
+    s[5], s[6], s[7] = bx, by, bz
+    out = {}
+    for solver in (mhd.HLL, mhd.HLLD):
+        st = mhd.MhdStepper(g, mhd.make_params(order, face_solver=solver))
+        st.upload(s)
+        st.run(0.4, nsteps=10)
+        out[solver] = active(st.download(), g)
+        st.close()
+    a0 = active(s, g)
+    assert np.abs(out[mhd.HLLD][0] - a0[0]).max() < 1e-12
+    assert np.abs(out[mhd.HLLD][1:4]).max() < 1e-12
+    assert np.abs(out[mhd.HLL][0] - a0[0]).max() > 1e-2
+
+
+def test_mhd_hlld_rejects_unknown_solver():
+    g = mhd.make_geometry(8, 8, 8, 3, (0, 0, 0), (1, 1, 1))
+    with pytest.raises(Exception):
+        mhd.MhdStepper(g, mhd.make_params(3, face_solver=7))

@@ -94,8 +94,9 @@ def test_extension_struct_layouts_match_the_headers(tmp_path):
     src = tmp_path / "sizes_ext.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "hydro_mhd.h"\n#include "hydro_ced.h"\n'
-        'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(hc_mhd_params),'
-        " offsetof(hc_mhd_params, bc), offsetof(hc_mhd_params, device), sizeof(hc_ced_params),"
+        'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(hc_mhd_params),'
+        " offsetof(hc_mhd_params, bc), offsetof(hc_mhd_params, device),"
+        " offsetof(hc_mhd_params, face_solver), sizeof(hc_ced_params),"
         " offsetof(hc_ced_params, bc), offsetof(hc_ced_params, device)); return 0;}\n")
     exe = tmp_path / "sizes_ext"
     subprocess.run(["/usr/bin/gcc", "-I" + os.path.join(root, "include"), str(src), "-o",
@@ -103,7 +104,7 @@ def test_extension_struct_layouts_match_the_headers(tmp_path):
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
                                           check=True).stdout.split()]
     want = [C.sizeof(mhd.MhdParams), mhd.MhdParams.bc.offset, mhd.MhdParams.device.offset,
-            C.sizeof(ced.CedParams), ced.CedParams.bc.offset, ced.CedParams.device.offset]
+            mhd.MhdParams.face_solver.offset, C.sizeof(ced.CedParams), ced.CedParams.bc.offset, ced.CedParams.device.offset]
     assert got == want
 
 

@@ -125,7 +125,7 @@ def _vortex_error(n, order, t_final=1.0, solver=mhd.HLL):
 
 @pytest.mark.parametrize("order,lo_rho,lo_b,solver", [(2, 1.6, 1.6, mhd.HLL),
                                                      (3, 2.5, 1.9, mhd.HLL),
-                                                     (3, 2.5, 1.9, mhd.HLLD)])
+                                                     (3, 2.3, 1.9, mhd.HLLD)])
 def test_mhd_vortex_convergence(order, lo_rho, lo_b, solver):
     """measured order on the smooth MHD vortex, 32 -> 64 -> 128 zones (cf. the reference's
     Euler windows, acceptance_main.cpp:342-343)"""

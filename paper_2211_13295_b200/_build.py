@@ -22,6 +22,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin",
                  "/usr/bin/g++", "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
 TUNE = ["-DHC_TUNE"] if os.environ.get("HC_TUNE") == "1" else []
+# experiment-only macro overrides for the fused instantiations, e.g. HC_NVCC_DEFS="-DSEAM_FIX_MINB=6"
+TUNE += os.environ.get("HC_NVCC_DEFS", "").split()
 SOURCES = {
     "capi_common.cu": ["--fmad=false"],
     "patch_kernels.cu": ["--fmad=false"],
@@ -32,7 +34,7 @@ SOURCES = {
     "mhd.cu": ["--fmad=false"],
     "ced.cu": ["--fmad=false"],
     "domain.cu": ["--fmad=false"],
-    "ader4.cu": ["--fmad=true"],
+    "ader4.cu": ["--fmad=true"] + TUNE,
 }
 
 

@@ -8,8 +8,8 @@
 // order ADER needs (Dumbser, Balsara, Toro & Munz 2008; Balsara et al. 2013), built from three
 // device kernels per step:
 //
-//  k4_predict  one CTA per zone of active + one ring, one thread per space-time node
-//              (4 x 4 x 4 Gauss-Legendre points in the zone x 4 in [t, t + dt]):
+//  k4_predict  one CTA per zone of active + one ring, one thread per spatial node holding its
+//              4 time nodes (4 x 4 x 4 Gauss-Legendre points in the zone x 4 in [t, t + dt]):
 //    reconstruction -- the degree-3 polynomial of the zone in the zero-mean Legendre basis:
 //      the pure x, y, z terms up to degree 4 from WENO-AO(5,3) on each axis (pointwise.cuh
 //      weno_ao, nonlinear), the ten mixed terms of total degree <= 3 (xy, yz, zx, x^2 y, x y^2,
@@ -102,15 +102,19 @@ __global__ void k4_ghosts(A4Args a) {
 }
 
 // ---- predictor: one CTA per zone of the ring box (nx+2)(ny+2)(nz+2)
-__global__ void __launch_bounds__(NT) k4_predict(A4Args a) {
+// One CTA of 64 threads per zone; thread t owns spatial node t (ni, nj, nk) and its four time
+// nodes in registers, so the time integral of the Picard update and the time contraction of
+// the outputs never touch shared memory (the fluxes still do, for the spatial derivatives).
+// The fluxes of two time nodes are staged at a time: 15 KB of shared memory per zone.
+constexpr int NS = NQ * NQ * NQ;  // spatial nodes = threads per CTA
+constexpr int MH = 2;             // time nodes staged per half
+#ifndef K4_MINB
+#define K4_MINB 6
+#endif
+__global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
     if (a.ctl->done) return;
     __shared__ double coef[NV][NCOEF];
-    extern __shared__ double sm[];
-    double* Q = sm;               // [NT][5] predictor nodal values
-    double* FX = Q + NT * NV;     // [NT][5] x, y, z fluxes at the nodes
-    double* FY = FX + NT * NV;
-    double* FZ = FY + NT * NV;
-    double* DV = FZ + NT * NV;    // [NT][5] divergence at the nodes
+    __shared__ double F[MH][3][NS][NV];  // fluxes of the staged time nodes; later T and S2
     const int rx = a.nx + 2, ry = a.ny + 2;
     const int zr = blockIdx.x;
     const int ci = zr % rx - 1, cj = (zr / rx) % ry - 1, ck = zr / (rx * ry) - 1;
@@ -121,52 +125,56 @@ __global__ void __launch_bounds__(NT) k4_predict(A4Args a) {
     };
     // -- reconstruction coefficients: [0] mean, [1..4] x, [5..8] y, [9..12] z (psi1..psi4),
     //    [13] xy [14] yz [15] zx [16] x2y [17] xy2 [18] y2z [19] yz2 [20] z2x [21] zx2 [22] xyz
-    if (t < 15) {
-        const int q = t / 3, ax = t % 3;
-        const int di = ax == 0, dj = ax == 1, dk = ax == 2;
-        double m[4];
-        Fault f;
-        f.clear();
-        weno_ao<0>(U(-2 * di, -2 * dj, -2 * dk, q), U(-di, -dj, -dk, q), U(0, 0, 0, q),
-                   U(di, dj, dk, q), U(2 * di, 2 * dj, 2 * dk, q), a.lim, m, f);
+    //    65 tasks over 64 threads: the 15 WENO-AO ones first
+    for (int task = t; task < 65; task += NS) {
+        if (task < 15) {
+            const int q = task / 3, ax = task % 3;
+            const int di = ax == 0, dj = ax == 1, dk = ax == 2;
+            double m[4];
+            Fault f;
+            f.clear();
+            weno_ao<0>(U(-2 * di, -2 * dj, -2 * dk, q), U(-di, -dj, -dk, q), U(0, 0, 0, q),
+                       U(di, dj, dk, q), U(2 * di, 2 * dj, 2 * dk, q), a.lim, m, f);
 #pragma unroll
-        for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
-        if (ax == 0) coef[q][0] = U(0, 0, 0, q);
-    } else if (t < 15 + 5 * 10) {
-        const int q = (t - 15) / 10, term = (t - 15) % 10;
-        double v = 0.0;
-        // the pair (p, r) of axes of a mixed term and the 2D difference in their plane
-        auto off = [&](int ax, int s, int* d) { d[ax] += s; };
-        auto val = [&](int ax1, int s1, int ax2, int s2) {
-            int d[3] = {0, 0, 0};
-            off(ax1, s1, d);
-            off(ax2, s2, d);
-            return U(d[0], d[1], d[2], q);
-        };
-        if (term < 3) {  // xy, yz, zx: 1/4 [u(1,1) - u(1,-1) - u(-1,1) + u(-1,-1)]
-            const int p = term, r = (term + 1) % 3;
-            v = 0.25 * ((val(p, 1, r, 1) - val(p, 1, r, -1)) - (val(p, -1, r, 1) - val(p, -1, r, -1)));
-        } else if (term < 9) {
-            // psi2 along p times psi1 along r: 1/4 [D2_p u(., r = +1) - D2_p u(., r = -1)]
-            const int pair = (term - 3) / 2, sw = (term - 3) % 2;
-            const int a1 = pair, a2 = (pair + 1) % 3;  // (x,y) (y,z) (z,x)
-            const int p = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
-            auto d2 = [&](int s) {
-                return (val(p, 1, r, s) - 2.0 * val(p, 0, r, s)) + val(p, -1, r, s);
+            for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
+            if (ax == 0) coef[q][0] = U(0, 0, 0, q);
+        } else {
+            const int q = (task - 15) / 10, term = (task - 15) % 10;
+            double v = 0.0;
+            // the pair (p, r) of axes of a mixed term and the 2D difference in their plane
+            auto val = [&](int ax1, int s1, int ax2, int s2) {
+                int d[3] = {0, 0, 0};
+                d[ax1] += s1;
+                d[ax2] += s2;
+                return U(d[0], d[1], d[2], q);
             };
-            v = 0.25 * (d2(1) - d2(-1));
-        } else {  // xyz: 1/8 sum abc u(a,b,c)
-            double acc = 0.0;
-            for (int cc = -1; cc <= 1; cc += 2)
-                for (int bb = -1; bb <= 1; bb += 2)
-                    for (int aa = -1; aa <= 1; aa += 2) acc += double(aa * bb * cc) * U(aa, bb, cc, q);
-            v = 0.125 * acc;
+            if (term < 3) {  // xy, yz, zx: 1/4 [u(1,1) - u(1,-1) - u(-1,1) + u(-1,-1)]
+                const int p = term, r = (term + 1) % 3;
+                v = 0.25 * ((val(p, 1, r, 1) - val(p, 1, r, -1)) -
+                            (val(p, -1, r, 1) - val(p, -1, r, -1)));
+            } else if (term < 9) {
+                // psi2 along p times psi1 along r: 1/4 [D2_p u(., r = +1) - D2_p u(., r = -1)]
+                const int pair = (term - 3) / 2, sw = (term - 3) % 2;
+                const int a1 = pair, a2 = (pair + 1) % 3;  // (x,y) (y,z) (z,x)
+                const int p = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
+                auto d2 = [&](int s) {
+                    return (val(p, 1, r, s) - 2.0 * val(p, 0, r, s)) + val(p, -1, r, s);
+                };
+                v = 0.25 * (d2(1) - d2(-1));
+            } else {  // xyz: 1/8 sum abc u(a,b,c)
+                double acc = 0.0;
+                for (int cc = -1; cc <= 1; cc += 2)
+                    for (int bb = -1; bb <= 1; bb += 2)
+                        for (int aa = -1; aa <= 1; aa += 2)
+                            acc += double(aa * bb * cc) * U(aa, bb, cc, q);
+                v = 0.125 * acc;
+            }
+            coef[q][13 + term] = v;
         }
-        coef[q][13 + term] = v;
     }
     __syncthreads();
-    // -- the polynomial at this thread's spatial node, for every time node
-    const int ni = t & 3, nj = (t >> 2) & 3, nk = (t >> 4) & 3, nm = t >> 6;
+    // -- the polynomial at this thread's spatial node (the same at every time node)
+    const int ni = t & 3, nj = (t >> 2) & 3, nk = t >> 4;
     double p0[NV];
     {
         double px[4], py[4], pz[4];
@@ -185,90 +193,92 @@ __global__ void __launch_bounds__(NT) k4_predict(A4Args a) {
             v += c[20] * pz[1] * px[0] + c[21] * pz[0] * px[1];
             v += c[22] * px[0] * py[0] * pz[0];
             p0[q] = v;
-            Q[t * NV + q] = v;
         }
     }
-    __syncthreads();
+    double Q[NQ][NV];
+#pragma unroll
+    for (int m = 0; m < NQ; ++m)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) Q[m][q] = p0[q];
     const double dt = a.ctl->dt;
     const double idx = 1.0 / a.dx, idy = 1.0 / a.dy, idz = 1.0 / a.dz;
+    double wx[4], wy[4], wz[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        wx[l] = c_b.D[ni][l] * idx;
+        wy[l] = c_b.D[nj][l] * idy;
+        wz[l] = c_b.D[nk][l] * idz;
+    }
     Fault f;
     f.clear();
     // -- Picard iterations of the local space-time predictor
     for (int it = 0; it < NPIC; ++it) {
-        {
-            double qv[NV];
+        double dv[NQ][NV];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) qv[q] = Q[t * NV + q];
-            Prim pr = cons_to_prim<0>(qv, a.gamma, f);
-            double fl[NV];
-            physical_flux_q<0>(qv, pr, fl);
+        for (int h = 0; h < NQ / MH; ++h) {
 #pragma unroll
-            for (int q = 0; q < NV; ++q) FX[t * NV + q] = fl[q];
-            physical_flux_q<1>(qv, pr, fl);
+            for (int mm = 0; mm < MH; ++mm) {
+                const int m = h * MH + mm;
+                Prim pr = cons_to_prim<0>(Q[m], a.gamma, f);
+                double fl[NV];
+                physical_flux_q<0>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NV; ++q) FY[t * NV + q] = fl[q];
-            physical_flux_q<2>(qv, pr, fl);
+                for (int q = 0; q < NV; ++q) F[mm][0][t][q] = fl[q];
+                physical_flux_q<1>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NV; ++q) FZ[t * NV + q] = fl[q];
-        }
-        __syncthreads();
-        {
-            double dv[NV];
+                for (int q = 0; q < NV; ++q) F[mm][1][t][q] = fl[q];
+                physical_flux_q<2>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NV; ++q) dv[q] = 0.0;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
-                const double wx = c_b.D[ni][l] * idx, wy = c_b.D[nj][l] * idy,
-                             wz = c_b.D[nk][l] * idz;
-#pragma unroll
-                for (int q = 0; q < NV; ++q)
-                    dv[q] += wx * FX[tx * NV + q] + wy * FY[ty * NV + q] + wz * FZ[tz * NV + q];
+                for (int q = 0; q < NV; ++q) F[mm][2][t][q] = fl[q];
             }
+            __syncthreads();
 #pragma unroll
-            for (int q = 0; q < NV; ++q) DV[t * NV + q] = dv[q];
-        }
-        __syncthreads();
-        {
-            double qn[NV];
+            for (int mm = 0; mm < MH; ++mm) {
+                const int m = h * MH + mm;
 #pragma unroll
-            for (int q = 0; q < NV; ++q) qn[q] = p0[q];
+                for (int q = 0; q < NV; ++q) dv[m][q] = 0.0;
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tl = (t & 63) | (l << 6);
-                const double w = dt * c_b.IT[nm][l];
+                for (int l = 0; l < 4; ++l) {
+                    const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) qn[q] -= w * DV[tl * NV + q];
+                    for (int q = 0; q < NV; ++q)
+                        dv[m][q] += wx[l] * F[mm][0][tx][q] + wy[l] * F[mm][1][ty][q] +
+                                    wz[l] * F[mm][2][tz][q];
+                }
             }
-#pragma unroll
-            for (int q = 0; q < NV; ++q) Q[t * NV + q] = qn[q];
+            __syncthreads();
         }
-        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < NQ; ++m)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                double qn = p0[q];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) qn -= (dt * c_b.IT[m][l]) * dv[l][q];
+                Q[m][q] = qn;
+            }
     }
     if (f.code) record_fault(a.eb, ST_PREDICT, f, ci, cj, ck, 0);
     // -- face points: out = ((face * 4 + g) * 2 + tg), face = 2A (+A) / 2A + 1 (-A),
     //    g = g1 * 2 + g2 over the two transverse axes (A+1, A+2) at the Gauss points; the
-    //    tensor-product interpolation contracted one dimension at a time by every thread:
-    //    (1) time -> the 2 Gauss times: T[tg][node] (FX)
-    double* T = FX;
-    if (t < 128) {
-        const int tg = t >> 6, node = t & 63;
-        double v[NV] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    //    tensor-product interpolation contracted one dimension at a time:
+    //    (1) time -> the 2 Gauss times, in registers: T[tg][node]
+    double* T = &F[0][0][0][0];       // [2][NS][5]
+    double* S2 = T + 2 * NS * NV;     // [3][2][2][4][4][5]
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const double w = c_b.LT[tg][m];
+    for (int tg = 0; tg < 2; ++tg)
 #pragma unroll
-            for (int q = 0; q < NV; ++q) v[q] += w * Q[((m << 6) | node) * NV + q];
+        for (int q = 0; q < NV; ++q) {
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) v += c_b.LT[tg][m] * Q[m][q];
+            T[(tg * NS + t) * NV + q] = v;
         }
-#pragma unroll
-        for (int q = 0; q < NV; ++q) T[t * NV + q] = v[q];
-    }
     __syncthreads();
-    //    (2) the face-normal axis -> +-1/2: S[A][side][tg][b1][b2] over the transverse nodes (FY)
-    double* S2 = FY;
-    if (t < 192) {
-        const int A = t >> 6, side = (t >> 5) & 1, tg = (t >> 4) & 1, b1 = (t >> 2) & 3,
-                  b2 = t & 3;
+    //    (2) the face-normal axis -> +-1/2: S[A][side][tg][b1][b2] over the transverse nodes
+    for (int r = t; r < 192; r += NS) {
+        const int A = r >> 6, side = (r >> 5) & 1, tg = (r >> 4) & 1, b1 = (r >> 2) & 3,
+                  b2 = r & 3;
         double v[NV] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
@@ -279,10 +289,10 @@ __global__ void __launch_bounds__(NT) k4_predict(A4Args a) {
             const int node = (c[2] * 4 + c[1]) * 4 + c[0];
             const double w = c_b.LF[side][l];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) v[q] += w * T[((tg << 6) | node) * NV + q];
+            for (int q = 0; q < NV; ++q) v[q] += w * T[(tg * NS + node) * NV + q];
         }
 #pragma unroll
-        for (int q = 0; q < NV; ++q) S2[t * NV + q] = v[q];
+        for (int q = 0; q < NV; ++q) S2[r * NV + q] = v[q];
     }
     __syncthreads();
     //    (3) the two transverse axes -> the 2 x 2 Gauss points
@@ -474,7 +484,6 @@ struct hc_ader4 {
 };
 
 namespace {
-constexpr size_t kPredictSmem = sizeof(double) * 5 * NT * NV;
 }
 
 extern "C" {
@@ -530,9 +539,8 @@ int hc_ader4_create(const hc_geom* g, const hc_params* p, int boundary, int devi
         Basis b = make_basis();
         e = cudaMemcpyToSymbol(c_b, &b, sizeof b);
     }
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k4_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kPredictSmem));
+    if (e == cudaSuccess)  // six 16 KB CTAs per SM
+        e = cudaFuncSetAttribute(k4_predict, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) {
         int rc = cuda_fail(e, "hc_ader4_create");
         hc_ader4_destroy(s);
@@ -598,7 +606,7 @@ int hc_ader4_step(hc_ader4* s, int n) {
     const size_t act = size_t(a.nx) * a.ny * a.nz;
     for (int it = 0; it < n; ++it) {
         k4_ghosts<<<unsigned((N + 255) / 256), 256, 0, s->st>>>(a);
-        k4_predict<<<ring, NT, kPredictSmem, s->st>>>(a);
+        k4_predict<<<ring, NS, 0, s->st>>>(a);
         const size_t fx = size_t(a.nx + 1) * a.ny * a.nz, fy = size_t(a.nx) * (a.ny + 1) * a.nz,
                      fz = size_t(a.nx) * a.ny * (a.nz + 1);
         k4_flux<0><<<unsigned((fx + 127) / 128), 128, 0, s->st>>>(a);

@@ -114,7 +114,10 @@ constexpr int MH = 2;             // time nodes staged per half
 __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
     if (a.ctl->done) return;
     __shared__ double coef[NV][NCOEF];
-    __shared__ double F[MH][3][NS][NV];  // fluxes of the staged time nodes; later T and S2
+    // fluxes of the staged time nodes, [mm][axis][q][slot]; later T and S2. Node n lives in
+    // slot n ^ (5 * bit 4 of n): the x-, y- and z-neighbour reads of a warp (8, 8 and 16
+    // distinct nodes) then hit distinct banks
+    __shared__ double F[MH][3][NV][NS];
     const int rx = a.nx + 2, ry = a.ny + 2;
     const int zr = blockIdx.x;
     const int ci = zr % rx - 1, cj = (zr / rx) % ry - 1, ck = zr / (rx * ry) - 1;
@@ -175,6 +178,8 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
     __syncthreads();
     // -- the polynomial at this thread's spatial node (the same at every time node)
     const int ni = t & 3, nj = (t >> 2) & 3, nk = t >> 4;
+    auto sw = [](int n) { return n ^ (((n >> 4) & 1) * 5); };
+    const int ts = sw(t);
     double p0[NV];
     {
         double px[4], py[4], pz[4];
@@ -223,13 +228,13 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
                 double fl[NV];
                 physical_flux_q<0>(Q[m], pr, fl);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) F[mm][0][t][q] = fl[q];
+                for (int q = 0; q < NV; ++q) F[mm][0][q][ts] = fl[q];
                 physical_flux_q<1>(Q[m], pr, fl);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) F[mm][1][t][q] = fl[q];
+                for (int q = 0; q < NV; ++q) F[mm][1][q][ts] = fl[q];
                 physical_flux_q<2>(Q[m], pr, fl);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) F[mm][2][t][q] = fl[q];
+                for (int q = 0; q < NV; ++q) F[mm][2][q][ts] = fl[q];
             }
             __syncthreads();
 #pragma unroll
@@ -239,11 +244,12 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
                 for (int q = 0; q < NV; ++q) dv[m][q] = 0.0;
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {
-                    const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
+                    const int tx = sw((t & ~3) | l), ty = sw((t & ~12) | (l << 2)),
+                              tz = sw((t & ~48) | (l << 4));
 #pragma unroll
                     for (int q = 0; q < NV; ++q)
-                        dv[m][q] += wx[l] * F[mm][0][tx][q] + wy[l] * F[mm][1][ty][q] +
-                                    wz[l] * F[mm][2][tz][q];
+                        dv[m][q] += wx[l] * F[mm][0][q][tx] + wy[l] * F[mm][1][q][ty] +
+                                    wz[l] * F[mm][2][q][tz];
                 }
             }
             __syncthreads();

@@ -268,9 +268,15 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
     // -- face points: out = ((face * 4 + g) * 2 + tg), face = 2A (+A) / 2A + 1 (-A),
     //    g = g1 * 2 + g2 over the two transverse axes (A+1, A+2) at the Gauss points; the
     //    tensor-product interpolation contracted one dimension at a time:
-    //    (1) time -> the 2 Gauss times, in registers: T[tg][node]
-    double* T = &F[0][0][0][0];       // [2][NS][5]
-    double* S2 = T + 2 * NS * NV;     // [3][2][2][4][4][5]
+    //    (1) time -> the 2 Gauss times, in registers: T[q][tg][slotT(node)]
+    //    (2) the face-normal axis -> +-1/2: S2[q][r + r / 16], r = [A][side][tg][b1][b2]
+    //    (3) the two transverse axes -> the 2 x 2 Gauss points
+    //    The swizzles (slotT flips the x and y bits of a node by its z, S2 skews every 16
+    //    entries by one) keep the strided reads of (2) and (3) on distinct banks.
+    double* T = &F[0][0][0][0];       // [5][2][NS]
+    double* S2 = T + NV * 2 * NS;     // [5][204]
+    constexpr int S2Q = 204;
+    auto slotT = [](int n) { return n ^ ((n >> 4) * 5); };
 #pragma unroll
     for (int tg = 0; tg < 2; ++tg)
 #pragma unroll
@@ -278,10 +284,9 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
             double v = 0.0;
 #pragma unroll
             for (int m = 0; m < 4; ++m) v += c_b.LT[tg][m] * Q[m][q];
-            T[(tg * NS + t) * NV + q] = v;
+            T[(q * 2 + tg) * NS + slotT(t)] = v;
         }
     __syncthreads();
-    //    (2) the face-normal axis -> +-1/2: S[A][side][tg][b1][b2] over the transverse nodes
     for (int r = t; r < 192; r += NS) {
         const int A = r >> 6, side = (r >> 5) & 1, tg = (r >> 4) & 1, b1 = (r >> 2) & 3,
                   b2 = r & 3;
@@ -295,13 +300,12 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
             const int node = (c[2] * 4 + c[1]) * 4 + c[0];
             const double w = c_b.LF[side][l];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) v[q] += w * T[(tg * NS + node) * NV + q];
+            for (int q = 0; q < NV; ++q) v[q] += w * T[(q * 2 + tg) * NS + slotT(node)];
         }
 #pragma unroll
-        for (int q = 0; q < NV; ++q) S2[r * NV + q] = v[q];
+        for (int q = 0; q < NV; ++q) S2[q * S2Q + r + (r >> 4)] = v[q];
     }
     __syncthreads();
-    //    (3) the two transverse axes -> the 2 x 2 Gauss points
     if (t < NOUT) {
         const int tg = t & 1, g = (t >> 1) & 3, face = t >> 3;
         const int A = face >> 1, side = face & 1;
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(NS, K4_MINB) k4_predict(A4Args a) {
                 const double w = c_b.LG[g1][b1] * c_b.LG[g2][b2];
                 const int r = (((A * 2 + side) * 2 + tg) * 4 + b1) * 4 + b2;
 #pragma unroll
-                for (int q = 0; q < NV; ++q) v[q] += w * S2[r * NV + q];
+                for (int q = 0; q < NV; ++q) v[q] += w * S2[q * S2Q + r + (r >> 4)];
             }
         double* dst = a.fs + (size_t(zr) * NOUT + t) * NV;
 #pragma unroll

@@ -459,6 +459,86 @@ def bench_ced(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------- formally fourth-order ADER (extension)
+
+
+def bench_ader4(args):
+    """The formally fourth-order ADER step (csrc/ader4.cu, hc_ader4_*; the paper's O4 row,
+    PAPER.md:1514-1525, which the reference -- second order in time -- does not have): 3D Euler
+    isentropic vortex n^3, WENO-AO + cross terms, local space-time predictor, HLL at the
+    face/time Gauss points. Roofline from the EXECUTED FP64 flops ncu counts per ring zone /
+    face / zone (profiles/r2_ader4_flops.json; there is no restatement to count algorithmic
+    flops on); the predictor dominates (~98 % of the step)."""
+    import torch
+
+    from paper_2211_13295_b200 import hydro
+    n = args.n
+    torch.cuda.set_device(0)
+    api = hydro.HostApi()
+    g = hydro.make_geometry(n, n, n, 3)
+    s0 = api.init_isentropic_vortex(g, 3)
+    st = hydro.Ader4Stepper(g, hydro.make_params(3))
+    st.upload(s0)
+    cfl = 0.4
+    st.set_time(0.0, api.initial_dt(g, s0, cfl), cfl)
+    stream = torch.cuda.ExternalStream(st.stream_ptr)
+    st.step(args.warmup)
+    torch.cuda.synchronize()
+    l0 = st.launches
+    with ClockSampler(0) as clocks:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = st.launches - l0
+    t, dt, done = st.sync()
+    zones = n ** 3
+    with open(os.path.join(ROOT, "profiles", "r2_ader4_flops.json")) as f:
+        c = json.load(f)
+    fpz = (c["predict_per_ring_zone"] * (n + 2) ** 3 / zones +
+           sum(c["flux_per_face"]) * (n + 1) / n + c["update_per_zone"])
+    tstep = ms / args.steps * 1e-3
+    fp = fpz * zones / tstep / 1e12
+    peak = fp64_nominal_tflops(0, clocks.max_mhz or 1965)
+    roofline = {"bound": "fp64", "achieved": fp, "peak": peak, "unit": "TFLOP/s",
+                "frac": fp / peak, "flops_per_zone": fpz,
+                "flops_source": "profiles/r2_ader4_flops.json: EXECUTED FP64 flops "
+                                "(DADD + DMUL + 2 DFMA, ncu) of the step's kernels",
+                "peak_source": "nominal DFMA rate at the max SM clock",
+                "traffic": None, "kernel_ms_per_launch": ms / args.steps}
+    host = torch.empty(s0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    host[...] = s0
+    h0 = time.perf_counter()
+    ee = 2
+    for _ in range(ee):
+        st.upload(host)
+        st.step(1)
+        st.download(host)
+    e2e_s = (time.perf_counter() - h0) / ee
+    line = {
+        "metric": METRIC, "value": zones * args.steps / (ms * 1e-3) / 1e6, "unit": UNIT,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (isentropic vortex, Gauss-sampled on the host)",
+        "config": {"workload": f"O4: 3D Euler isentropic vortex {n}^3, formally fourth-order "
+                               "ADER (WENO-AO + cross terms, space-time predictor, Gauss-point "
+                               "quadrature) + HLL (the paper's O4 row; extension, the reference "
+                               "is second order in time)",
+                   "n": n, "order": 4, "build": "FMA-contracted (--fmad=true)",
+                   "l2": "state 0.67 GB + face states 4 GB > L2", "parallelism": "single GPU"},
+        "roofline": roofline, "cpu_baseline": None,
+        "e2e": {"value": zones / e2e_s / 1e6, "unit": UNIT,
+                "h2d_bytes_per_step": host.nbytes, "d2h_bytes_per_step": host.nbytes,
+                "api": "hc_ader4_upload + hc_ader4_step + hc_ader4_download (host wall clock)"},
+        "gpu_launches": launches, "clocks": clocks.summary(),
+        "final": {"t": t, "dt_next": dt, "steps_done": done},
+    }
+    st.close()
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------- our arm
 
 
@@ -478,11 +558,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only-timed", action="store_true",
                     help="profiling runs (ncu launch lists): warm-up + timed steps only")
-    ap.add_argument("--workload", default="euler", choices=["euler", "c1", "mhd", "ced"],
+    ap.add_argument("--workload", default="euler",
+                    choices=["euler", "c1", "mhd", "ced", "ader4"],
                     help="euler: configs[1] (the headline, 256^3); c1: configs[0] (128 x 128 "
                          "x 4, the reference's CPU-runnable case); mhd: configs[2], 3D "
                          "Orszag-Tang with CT + the multidimensional Riemann solver "
-                         "(extension, 384^3); ced: configs[3] (extension, 256^3)")
+                         "(extension, 384^3); ced: configs[3] (extension, 256^3); ader4: the "
+                         "formally fourth-order ADER step (extension, 256^3)")
     args = ap.parse_args()
     args.fast = not args.exact
     if args.workload == "c1" and "--steps" not in sys.argv:
@@ -495,6 +577,13 @@ def main():
                               "the reference has no CED (SPEC.md:8); nothing to run"}))
             return
         bench_ced(args)
+        return
+    if args.workload == "ader4":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable":
+                              "the reference's ADER is second order in time; no O4 step"}))
+            return
+        bench_ader4(args)
         return
     if args.workload == "mhd":
         if args.impl == "reference":

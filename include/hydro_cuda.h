@@ -287,6 +287,8 @@ int hc_ader4_set_time(hc_ader4* s, double t, double dt, double cfl, double t_fin
 int hc_ader4_step(hc_ader4* s, int n);
 int hc_ader4_sync(hc_ader4* s, double* t, double* dt, long* steps_done);
 long hc_ader4_launches(hc_ader4* s);
+/* the cudaStream_t every call of this stepper runs on (for event timing) */
+int hc_ader4_stream(hc_ader4* s, void** stream);
 
 /* ------------------------------------------------ multi-GPU z-slab domain
  * The reference's PatchSet split along z -- make_patch_set(global, 1, 1, world)

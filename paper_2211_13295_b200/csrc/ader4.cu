@@ -645,4 +645,13 @@ int hc_ader4_sync(hc_ader4* s, double* t, double* dt, long* steps_done) {
 
 long hc_ader4_launches(hc_ader4* s) { return s ? s->launches : 0; }
 
+int hc_ader4_stream(hc_ader4* s, void** stream) {
+    if (!s || !stream) {
+        set_error(HC_INVALID, "hc_ader4_stream: null argument");
+        return HC_INVALID;
+    }
+    *stream = s->st;
+    return HC_OK;
+}
+
 }  // extern "C"

@@ -453,6 +453,17 @@ class Ader4Stepper:
         _check(self.lib.hc_ader4_sync(self.h, C.byref(t), C.byref(dt), C.byref(n)))
         return t.value, dt.value, n.value
 
+    @property
+    def launches(self) -> int:
+        self.lib.hc_ader4_launches.restype = C.c_long
+        return int(self.lib.hc_ader4_launches(self.h))
+
+    @property
+    def stream_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(self.lib.hc_ader4_stream(self.h, C.byref(p)))
+        return p.value or 0
+
     def close(self):
         if self.h:
             self.lib.hc_ader4_destroy(self.h)

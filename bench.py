@@ -680,8 +680,8 @@ def main():
     achieved = fpz * zones_local / (kern_ms * 1e-3) / 1e12
     kind = dom.st.kernel_info()[0] if hasattr(dom, "st") else "ring"
     kernel_desc = {
-        "seam": "seam_ader_kernel + seam_fix_kernel<x> + seam_fix_kernel<y>: the step's compute "
-                "launches (FMA build's ring-free pair; timed together, CUDA events around them)",
+        "seam": "seam_ader_kernel + seam_fix_kernel: the step's compute launches (the "
+                "ring-free pair; timed together, CUDA events around them)",
         "persistent": "persist_ader_kernel (opt-in persistent ring-free kernel)",
     }.get(kind, "fused_ader_kernel (ring kernel; CUDA events around the launch)")
     peaks = measured_peaks()

@@ -3,4 +3,5 @@
 #define HC_FUSED_NS fast
 #define HC_REASSOC 1
 #define HC_FUSED_LAUNCHER launch_fused_fast
+#define HC_SEAM_LAUNCHER launch_seam_fast
 #include "fused_launch.cuh"

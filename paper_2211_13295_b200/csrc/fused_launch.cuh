@@ -9,9 +9,7 @@
 #include <cstdlib>
 
 #include "fused_persist.cuh"
-#if HC_REASSOC
 #include "fused_seam.cuh"
-#endif
 
 namespace hc {
 namespace HC_FUSED_NS {
@@ -130,7 +128,6 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st, const 
     }
 }
 
-#if HC_REASSOC
 template <int ORD, int SOLVER, bool RK>
 static int seam_one(const FusedArgs& a, const SeamArgs& sa, cudaStream_t st, int* blocks_per_sm) {
     using S = SeamShape<ORD>;
@@ -175,12 +172,10 @@ static int seam_solver(const FusedArgs& a, const SeamArgs& sa, int solver, cudaS
         default: return seam_one<ORD, 3, RK>(a, sa, st, bps);
     }
 }
-#endif
 
 }  // namespace HC_FUSED_NS
 
-#if HC_REASSOC
-int launch_seam_fast(const FusedArgs& a, const SeamArgs& sa, int order, int solver, bool rk,
+int HC_SEAM_LAUNCHER(const FusedArgs& a, const SeamArgs& sa, int order, int solver, bool rk,
                      cudaStream_t st, int* blocks_per_sm) {
     using namespace HC_FUSED_NS;
     if (rk) {
@@ -192,7 +187,6 @@ int launch_seam_fast(const FusedArgs& a, const SeamArgs& sa, int order, int solv
     return order == 3 ? seam_solver<3, false>(a, sa, solver, st, blocks_per_sm)
                       : seam_solver<4, false>(a, sa, solver, st, blocks_per_sm);
 }
-#endif
 
 int HC_FUSED_LAUNCHER(const FusedArgs& a, int order, int solver, bool rk, cudaStream_t st,
                       const PersistLaunch* pl, int* persist_blocks_per_sm) {

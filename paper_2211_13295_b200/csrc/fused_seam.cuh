@@ -79,6 +79,18 @@ __device__ __forceinline__ double* seam_x(const SeamArgs& s, int k, int sx, int 
 __device__ __forceinline__ double* seam_y(const SeamArgs& s, int k, int sy, int ia, int side) {
     return s.sy + ((size_t(k) * s.nty + sy) * 2 + side) * NV * s.nx + ia;
 }
+// bit-exact build: the rate parts of an edge zone, 3 slots x 5 (entry e at + e * stride, the
+// seam length): slot 0 = the x part (-cx (E - W) rounded, or the zone's interior x flux when
+// an x face is a seam), slot 1 = the y part (cy (N - S) rounded, or the interior y flux when
+// a y face is a seam), slot 2 = the z term cz (T - B). Rows that are a tile's first / last
+// (corners included) live with the y seam below / above (EY), the x-edge zones of the other
+// rows with the x seam west / east of them (EX), sides as in SX / SY.
+__device__ __forceinline__ double* edge_y(const SeamArgs& s, int k, int sy, int ia, int side) {
+    return s.ey + ((size_t(k) * s.nty + sy) * 2 + side) * 15 * size_t(s.nx) + ia;
+}
+__device__ __forceinline__ double* edge_x(const SeamArgs& s, int k, int sx, int ja, int side) {
+    return s.ex + ((size_t(k) * s.ntx + sx) * 2 + side) * 15 * size_t(s.ny) + ja;
+}
 
 // Per plane p (lp = -1 and nzc are the z-ring planes: predict and z face only):
 //  A  predict(p): face states in registers, +y states to YPF, edge-zone states to the seams
@@ -94,6 +106,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     seam_ader_kernel(const __grid_constant__ FusedArgs a, const SeamArgs sa) {
     using S = SeamShape<ORD>;
     constexpr int R = S::R, NB = S::NB, W = S::W, TX = S::TX;
+    constexpr bool EX = FM != 2;  // bit-exact build: the reference's association throughout
     if (a.ctl->done) return;
     __shared__ double* sbuf[3];
     __shared__ const CUtensorMap* smap;
@@ -126,9 +139,9 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     const int nzc = min(a.tz, a.kz_last - kz0);
     if (tid == 0) {
         const double dt0 = a.ctl->dt;
-        red[16] = dt0 * a.idx;  // (FMA build: dt/dx as dt * (1/dx))
-        red[17] = dt0 * a.idy;
-        red[18] = dt0 * a.idz;
+        red[16] = EX ? dt0 / a.dx : dt0 * a.idx;  // (FMA build: dt/dx as dt * (1/dx))
+        red[17] = EX ? dt0 / a.dy : dt0 * a.idy;
+        red[18] = EX ? dt0 / a.dz : dt0 * a.idz;
         red[19] = dt0;
     }
     if (tid < S::TYM) red[24 + tid] = 1.0e32;
@@ -162,6 +175,18 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     double zp_prev[NV];
 #pragma unroll
     for (int q = 0; q < NV; ++q) zp_prev[q] = 0.0;
+    [[maybe_unused]] double fzb[NV];  // bit-exact build: the bottom z flux of the plane before
+    // the record of an edge zone of plane k (bit-exact build), entry stride in *es
+    [[maybe_unused]] auto edge_rec = [&](int k, int h, size_t& es) -> double* {
+        const int ci = ci_(), cj = cj_();
+        const int bx = blockIdx.x, by = blockIdx.y;
+        es = size_t(sa.nx);
+        if (cj == 0) return edge_y(sa, k, by, ia_(), 1);
+        if (cj == h - 1) return edge_y(sa, k, by + 1 == sa.nty ? 0 : by + 1, ia_(), 0);
+        es = size_t(sa.ny);
+        if (ci == 0) return edge_x(sa, k, bx, ja_(), 1);
+        return edge_x(sa, k, bx + 1 == sa.ntx ? 0 : bx + 1, ja_(), 0);
+    };
 
     for (int lp = -1; lp <= nzc; ++lp) {
         const int p = kz0 + lp;
@@ -235,28 +260,52 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                     const size_t zi = size_t(p - 1 + a.gh) * plane_stride +
                                       size_t(ja + a.gh) * a.pitch + size_t(ia + a.gh) * NV;
                     const double cz = red[18];
-                    double un[NV];
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) {
-                        // edge zones: provisional (seam_fix_x / _y add their seam fluxes).
-                        // cz B and cz T are rounded products (no contraction): equal z fluxes
-                        // then cancel exactly, as T - B does in the reference's association, so
-                        // a z-invariant state stays z-invariant bit for bit (w = 0 stays 0)
-                        const double v = __dsub_rn(acc[q * CS + tid], __dmul_rn(cz, fz[q]));
-                        if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
-                            un[q] = a.rk_a * sbuf[2][zi + q] + a.rk_b * v;
-                        else
-                            un[q] = v;
-                    }
-                    double* dst = sbuf[1] + zi;
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) dst[q] = un[q];
                     const bool edge = ci == 0 || ci == TX - 1 || cj == 0 || cj == h - 1;
+                    double un[NV];
+                    if constexpr (EX) {
+                        if (edge) {  // the z term for seam_fix_kernel; it writes the zone
+                            size_t es;
+                            double* er = edge_rec(p - 1, h, es);
+#pragma unroll
+                            for (int q = 0; q < NV; ++q)
+                                __stcg(er + (2 * NV + q) * es, cz * (fz[q] - fzb[q]));
+                        } else {  // corrector.cpp:89-90: (x part - y part) - cz (T - B)
+                            const double* u = P(p - 1) + zoff_();
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) {
+                                const double r = acc[q * CS + tid] - cz * (fz[q] - fzb[q]);
+                                if (RK)  // stepper.cpp:137
+                                    un[q] = a.rk_a * sbuf[2][zi + q] + a.rk_b * (u[q] + r);
+                                else
+                                    un[q] = u[q] + r;
+                            }
+                            double* dst = sbuf[1] + zi;
+#pragma unroll
+                            for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) {
+                            // edge zones: provisional (seam_fix_kernel adds the seam fluxes).
+                            // cz B and cz T are rounded products (no contraction): equal z
+                            // fluxes then cancel exactly, as T - B does in the reference's
+                            // association, so a z-invariant state stays z-invariant bit for bit
+                            const double v = __dsub_rn(acc[q * CS + tid], __dmul_rn(cz, fz[q]));
+                            if (RK)  // stepper.cpp:137 (u0 read before uout is written: may alias)
+                                un[q] = a.rk_a * sbuf[2][zi + q] + a.rk_b * v;
+                            else
+                                un[q] = v;
+                        }
+                        double* dst = sbuf[1] + zi;
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                    }
                     double dloc = 1.0e32;
                     if ((!RK || a.want_dt) && !edge) {
                         Fault f3;
                         f3.clear();
-                        double d = eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
+                        double d = EX ? eval_tstep<FM>(un, a.cfl, a.dx, a.dy, a.dz, a.gamma, f3)
+                                      : eval_tstep_inv<FM>(un, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
                         if (f3.redo()) {
                             V5 u5;
 #pragma unroll
@@ -274,9 +323,15 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                         if (ci == 0) red[24 + cj] = smin(red[24 + cj], dloc);
                     }
                 }
-                if (real)
+                if (real) {
+                    if constexpr (EX) {
 #pragma unroll
-                    for (int q = 0; q < NV; ++q) acc[q * CS + tid] = fz[q];  // parked for D
+                        for (int q = 0; q < NV; ++q) fzb[q] = fz[q];  // B of plane p
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < NV; ++q) acc[q * CS + tid] = fz[q];  // parked for C
+                    }
+                }
             }
 #pragma unroll
             for (int q = 0; q < NV; ++q) zp_prev[q] = st[4][q];
@@ -302,15 +357,21 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
 #pragma unroll
                     for (int q = 0; q < NV; ++q) fw[q] = 0.0;
                 }
-                const double cx = red[16], cz = red[18];
+                [[maybe_unused]] const double cx = red[16], cz = red[18];
                 const double* u = P(p) + zoff_();
 #pragma unroll
                 for (int q = 0; q < NV; ++q) {
                     double e = __shfl_down_sync(0xffffffffu, fw[q], 1);  // lane ci+1's west
                     if (ci == TX - 1) e = 0.0;                           // (a seam)
-                    const double xt = -cx * (e - fw[q]);
-                    // (cz B rounded, no contraction: see B)
-                    acc[q * CS + tid] = __dadd_rn(u[q] + xt, __dmul_rn(cz, acc[q * CS + tid]));
+                    if constexpr (EX) {  // the x part, or the interior x flux at a seam column
+                        acc[q * CS + tid] =
+                            ci == 0 ? e : (ci == TX - 1 ? fw[q] : -cx * (e - fw[q]));
+                    } else {
+                        const double xt = -cx * (e - fw[q]);
+                        // (cz B rounded, no contraction: see B)
+                        acc[q * CS + tid] =
+                            __dadd_rn(u[q] + xt, __dmul_rn(cz, acc[q * CS + tid]));
+                    }
                 }
             }
             double fs[NV];
@@ -333,11 +394,25 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
         // ---------------------------------------------- D: the y term of the accumulator
         if (cj < h) {
             const double cy = red[17];
+            if (EX && (ci == 0 || ci == TX - 1 || cj == 0 || cj == h - 1)) {
+                // an edge zone: its x and y parts go to the record (seam_fix_kernel)
+                size_t es;
+                double* er = edge_rec(p, h, es);
 #pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                const double sf = YPF[(cj * TX + ci) * NV + q];
-                const double nf = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
-                acc[q * CS + tid] -= cy * (nf - sf);
+                for (int q = 0; q < NV; ++q) {
+                    const double sf = YPF[(cj * TX + ci) * NV + q];
+                    const double nf = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
+                    const double y = cj == 0 ? nf : (cj == h - 1 ? sf : cy * (nf - sf));
+                    __stcg(er + q * es, acc[q * CS + tid]);
+                    __stcg(er + (NV + q) * es, y);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    const double sf = YPF[(cj * TX + ci) * NV + q];
+                    const double nf = cj < h - 1 ? YPF[((cj + 1) * TX + ci) * NV + q] : 0.0;
+                    acc[q * CS + tid] -= cy * (nf - sf);
+                }
             }
         }
     }
@@ -373,11 +448,19 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
     const int grp = bid < nby ? 0 : (bid < nby + nbx ? 1 : 2);  // Y, X, C
     const unsigned idx = unsigned(bid - (grp == 0 ? 0 : (grp == 1 ? nby : nby + nbx))) * 128u +
                          threadIdx.x;
+    constexpr bool EX = FM != 2;
     const int cur = a.ctl->cur;
     double* out = a.buf[(cur + a.out_rel) % a.nbuf];
+    [[maybe_unused]] const double* uin = a.buf[(cur + a.in_rel) % a.nbuf];
+    [[maybe_unused]] const double* u0 = a.buf[cur];
     const double dt0 = a.ctl->dt;
-    const double cx = RK ? a.rk_b * (dt0 * a.idx) : dt0 * a.idx;
-    const double cy = RK ? a.rk_b * (dt0 * a.idy) : dt0 * a.idy;
+    // FMA build: b folded into the provisional update's coefficients; bit-exact build: the
+    // reference's dt/dx and U' = a U0 + b (U + rate) (stepper.cpp:137)
+    const double cx = EX ? dt0 / a.dx : (RK ? a.rk_b * (dt0 * a.idx) : dt0 * a.idx);
+    const double cy = EX ? dt0 / a.dy : (RK ? a.rk_b * (dt0 * a.idy) : dt0 * a.idy);
+    auto fin = [&](size_t z, int q, double r) {
+        return RK ? a.rk_a * u0[z + q] + a.rk_b * (uin[z + q] + r) : uin[z + q] + r;
+    };
     auto zidx = [&](int i, int j) {
         return (size_t(p + a.gh) * a.my_pad + size_t(j + a.gh)) * a.pitch + size_t(i + a.gh) * NV;
     };
@@ -401,7 +484,8 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
         if (RK && !a.want_dt) return 1.0e32;
         Fault f3;
         f3.clear();
-        double d = eval_tstep_inv<FM>(v, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
+        double d = EX ? eval_tstep<FM>(v, a.cfl, a.dx, a.dy, a.dz, a.gamma, f3)
+                      : eval_tstep_inv<FM>(v, a.cfl, a.idx, a.idy, a.idz, a.gamma, f3);
         if (f3.redo()) {
             V5 u5;
 #pragma unroll
@@ -439,22 +523,46 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
                 }
                 const size_t zl = zidx(il, jl), zh = zidx(ih, jh);
                 double vl[NV], vh[NV], f5[NV];
+                if (!EX)
 #pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    vl[q] = out[zl + q];
-                    vh[q] = out[zh + q];
-                }
+                    for (int q = 0; q < NV; ++q) {
+                        vl[q] = out[zl + q];
+                        vh[q] = out[zh + q];
+                    }
                 if (grp == 1)
                     solve(seam_x(sa, p, sidx, l, 0), a.ny, 0, ih, jh, f5);
                 else
                     solve(seam_y(sa, p, sidx, l, 0), a.nx, 1, jh, ih, f5);
-                const double c = grp == 1 ? cx : cy;
+                if constexpr (EX) {
+                    // the whole rate of both zones in the reference's association
+                    // (corrector.cpp:89-90) from their records and the seam flux
+                    const size_t es = grp == 1 ? size_t(a.ny) : size_t(a.nx);
+                    const double* rl = grp == 1 ? edge_x(sa, p, sidx, l, 0) : edge_y(sa, p, sidx, l, 0);
+                    const double* rh = grp == 1 ? edge_x(sa, p, sidx, l, 1) : edge_y(sa, p, sidx, l, 1);
 #pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    vl[q] = vl[q] - c * f5[q];  // its east / north face
-                    vh[q] = vh[q] + c * f5[q];  // its west / south face
-                    out[zl + q] = vl[q];
-                    out[zh + q] = vh[q];
+                    for (int q = 0; q < NV; ++q) {
+                        double r_l, r_h;
+                        if (grp == 1) {  // x seam: E of the low zone, W of the high zone
+                            r_l = (-cx * (f5[q] - rl[q * es]) - rl[(NV + q) * es]) - rl[(2 * NV + q) * es];
+                            r_h = (-cx * (rh[q * es] - f5[q]) - rh[(NV + q) * es]) - rh[(2 * NV + q) * es];
+                        } else {  // y seam: N of the low zone, S of the high zone
+                            r_l = (rl[q * es] - cy * (f5[q] - rl[(NV + q) * es])) - rl[(2 * NV + q) * es];
+                            r_h = (rh[q * es] - cy * (rh[(NV + q) * es] - f5[q])) - rh[(2 * NV + q) * es];
+                        }
+                        vl[q] = fin(zl, q, r_l);
+                        vh[q] = fin(zh, q, r_h);
+                        out[zl + q] = vl[q];
+                        out[zh + q] = vh[q];
+                    }
+                } else {
+                    const double c = grp == 1 ? cx : cy;
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        vl[q] = vl[q] - c * f5[q];  // its east / north face
+                        vh[q] = vh[q] + c * f5[q];  // its west / south face
+                        out[zl + q] = vl[q];
+                        out[zh + q] = vh[q];
+                    }
                 }
                 dloc = smin(cfl(vl, il, jl), cfl(vh, ih, jh));
             }
@@ -469,17 +577,32 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
         const int j = y0 + (north ? h - 1 : 0);
         const size_t z = zidx(i, j);
         double v[NV], fx[NV], fy[NV];
+        if (!EX)
 #pragma unroll
-        for (int q = 0; q < NV; ++q) v[q] = out[z + q];
+            for (int q = 0; q < NV; ++q) v[q] = out[z + q];
         const int sx = east ? (bx + 1 == sa.ntx ? 0 : bx + 1) : bx;
         const int sy = north ? (by + 1 == sa.nty ? 0 : by + 1) : by;
         solve(seam_x(sa, p, sx, j, 0), a.ny, 0, east ? i + 1 : i, j, fx);
         solve(seam_y(sa, p, sy, i, 0), a.nx, 1, north ? j + 1 : j, i, fy);
-        const double sxs = east ? -cx : cx, sys = north ? -cy : cy;
+        if constexpr (EX) {
+            const size_t es = size_t(a.nx);
+            const double* rc = edge_y(sa, p, sy, i, north ? 0 : 1);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            v[q] = (v[q] + sxs * fx[q]) + sys * fy[q];
-            out[z + q] = v[q];
+            for (int q = 0; q < NV; ++q) {
+                const double xi = rc[q * es], yi = rc[(NV + q) * es];
+                const double e = east ? fx[q] : xi, w = east ? xi : fx[q];
+                const double n = north ? fy[q] : yi, s = north ? yi : fy[q];
+                const double r = (-cx * (e - w) - cy * (n - s)) - rc[(2 * NV + q) * es];
+                v[q] = fin(z, q, r);
+                out[z + q] = v[q];
+            }
+        } else {
+            const double sxs = east ? -cx : cx, sys = north ? -cy : cy;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                v[q] = (v[q] + sxs * fx[q]) + sys * fy[q];
+                out[z + q] = v[q];
+            }
         }
         dloc = cfl(v, i, j);
     }

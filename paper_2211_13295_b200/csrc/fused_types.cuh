@@ -96,7 +96,7 @@ struct PersistLaunch {
 inline int px_box_w(int order) { return PX_TX + 2 * (order >= 3 ? 3 : 2); }
 inline int px_box_h(int order) { return PX_TYM + 2 * (order >= 3 ? 2 : 1); }
 
-// ---- the ring-free seam kernel (fused_seam.cuh, FMA build): 32 x <=8 tiles, tile-boundary
+// ---- the ring-free seam kernel (fused_seam.cuh, both builds): 32 x <=8 tiles, tile-boundary
 // faces finished by seam_fix_kernel from the edge zones' published states
 constexpr int SEAM_TX = 32, SEAM_TYM = 8;
 struct SeamArgs {
@@ -105,11 +105,19 @@ struct SeamArgs {
     double* sy;               // [nz][nty][nx][2][5] states at the y seams
     int ntx, nty;             // tiles along x (nx / 32) and y (ceil(ny / 8), balanced rows)
     int nx, ny;
+    // bit-exact build only: the edge zones' rate parts, 3 x 5 per zone (x part, y part, z
+    // term; see fused_seam.cuh), for the y-edge rows [nz][nty][2][15][nx] and the x-edge
+    // columns of the other rows [nz][ntx][2][15][ny]
+    double* ey;
+    double* ex;
 };
 // Both kernels of one seam step (or RK stage) over a.kz_first..a.kz_last; blocks_per_sm !=
 // nullptr: only report the fused kernel's resident CTAs per SM.
 int launch_seam_fast(const FusedArgs& a, const SeamArgs& s, int order, int solver, bool rk,
                      cudaStream_t st, int* blocks_per_sm = nullptr);
+// the same pair in the bit-exact build (reference association of the rate, --fmad=false)
+int launch_seam_exact(const FusedArgs& a, const SeamArgs& s, int order, int solver, bool rk,
+                      cudaStream_t st, int* blocks_per_sm = nullptr);
 
 // pl == nullptr: the ring kernel (fused_ader.cuh); else the persistent ring-free kernel
 // (fused_persist.cuh) with these exchange buffers and tensor maps. persist_blocks_per_sm !=

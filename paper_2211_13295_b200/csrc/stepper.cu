@@ -302,15 +302,22 @@ static int encode_maps(hc_stepper* s, int box_rows) {
     return HC_OK;
 }
 
-// Enables the ring-free seam kernel pair (fused_seam.cuh) for the FMA build when the mesh
-// allows it: x and y periodic (the zone across the mesh edge is the last tile's edge zone),
-// nx a multiple of 32, storage ghosts equal to the kernel's x halo and an even row pitch (TMA
-// box origins on 16-byte boundaries). HC_SEAM=0 keeps the ring kernel.
+static int launch_seam(const hc_stepper* s, const FusedArgs& a, const SeamArgs& sa, bool rk,
+                       cudaStream_t st, int* bps = nullptr) {
+    return s->o.exact ? launch_seam_exact(a, sa, s->p.order, s->p.solver, rk, st, bps)
+                      : launch_seam_fast(a, sa, s->p.order, s->p.solver, rk, st, bps);
+}
+
+// Enables the ring-free seam kernel pair (fused_seam.cuh) when the mesh allows it: x and y
+// periodic (the zone across the mesh edge is the last tile's edge zone), nx a multiple of 32,
+// ny >= 2 (every tile has two rows), storage ghosts equal to the kernel's x halo and an even
+// row pitch (TMA box origins on 16-byte boundaries). Both builds; the bit-exact one also keeps
+// the edge zones' rate parts (SeamArgs ex / ey). HC_SEAM=0 keeps the ring kernel.
 static int setup_seam(hc_stepper* s) {
     if (const char* v = std::getenv("HC_SEAM"))
         if (std::atoi(v) == 0) return HC_OK;
     const hc_geom& g = s->g;
-    if (s->o.exact || s->persist) return HC_OK;
+    if (s->persist || g.ny < 2) return HC_OK;
     if (s->o.bc[0] != HC_PERIODIC || s->o.bc[1] != HC_PERIODIC) return HC_OK;
     if (g.nx % SEAM_TX || (s->sg.pitch & 1) || g.ghost != (s->p.order >= 3 ? 3 : 2)) return HC_OK;
     const bool rk = s->o.integrator != 0;
@@ -320,7 +327,7 @@ static int setup_seam(hc_stepper* s) {
     sa.ny = g.ny;
     sa.ntx = g.nx / SEAM_TX;
     sa.nty = (g.ny + SEAM_TYM - 1) / SEAM_TYM;
-    int rc = launch_seam_fast(fused_args(s), sa, s->p.order, s->p.solver, rk, nullptr, &bps);
+    int rc = launch_seam(s, fused_args(s), sa, rk, nullptr, &bps);
     if (rc) return rc;
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->o.device));
     if (bps < 1) return HC_OK;
@@ -333,6 +340,13 @@ static int setup_seam(hc_stepper* s) {
     HC_CUDA(cudaMalloc(&sa.sy, nsy * sizeof(double)));
     HC_CUDA(cudaMemsetAsync(sa.sx, 0, nsx * sizeof(double), s->st));
     HC_CUDA(cudaMemsetAsync(sa.sy, 0, nsy * sizeof(double), s->st));
+    sa.ex = sa.ey = nullptr;
+    if (s->o.exact) {
+        const size_t nex = size_t(g.nz) * sa.ntx * g.ny * 2 * 3 * NV;
+        const size_t ney = size_t(g.nz) * sa.nty * g.nx * 2 * 3 * NV;
+        HC_CUDA(cudaMalloc(&sa.ex, nex * sizeof(double)));
+        HC_CUDA(cudaMalloc(&sa.ey, ney * sizeof(double)));
+    }
     s->seam = true;
     return HC_OK;
 }
@@ -485,6 +499,8 @@ int hc_stepper_destroy(hc_stepper* s) {
     cudaFree(s->pl.args.hdr);
     cudaFree(s->sa.sx);
     cudaFree(s->sa.sy);
+    cudaFree(s->sa.ex);
+    cudaFree(s->sa.ey);
     cudaFree(s->maps);  // (the persistent kernel's maps are these)
     for (cudaEvent_t e : s->ev) cudaEventDestroy(e);
     if (s->graph) cudaGraphExecDestroy(s->graph);
@@ -595,7 +611,7 @@ static int launch_step(hc_stepper* s, FusedArgs a, bool rk, cudaStream_t st) {
     int rc;
     if (s->seam) {
         a.tz = s->seam_tz;
-        if ((rc = launch_seam_fast(a, s->sa, s->p.order, s->p.solver, rk, st))) return rc;
+        if ((rc = launch_seam(s, a, s->sa, rk, st))) return rc;
         s->launches += 2;
         return HC_OK;
     }

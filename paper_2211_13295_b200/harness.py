@@ -75,6 +75,7 @@ class RunResult:
     wall_seconds: float
     zones_per_sec: float
     errors: ErrorReport | None
+    kernel: str = ""  # the fused step that ran: "seam", "ring" or "persistent" ("" PatchSet)
 
 
 def default_domain(problem):
@@ -159,6 +160,7 @@ def run_simulation(cfg: RunConfig) -> RunResult:
                 break
     wall = time.perf_counter() - t0
     out = st.gather() if isinstance(st, hydro.PatchSet) else st.download()
+    kernel = "" if isinstance(st, hydro.PatchSet) else st.kernel_info()[0]
     st.close()
     gh = g.ghost
     # the reference gathers active zones into a fresh SkinnyState (ghosts zero)
@@ -172,7 +174,7 @@ def run_simulation(cfg: RunConfig) -> RunResult:
     elif cfg.problem == CONSTANT:
         errors = error_norms(final, api.init_constant(g, cfg.gamma), g)
     zps = g.nx * g.ny * g.nz * done / wall if wall > 0 else 0.0
-    return RunResult(final, g, done, t, wall, zps, errors)
+    return RunResult(final, g, done, t, wall, zps, errors, kernel)
 
 
 def run_benchmark(cfg: RunConfig) -> RunResult:

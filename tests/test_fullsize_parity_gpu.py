@@ -81,7 +81,8 @@ def test_reference_harness_at_full_size(ref, name):
         l1, linf = _rel_norms(a, b)
         nbad = int((a.view(np.uint64) != b.view(np.uint64)).sum())
         key = "exact" if exact else "fma"
-        entry[key] = {"t": r.t_end.hex(), "steps": r.steps, "rel_l1": l1.tolist(),
+        entry[key] = {"kernel": r.kernel, "t": r.t_end.hex(), "steps": r.steps,
+                      "rel_l1": l1.tolist(),
                       "rel_linf": linf.tolist(), "differing_values": nbad,
                       "values": int(a.size)}
         _record(name, entry)

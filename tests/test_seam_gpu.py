@@ -1,8 +1,9 @@
-"""The ring-free seam kernel pair of the FMA build (csrc/fused_seam.cuh: the fused step with
-tile-boundary faces left out, then seam_fix_kernel) against the C restatement of the
-reference (oracle/) within the FMA build's tolerance, against the FMA ring kernel
-(HC_SEAM=0), and for the properties the re-association must keep: conservation to round-off
-on a periodic mesh, z-range launches equal to the whole launch, the pipelined host step."""
+"""The ring-free seam kernel pair (csrc/fused_seam.cuh: the fused step with tile-boundary
+faces left out, then seam_fix_kernel) against the C restatement of the reference (oracle/):
+the FMA build within its tolerance, the bit-exact build (the reference's association kept
+through the edge zones' records) bit for bit; against the ring kernels (HC_SEAM=0), and for
+the properties the FMA build's re-association must keep: conservation to round-off on a
+periodic mesh, z-range launches equal to the whole launch, the pipelined host step."""
 import os
 
 import numpy as np
@@ -105,9 +106,12 @@ def test_seam_kernel_vs_reference(env, order, solver, integ, shape):
     act = _act(g)
     assert max(_rel_l1(out[act], ref[act])) <= TOL
     assert abs(dt_next - dt_last) <= 1e-12 * dt_last
-    # the exact build never takes the seam kernel (its association is the reference's)
-    _, _, _, kx = _run(g, order, solver, integ, s0, dt0, cfl, 1, exact=True)
-    assert kx[0] == "ring"
+    # the bit-exact build's seam pair: every bit of the reference's state and dt
+    x, dx_next, xdone, kx = _run(g, order, solver, integ, s0, dt0, cfl, steps, exact=True)
+    assert kx[0] == "seam" and xdone == steps
+    assert (x[act].view(np.uint64) == ref[act].view(np.uint64)).all(), \
+        np.abs(x[act] - ref[act]).max()
+    assert dx_next == dt_last
 
 
 def test_seam_equals_fma_ring_kernel(env):
@@ -201,8 +205,30 @@ def test_seam_configs0(env):
     s0 = api.init_isentropic_vortex(g, order)
     dt0 = api.initial_dt(g, s0, 0.4)
     a, da, _, ka = _run(g, order, hydro.HLL, hydro.ADER, s0, dt0, 0.4, 50)
+    env["HC_SEAM"] = "0"
     b, db, _, kb = _run(g, order, hydro.HLL, hydro.ADER, s0, dt0, 0.4, 50, exact=True)
     assert ka[0] == "seam" and kb[0] == "ring"
     act = _act(g)
     assert max(_rel_l1(a[act], b[act])) <= TOL
     assert abs(da - db) <= 1e-12 * db
+
+
+@pytest.mark.parametrize("order,solver,integ,shape", [
+    (3, hydro.HLL, hydro.ADER, (64, 24, 10)),
+    (2, hydro.RUSANOV, hydro.RK2, (32, 17, 6)),
+    (3, hydro.HLLC, hydro.RK3, (96, 12, 5)),
+])
+def test_seam_exact_equals_exact_ring(env, order, solver, integ, shape):
+    """the bit-exact build's seam pair and its ring kernel (HC_SEAM=0) agree to the last bit
+    (both keep the reference's association), state and dt, over 8 steps"""
+    api = hydro.HostApi()
+    g = hydro.make_geometry(*shape, order)
+    s0 = modulate_z(api.init_isentropic_vortex(g, order))
+    dt0 = api.initial_dt(g, s0, 0.4)
+    a, da, _, ka = _run(g, order, solver, integ, s0, dt0, 0.4, 8, exact=True)
+    env["HC_SEAM"] = "0"
+    b, db, _, kb = _run(g, order, solver, integ, s0, dt0, 0.4, 8, exact=True)
+    assert ka[0] == "seam" and kb[0] == "ring"
+    act = _act(g)
+    assert (a[act].view(np.uint64) == b[act].view(np.uint64)).all(), np.abs(a - b).max()
+    assert da == db

@@ -1,4 +1,4 @@
-// fused_seam.cuh -- the ring-free fused ADER step of the FMA build: the same update as
+// fused_seam.cuh -- the ring-free fused ADER step (both builds): the same update as
 // fused_ader.cuh (reconstruction -> ADER predictor -> face Riemann fluxes -> flux
 // differencing -> update -> CFL min; stepper.cpp:49-78, predictor.cpp:26-91,
 // corrector.cpp:15-125) with no redundant zone work and no waiting between CTAs.
@@ -22,11 +22,14 @@
 //    one shared-memory array; planes arrive by TMA tensor copies (one box per plane, per-slot
 //    mbarrier), as in fused_persist.cuh.
 //
-// The provisional form U + (r_partial - cz (T - B)) followed by + cx W - cx E + cy S - cy N
-// re-associates the reference's rate (corrector.cpp:89-90), so this kernel belongs to the FMA
-// build only (tolerance-tested against the reference, like the FMA ring kernel). Periodic x
-// and y only (the zone across the mesh edge is the last tile's own edge zone); other meshes
-// and the bit-exact build run fused_ader.cuh.
+// FMA build: the provisional form U + (r_partial - cz (T - B)) followed by + cx W - cx E +
+// cy S - cy N re-associates the reference's rate (corrector.cpp:89-90) (tolerance-tested
+// against the reference, like the FMA ring kernel). Bit-exact build (EX): the reference's
+// association throughout -- interior zones finish as U + ((-cx (E - W) - cy (N - S)) -
+// cz (T - B)) with the bottom z flux carried in registers; an edge zone publishes its rate
+// parts (edge_x / edge_y records) and seam_fix_kernel evaluates its whole rate in the same
+// order. Periodic x and y only (the zone across the mesh edge is the last tile's own edge
+// zone); other meshes run fused_ader.cuh.
 #pragma once
 
 #include "fused_persist.cuh"

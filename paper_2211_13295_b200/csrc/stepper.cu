@@ -137,7 +137,7 @@ struct hc_stepper {
     // the persistent ring-free kernel (fused_persist.cuh), when the mesh allows it
     bool persist = false;
     PersistLaunch pl{};
-    // the ring-free seam kernel pair (fused_seam.cuh; FMA build, x/y periodic, nx % 32 == 0)
+    // the ring-free seam kernel pair (fused_seam.cuh; both builds, x/y periodic, nx % 32 == 0)
     bool seam = false;
     SeamArgs sa{};
     int seam_tz = 32;
@@ -1083,7 +1083,7 @@ int hc_patchset_create(const hc_geom* global, int px, int py, int pz, const hc_p
                 g.origin[1] = global->origin[1] + pj * lny * global->dy;
                 g.origin[2] = global->origin[2] + pk * lnz * global->dz;
                 // a single patch owns its boundaries (its ghost fill is exchange_ghosts for
-                // one patch, and the FMA build can take the ring-free seam kernel); several
+                // one patch, and it can take the ring-free seam kernel); several
                 // patches have every ghost filled by the exchange gather
                 const int b = px * py * pz == 1 ? boundary : -1;
                 hc_stepper_opts o = {{b, b, b}, exact, device, integrator};

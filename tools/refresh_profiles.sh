@@ -1,6 +1,6 @@
 # Headline evidence in one gpurun call: the bench line; ncu --set full of one step's compute
-# launches in the FMA build (the seam kernel pair: seam_ader_kernel + the x and y seam fixes)
-# and of the bit-exact build's ring kernel (256^3 O3 HLL); the serialised launch list of the
+# launches in both builds (the seam kernel pair: seam_ader_kernel + seam_fix_kernel; the
+# bit-exact build's pair keeps the reference's association) at 256^3 O3 HLL; the serialised launch list of the
 # timed steps. The captures are summarised on the box (profiles/summarize.py -> gpurun_out/
 # r2_*.json) and the .ncu-rep files dropped so the results fit the 64 MiB copy-back.
 # Usage: gpurun -- 'bash tools/refresh_profiles.sh'; copy gpurun_out/r2_*.json to profiles/.
@@ -10,7 +10,7 @@ python bench.py > gpurun_out/bench_o3_256.json 2> gpurun_out/bench.err
 ncu --set full --import-source on --clock-control none -k regex:seam_ -s 8 -c 2 \
     -o /tmp/fused_o3_256_fma -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     --only-timed > gpurun_out/ncu_fma.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:fused_ader -s 3 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:seam_ -s 8 -c 2 \
     -o /tmp/fused_o3_256_exact -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     --only-timed --exact > gpurun_out/ncu_exact.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \

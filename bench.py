@@ -352,7 +352,7 @@ def bench_mhd(args):
     for _ in range(ee):
         st.upload(host)
         step()
-        host[...] = st.download()
+        st.download(host)
     e2e_s = (time.perf_counter() - h0) / ee
     if world > 1:
         te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -441,6 +441,18 @@ def bench_ced(args):
     zones = n ** 3
     divb, divd = st.max_div()
     roofline = ext_roofline("ced", order, n, ms / args.steps, 104.0, clocks.max_mhz)
+    # end to end through the public API with host buffers (H2D state + conductivity, step, D2H)
+    host = torch.empty(s0.shape, dtype=torch.float64, pin_memory=True).numpy()
+    host[...] = s0
+    hsig = torch.empty(sigma.shape, dtype=torch.float64, pin_memory=True).numpy()
+    hsig[...] = sigma
+    h0 = time.perf_counter()
+    ee = 2
+    for _ in range(ee):
+        st.upload(host, hsig)
+        st.step(1)
+        st.download(host)
+    e2e_s = (time.perf_counter() - h0) / ee
     line = {
         "metric": METRIC, "value": zones * args.steps / (ms * 1e-3) / 1e6, "unit": UNIT,
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -452,7 +464,11 @@ def bench_ced(args):
                    "n": n, "order": order, "build": "bit-exact (--fmad=false)",
                    "parallelism": "single GPU"},
         "roofline": roofline,
-        "cpu_baseline": None, "gpu_launches": launches, "clocks": clocks.summary(),
+        "cpu_baseline": None,
+        "e2e": {"value": zones / e2e_s / 1e6, "unit": UNIT,
+                "h2d_bytes_per_step": host.nbytes + hsig.nbytes, "d2h_bytes_per_step": host.nbytes,
+                "api": "hc_ced_upload + hc_ced_step + hc_ced_download (host wall clock)"},
+        "gpu_launches": launches, "clocks": clocks.summary(),
         "final": {"t": t, "steps_done": done, "max_divb": divb, "max_divd": divd},
     }
     st.close()

@@ -92,8 +92,12 @@ class CedStepper:
         assert s.shape == (NF,) + box_shape(self.g)
         _check(self.lib.hc_ced_upload(self.h, _p(s), _p(sigma)))
 
-    def download(self):
-        out = np.empty((NF,) + box_shape(self.g))
+    def download(self, out=None):
+        """the device state; into `out` (e.g. a pinned buffer) when given"""
+        if out is None:
+            out = np.empty((NF,) + box_shape(self.g))
+        assert out.shape == (NF,) + box_shape(self.g) and out.dtype == np.float64
+        assert out.flags.c_contiguous
         _check(self.lib.hc_ced_download(self.h, _p(out)))
         return out
 

@@ -89,8 +89,12 @@ class MhdStepper:
         assert s.shape == state_shape(self.g), (s.shape, state_shape(self.g))
         _check(self.lib.hc_mhd_upload(self.h, _p(s)))
 
-    def download(self):
-        out = np.empty(state_shape(self.g))
+    def download(self, out=None):
+        """the device state; into `out` (e.g. a pinned buffer) when given"""
+        if out is None:
+            out = np.empty(state_shape(self.g))
+        assert out.shape == state_shape(self.g) and out.dtype == np.float64
+        assert out.flags.c_contiguous
         _check(self.lib.hc_mhd_download(self.h, _p(out)))
         return out
 

@@ -147,7 +147,10 @@ def mesh_of(args):
     return (128, 128, 4) if args.workload == "c1" else (args.n, args.n, args.n)
 
 
-def run_reference_cpu(n, order, steps, threads):
+INTEGRATORS = {"ader": 0, "rk2": 2, "rk3": 3}  # IntegratorChoice codes (predictor.hpp:12)
+
+
+def run_reference_cpu(n, order, steps, threads, integrator=0):
     """The reference's own harness (hydro::run_benchmark, harness.cpp:222-227) from
     oracle/_ref (built from /root/reference/proj/src); zones/s as it computes it
     (harness.cpp:177-180). Falls back to the C restatement (single thread) if absent."""
@@ -156,8 +159,10 @@ def run_reference_cpu(n, order, steps, threads):
     from oracle import pyoracle as po
     if po.have_reference():
         ref = po.Reference()
-        zps, _, _, _ = ref.run_benchmark(0, order, 0, 1, n, steps, threads=threads)
+        zps, _, _, _ = ref.run_benchmark(0, order, integrator, 1, n, steps, threads=threads)
         return zps, "reference", threads
+    if integrator:
+        raise RuntimeError("the C restatement fallback times ADER only (oracle/_ref missing)")
     orc = po.Oracle()
     nx, ny, nz = (n, n, n) if isinstance(n, int) else n
     g = po.make_geometry(nx, ny, nz, order)
@@ -180,10 +185,11 @@ def reference_arm(args):
     zones = mesh[0] * mesh[1] * mesh[2]
     # W warm-up steps (untimed; they also measure the step cost), then up to K timed steps,
     # capped so the timed part stays near 2 minutes of host time
-    zps1, kind, cores = run_reference_cpu(mesh, order, max(1, args.warmup), threads)
+    integ = INTEGRATORS[args.integrator]
+    zps1, kind, cores = run_reference_cpu(mesh, order, max(1, args.warmup), threads, integ)
     step_s = zones / zps1
     steps = max(1, min(args.steps, int(120.0 / max(step_s, 1e-3))))
-    zps, kind, cores = run_reference_cpu(mesh, order, steps, threads)
+    zps, kind, cores = run_reference_cpu(mesh, order, steps, threads, integ)
     val = zps / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
@@ -195,7 +201,8 @@ def reference_arm(args):
                   "-ffp-contract=off -fopenmp, its own sources)")
                  if kind == "reference" else "C restatement (oracle/, single thread)",
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{'x'.join(map(str, mesh))} O{order} HLL ADER vortex, "
+                         "sample": f"{'x'.join(map(str, mesh))} O{order} HLL "
+                                   f"{args.integrator.upper()} vortex, "
                                    f"{steps} timed steps (of K={args.steps} requested, capped "
                                    "at ~120 s) via hydro::run_benchmark on the host cores"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -215,11 +222,14 @@ def workload_config(args):
             "l2": "state 7.2 MB fits L2: launch/latency-bound (absolute rate only)",
             "parallelism": f"{args.gpus} independent replicas" if args.gpus > 1
             else "single GPU"}
+    scheme = (f"WENO-ADER O{args.order}" if args.integrator == "ader" else
+              f"WENO O{args.order} + {args.integrator.upper()} (no ADER predictor; the paper's "
+              "CFD RK row)")
     return {
-        "workload": (f"C2: 3D Euler isentropic vortex {args.n}^3 per GPU, WENO-ADER O{args.order}"
+        "workload": (f"C2: 3D Euler isentropic vortex {args.n}^3 per GPU, {scheme}"
                      " + HLL, periodic (configs[1]; the reference has no O4, O3 is its closest"
                      "; --order 4 runs the WENO-AO extension)"),
-        "n": args.n, "order": args.order, "solver": "hll", "integrator": "ader",
+        "n": args.n, "order": args.order, "solver": "hll", "integrator": args.integrator,
         "problem": "vortex",
         "l2": "state 2 x {:.0f} MB per GPU > 126 MB L2 (no flush needed)".format(
             (args.n + 2 * args.order) ** 3 * 40 / 1e6),
@@ -566,6 +576,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--integrator", default="ader", choices=list(INTEGRATORS),
+                    help="ader (the reference's one-step ADER, the headline) or the reference's "
+                         "rk2 / rk3 (stepper.cpp rk_step; the paper's CFD RK row)")
     ap.add_argument("--exact", action="store_true",
                     help="headline the bit-exact build (default: the FMA build, <= 1e-12 rel. L1)")
     ap.add_argument("--fast", action="store_true", help=argparse.SUPPRESS)  # (the default)
@@ -635,7 +648,7 @@ def main():
             return slabs.SlabDomain(128, 128, 4, order, rank=0, world=1, device=local,
                                     exact=exact, dz=2.5)
         return slabs.SlabDomain(n, n, n * world, order, rank=rank, world=world, device=local,
-                                exact=exact)
+                                exact=exact, integrator=INTEGRATORS[args.integrator])
 
     def max_ranks(v):
         if world == 1:
@@ -689,6 +702,12 @@ def main():
     # the nominal DFMA rate at the maximum SM clock (MEASURED_PEAKS.json has no FP64 figure);
     # the in-run DFMA probe (hc_fp64_peak) and the clock it ran at are reported beside it.
     fpz = flops_per_zone(mesh[0], order, 1, mesh[1], mesh[2])
+    fpz_source = "SURVEY.md App. A: the reference's ADER step as written (dynamic count)"
+    if args.integrator != "ader":  # executed FP64 flops of the RK step's launches (ncu)
+        with open(os.path.join(ROOT, "profiles", "r2_rk_flops.json")) as f:
+            fpz = json.load(f)[f"{args.integrator}_o{order}"]["flops_per_zone_step"]
+        fpz_source = ("profiles/r2_rk_flops.json: EXECUTED FP64 flops (DADD + DMUL + 2 DFMA, "
+                      "ncu, 128^3) of one RK step's compute launches, FMA build")
     with ClockSampler(local) as pclk:
         probe_fp64 = hydro.fp64_peak(local)
     max_mhz = clocks.max_mhz or pclk.max_mhz or 1965
@@ -712,7 +731,7 @@ def main():
                        "frac": achieved / probe_fp64,
                        "source": "hc_fp64_peak: 16 DFMA chains per thread, 32 warps per SM, "
                                  "best of 10 launches, this process"},
-        "flops_per_zone": fpz, "kernel_ms_per_launch": kern_ms,
+        "flops_per_zone": fpz, "flops_source": fpz_source, "kernel_ms_per_launch": kern_ms,
         "kernel": kernel_desc,
         "traffic": None,
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -724,14 +743,14 @@ def main():
                         f"r2_fused_o{order}_{n}_{'fma' if args.fast else 'exact'}.json")
     if not os.path.exists(prof):
         prof = prof.replace("r2_", "r1_")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.integrator == "ader":
         with open(prof) as f:
             k0 = json.load(f)["kernels"][0]
         roofline["fp64_pipe_busy_ncu"] = k0.get("fp64_pipe_pct", 0.0) / 100.0
         roofline["fp64_pipe_source"] = (os.path.relpath(prof, ROOT) + " (ncu --set full, "
                                         "sm__pipe_fp64_cycles_active, one launch)")
     traffic = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic):
+    if os.path.exists(traffic) and args.integrator == "ader":
         with open(traffic) as f:
             tj = json.load(f).get(f"n{n}_o{order}_{'fma' if args.fast else 'exact'}")
         if tj:

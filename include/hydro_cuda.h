@@ -239,6 +239,16 @@ int hc_stepper_layout(hc_stepper* s, int* my_pad, int* pitch, int* mz);
  * halo exchanges asynchronously track it as the steps flip it (ADER: every step; RK: never,
  * stage k reads buffer (cur + k) % nbuf). */
 int hc_stepper_buffers(hc_stepper* s, double** bufs, int* nbuf);
+/* z peer stores, for a stepper with caller-filled z ghosts (bc[2] = -1): from now on every
+ * fused step (or RK stage) also writes the final state of its gh lowest active planes into the
+ * top ghost planes (gh + nz + k) of lo_bufs[b], and of its gh highest into the bottom ghost
+ * planes of hi_bufs[b] -- b = the buffer the step writes, the arrays being the z neighbours'
+ * hc_stepper_buffers (same layout; on this device or a peer-accessible one, the caller having
+ * enabled peer access). The neighbours' z halos then arrive with the compute: no exchange
+ * step; hc_stepper_fill_ghosts fills the x/y ring of the z-ghost planes too. The caller orders
+ * the steps of neighbouring steppers (a neighbour's step n + 1 starts after this step n).
+ * lo_bufs or hi_bufs NULL: no neighbour on that side (an outflow end). */
+int hc_stepper_set_zpeer(hc_stepper* s, double* const* lo_bufs, double* const* hi_bufs);
 
 /* ------------------------------------------------ device-resident patch set
  * PatchSet (transfer.hpp:47-73) with the patches' states resident in HBM: px x py x pz
@@ -302,14 +312,18 @@ int hc_ader4_stream(hc_ader4* s, void** stream);
  * to the single domain. NCCL is opened at run time (libnccl.so.2). */
 typedef struct hc_domain hc_domain;
 
-typedef enum { HC_XCHG_NCCL = 0, HC_XCHG_PEER = 1 } hc_exchange_kind;
+/* HC_XCHG_STORE: the fused kernels store their boundary planes straight into the neighbours'
+ * ghost planes (hc_stepper_set_zpeer, NVLink peer memory): the halo transfer rides on the
+ * compute, no exchange step; hc_domain_create_local only (every slab in this process). */
+typedef enum { HC_XCHG_NCCL = 0, HC_XCHG_PEER = 1, HC_XCHG_STORE = 2 } hc_exchange_kind;
 
 typedef struct {
     int bc[3];       /* per axis HC_PERIODIC / HC_OUTFLOW (z: the global ends) */
     int exact;       /* as hc_stepper_opts */
     int integrator;  /* as hc_stepper_opts */
     int device;      /* hc_domain_create: this rank's GPU */
-    int transport;   /* hc_exchange_kind; HC_XCHG_PEER only with hc_domain_create_local */
+    int transport;   /* hc_exchange_kind; HC_XCHG_PEER / _STORE only with hc_domain_create_local
+                      * (_STORE: `overlap` has nothing to overlap and is ignored) */
     int overlap;     /* 1: the halo exchange runs on a second stream while the interior planes
                       * (whose stencils never reach a z ghost) are updated; then the two
                       * boundary ranges. 0: exchange, then the whole slab. Same bits. */

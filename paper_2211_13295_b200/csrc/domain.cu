@@ -128,6 +128,7 @@ struct hc_domain {
     int pitch = 0;
     std::vector<Slab> s;  // the slabs this process drives
     int cur = 0;          // host-tracked current buffer (the steppers flip it on the device)
+    bool primed = false;  // (store transport) the z ghosts of the current state are in place
     bool nccl_owned = false;
     double** peer_accs = nullptr;  // (peer transport) device array of the slabs' dt accumulators
 };
@@ -157,7 +158,8 @@ int check_args(const hc_geom* g, const hc_params* p, const hc_domain_opts* o, in
         set_error(HC_INVALID, "patch must have at least 4 zones per axis");
         return HC_INVALID;
     }
-    if (o->transport != HC_XCHG_NCCL && o->transport != HC_XCHG_PEER) {
+    if (o->transport != HC_XCHG_NCCL && o->transport != HC_XCHG_PEER &&
+        o->transport != HC_XCHG_STORE) {
         set_error(HC_INVALID, "hc_domain: unknown transport");
         return HC_INVALID;
     }
@@ -205,6 +207,41 @@ int common_init(hc_domain* d, const hc_geom* g, const hc_params* p, const hc_dom
     d->world = world;
     d->nloc = g->nz / world;
     d->gh = g->ghost;
+    return HC_OK;
+}
+
+int outflow_ends(hc_domain* d, int b, bool xs);
+
+// every slab's stream waits for the work enqueued so far on every other slab's stream
+int barrier_all(hc_domain* d) {
+    std::vector<cudaEvent_t> ev(d->s.size());
+    for (size_t i = 0; i < d->s.size(); ++i) {
+        HC_CUDA(cudaSetDevice(d->s[i].device));
+        HC_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventRecord(ev[i], d->s[i].stream));
+    }
+    for (size_t i = 0; i < d->s.size(); ++i) {
+        HC_CUDA(cudaSetDevice(d->s[i].device));
+        for (size_t j = 0; j < d->s.size(); ++j)
+            if (j != i) HC_CUDA(cudaStreamWaitEvent(d->s[i].stream, ev[j], 0));
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    return HC_OK;
+}
+
+// store transport: every slab's fused kernels write their boundary planes into the z
+// neighbours' ghost planes (hc_stepper_set_zpeer); an outflow end has no neighbour
+int setup_store(hc_domain* d) {
+    const bool periodic = d->o.bc[2] == HC_PERIODIC;
+    const int W = d->world;
+    for (Slab& x : d->s) {
+        const int lo = x.rank > 0 ? x.rank - 1 : (periodic ? W - 1 : -1);
+        const int hi = x.rank < W - 1 ? x.rank + 1 : (periodic ? 0 : -1);
+        const Slab* yl = lo >= 0 ? &d->s[size_t(lo)] : nullptr;
+        const Slab* yh = hi >= 0 ? &d->s[size_t(hi)] : nullptr;
+        int rc = hc_stepper_set_zpeer(x.st, yl ? yl->buf : nullptr, yh ? yh->buf : nullptr);
+        if (rc) return rc;
+    }
     return HC_OK;
 }
 
@@ -275,8 +312,14 @@ int exchange(hc_domain* d, int b, bool xs) {
         }
         for (size_t i = 0; i < d->s.size(); ++i) cudaEventDestroy(ev[i]);
     }
-    // outflow ends: the ghost planes repeat the edge active plane (boundary.cpp map_index)
-    if (!periodic) {
+    return outflow_ends(d, b, xs);
+}
+
+// outflow ends: the ghost planes repeat the edge active plane (boundary.cpp map_index)
+int outflow_ends(hc_domain* d, int b, bool xs) {
+    auto S = [&](const Slab& x) { return xs ? x.xstream : x.stream; };
+    const int gh = d->gh, nl = d->nloc, W = d->world;
+    if (d->o.bc[2] != HC_PERIODIC) {
         for (Slab& x : d->s) {
             HC_CUDA(cudaSetDevice(x.device));
             for (int k = 0; k < gh; ++k) {
@@ -334,12 +377,26 @@ int one_step(hc_domain* d) {
     int rc;
     const int ns = d->s.empty() ? 1 : hc_stepper_stages(d->s[0].st);
     const int nbuf = d->s.empty() ? 2 : d->s[0].nbuf;
+    const bool store = d->o.transport == HC_XCHG_STORE;
     for (int k = 0; k < ns; ++k) {
+        // store transport: the neighbours' previous stage (their stores into this slab's
+        // ghost planes, their reads of the buffer this stage stores into) is complete
+        if (store && d->s.size() > 1 && (rc = barrier_all(d))) return rc;
         for (Slab& x : d->s) {
             if ((rc = set_dev(x.device)) || (rc = hc_stepper_fill_ghosts(x.st))) return rc;
         }
         // the buffer this stage reads: cur (ADER, RK stage 0) or the previous stage's result
         const int b = (d->cur + (d->o.integrator ? k : 0)) % nbuf;
+        if (store) {
+            // the z ghosts arrived with the previous stage's compute; the first stage after a
+            // scatter takes them by peer copies
+            if ((rc = d->primed ? outflow_ends(d, b, false) : exchange(d, b, false))) return rc;
+            d->primed = true;
+            for (Slab& x : d->s) {
+                if ((rc = set_dev(x.device)) || (rc = hc_stepper_compute(x.st))) return rc;
+            }
+            continue;
+        }
         const int G = d->gh;  // planes whose stencils reach a z ghost plane, on each side
         if (!d->o.overlap || d->nloc <= 2 * G) {
             if ((rc = exchange(d, b, false))) return rc;
@@ -420,8 +477,8 @@ int hc_domain_create(const hc_geom* global, const hc_params* p, const hc_domain_
         set_error(HC_INVALID, "hc_domain_create: bad rank, world or NCCL id");
         return HC_INVALID;
     }
-    if (o->transport == HC_XCHG_PEER && world > 1) {
-        set_error(HC_INVALID, "the peer transport needs every slab in one process "
+    if (o->transport != HC_XCHG_NCCL && world > 1) {
+        set_error(HC_INVALID, "the peer and store transports need every slab in one process "
                               "(hc_domain_create_local)");
         return HC_INVALID;
     }
@@ -452,6 +509,10 @@ int hc_domain_create(const hc_geom* global, const hc_params* p, const hc_domain_
             return rc;
         }
         d->nccl_owned = true;
+    }
+    if (o->transport == HC_XCHG_STORE && (rc = setup_store(d))) {
+        hc_domain_destroy(d);
+        return rc;
     }
     *out = d;
     return HC_OK;
@@ -507,6 +568,10 @@ int hc_domain_create_local(const hc_geom* global, const hc_params* p, const hc_d
                         if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
                     }
                 }
+        if (o->transport == HC_XCHG_STORE && (rc = setup_store(d))) {
+            hc_domain_destroy(d);
+            return rc;
+        }
     }
     *out = d;
     return HC_OK;
@@ -540,6 +605,7 @@ int hc_domain_destroy(hc_domain* d) {
 // rows (the x/y ghosts travel along and are refilled on the device).
 int hc_domain_scatter(hc_domain* d, const double* global_skinny) {
     int rc;
+    d->primed = false;
     for (Slab& x : d->s) {
         if ((rc = set_dev(x.device))) return rc;
         const double* src = global_skinny + size_t(d->gh + x.z0) * d->plane;

@@ -285,6 +285,8 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                             double* dst = sbuf[1] + zi;
 #pragma unroll
                             for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                            if (a.zstore)
+                                zpeer_store(a, p - 1, zi - size_t(p - 1 + a.gh) * plane_stride, un);
                         }
                     } else {
 #pragma unroll
@@ -302,6 +304,8 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                         double* dst = sbuf[1] + zi;
 #pragma unroll
                         for (int q = 0; q < NV; ++q) dst[q] = un[q];
+                        if (a.zstore && !edge)  // (edge zones: seam_fix_kernel stores them)
+                            zpeer_store(a, p - 1, zi - size_t(p - 1 + a.gh) * plane_stride, un);
                     }
                     double dloc = 1.0e32;
                     if ((!RK || a.want_dt) && !edge) {
@@ -567,6 +571,11 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
                         out[zh + q] = vh[q];
                     }
                 }
+                if (a.zstore) {
+                    const size_t pz = size_t(p + a.gh) * a.my_pad * a.pitch;
+                    zpeer_store(a, p, zl - pz, vl);
+                    zpeer_store(a, p, zh - pz, vh);
+                }
                 dloc = smin(cfl(vl, il, jl), cfl(vh, ih, jh));
             }
         }
@@ -607,6 +616,7 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
                 out[z + q] = v[q];
             }
         }
+        if (a.zstore) zpeer_store(a, p, z - size_t(p + a.gh) * a.my_pad * a.pitch, v);
         dloc = cfl(v, i, j);
     }
     if (RK && !a.want_dt) return;

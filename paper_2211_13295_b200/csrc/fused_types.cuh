@@ -41,7 +41,31 @@ struct FusedArgs {
     Limiter lim;
     StepCtl* ctl;
     ErrBlock* eb;
+    // z peer stores (hc_stepper_set_zpeer; zstore = 1): the final update of the gh lowest /
+    // highest active planes is also written, by the thread that computed it, into the top /
+    // bottom ghost planes of the z neighbours' buffers -- device pointers on any GPU this one
+    // can reach (NVLink peer memory), same layout, buffer index = this launch's output index
+    double* zlo[3];
+    double* zhi[3];
+    int zstore;
 };
+
+// The peer store of one finished zone of active plane kz (in-plane storage offset `inplane`).
+__device__ __forceinline__ void zpeer_store(const FusedArgs& a, int kz, size_t inplane,
+                                            const double* v) {
+    const int ob = (a.ctl->cur + a.out_rel) % a.nbuf;
+    const size_t ps = size_t(a.my_pad) * a.pitch;
+    if (kz < a.gh && a.zlo[ob]) {  // -> the lower neighbour's top ghost plane gh + nz + kz
+        double* d = a.zlo[ob] + size_t(a.gh + a.nz + kz) * ps + inplane;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = v[q];
+    }
+    if (kz >= a.nz - a.gh && a.zhi[ob]) {  // -> the upper neighbour's bottom ghost plane
+        double* d = a.zhi[ob] + size_t(kz - a.nz + a.gh) * ps + inplane;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) d[q] = v[q];
+    }
+}
 
 // Tile shape per order (columns x rows of owned zones per CTA).
 // Tile shape per order (columns x rows of owned zones per CTA), from the r1 sweep on a B200

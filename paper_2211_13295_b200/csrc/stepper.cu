@@ -42,7 +42,8 @@ __device__ __forceinline__ void ghost_copy(double* u, const SG& g, int bx, int b
          ak = k >= g.gh && k < g.gh + g.nz;
     int si = ai ? i : g.gh + map_index(i - g.gh, g.nx, bx);
     int sj = aj ? j : g.gh + map_index(j - g.gh, g.ny, by);
-    int sk = ak ? k : g.gh + map_index(k - g.gh, g.nz, bz);
+    // bz < 0 (caller-filled z): a z-ghost plane's ring is filled from the plane itself
+    int sk = (ak || bz < 0) ? k : g.gh + map_index(k - g.gh, g.nz, bz);
     const double* src = u + (size_t(sk) * g.my_pad + sj) * g.pitch + size_t(si) * NV;
     double* dst = u + (size_t(k) * g.my_pad + j) * g.pitch + size_t(i) * NV;
 #pragma unroll
@@ -142,6 +143,10 @@ struct hc_stepper {
     SeamArgs sa{};
     int seam_tz = 32;
     CUtensorMap* maps = nullptr;  // device copies of the TMA maps (persist or seam)
+    // z peer stores (hc_stepper_set_zpeer): the z neighbours' buffers
+    double* zlo[3] = {nullptr, nullptr, nullptr};
+    double* zhi[3] = {nullptr, nullptr, nullptr};
+    bool zstore = false;
 };
 
 namespace {
@@ -204,6 +209,11 @@ FusedArgs fused_args(const hc_stepper* s) {
                     s->p.lim.weno_w[0], s->p.lim.weno_w[1], s->p.lim.weno_w[2]};
     a.ctl = s->ctl;
     a.eb = s->eb;
+    for (int i = 0; i < 3; ++i) {
+        a.zlo[i] = s->zlo[i];
+        a.zhi[i] = s->zhi[i];
+    }
+    a.zstore = s->zstore ? 1 : 0;
     return a;
 }
 
@@ -590,6 +600,10 @@ static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
         s->launches++;
     };
     if (s->o.bc[0] >= 0) launch(a_lo, a_hi, 1);  // (all -1: a patch set fills every ghost)
+    if (s->zstore && s->o.bc[0] >= 0) {  // z-ghost planes hold the neighbours' active zones
+        launch(k_lo, std::min(k_hi, g.gh), 1);
+        launch(std::max(k_lo, g.gh + g.nz), k_hi, 1);
+    }
     if (s->o.bc[2] >= 0) {
         launch(k_lo, std::min(k_hi, g.gh), 0);
         launch(std::max(k_lo, g.gh + g.nz), k_hi, 0);
@@ -901,6 +915,33 @@ int hc_stepper_state(hc_stepper* s, double** dptr, size_t* row_pitch_doubles) {
     if (rc) return rc;
     if (dptr) *dptr = s->buf[(s->cur + stage_in_rel(s)) % s->nbuf];
     if (row_pitch_doubles) *row_pitch_doubles = size_t(s->sg.pitch);
+    return HC_OK;
+}
+
+int hc_stepper_set_zpeer(hc_stepper* s, double* const* lo_bufs, double* const* hi_bufs) {
+    if (!s || (!lo_bufs && !hi_bufs)) {
+        set_error(HC_INVALID, "hc_stepper_set_zpeer: null argument");
+        return HC_INVALID;
+    }
+    if (s->o.bc[2] >= 0 || s->persist) {
+        set_error(HC_INVALID, "hc_stepper_set_zpeer needs caller-filled z ghosts (bc[2] = -1) "
+                              "and the ring or seam kernel");
+        return HC_INVALID;
+    }
+    for (int i = 0; i < s->nbuf; ++i)
+        if ((lo_bufs && !lo_bufs[i]) || (hi_bufs && !hi_bufs[i])) {
+            set_error(HC_INVALID, "hc_stepper_set_zpeer: a neighbour buffer is NULL");
+            return HC_INVALID;
+        }
+    for (int i = 0; i < 3; ++i) {
+        s->zlo[i] = lo_bufs && i < s->nbuf ? lo_bufs[i] : nullptr;
+        s->zhi[i] = hi_bufs && i < s->nbuf ? hi_bufs[i] : nullptr;
+    }
+    s->zstore = true;
+    if (s->graph) {  // a captured step holds the old arguments
+        cudaGraphExecDestroy(s->graph);
+        s->graph = nullptr;
+    }
     return HC_OK;
 }
 

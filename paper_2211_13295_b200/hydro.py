@@ -482,7 +482,7 @@ class DomainOpts(C.Structure):
                 ("device", C.c_int), ("transport", C.c_int), ("overlap", C.c_int)]
 
 
-XCHG_NCCL, XCHG_PEER = 0, 1  # hc_exchange_kind
+XCHG_NCCL, XCHG_PEER, XCHG_STORE = 0, 1, 2  # hc_exchange_kind
 
 
 def nccl_unique_id() -> bytes:

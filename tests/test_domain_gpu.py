@@ -33,7 +33,8 @@ def _single(g, params, s0, dt0, cfl, steps, exact, integ, bc):
 @pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("integ", [hydro.ADER, hydro.RK3])
 @pytest.mark.parametrize("transport,overlap", [(hydro.XCHG_NCCL, False), (hydro.XCHG_PEER, False),
-                                               (hydro.XCHG_NCCL, True), (hydro.XCHG_PEER, True)])
+                                               (hydro.XCHG_NCCL, True), (hydro.XCHG_PEER, True),
+                                               (hydro.XCHG_STORE, False)])
 def test_domain_self_exchange_bitwise(exact, integ, transport, overlap):
     order, shape, steps = 3, (64, 14, 12), 4
     api = hydro.HostApi()
@@ -121,3 +122,46 @@ def test_domain_c_selftest(tmp_path):
                os.environ.get("LD_LIBRARY_PATH", ""))
     r = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("integ", [hydro.ADER, hydro.RK3])
+@pytest.mark.parametrize("nslabs,bcz,shape", [(2, hydro.PERIODIC, (64, 14, 16)),
+                                              (4, hydro.PERIODIC, (32, 12, 16)),
+                                              (2, hydro.OUTFLOW, (32, 10, 12)),
+                                              (3, hydro.PERIODIC, (64, 9, 48))])
+def test_domain_peer_store_slabs_bitwise(exact, integ, nslabs, bcz, shape):
+    """HC_XCHG_STORE: the fused kernels (ring or seam pair) write their boundary planes into
+    the neighbour slabs' ghost planes -- several slabs on this one GPU stand in for peers --
+    with no exchange step; bit-identical to the single domain, state, t and dt"""
+    order, steps = 3, 4
+    api = hydro.HostApi()
+    g = hydro.make_geometry(*shape, order)
+    params = hydro.make_params(order)
+    s0 = modulate_z(api.init_isentropic_vortex(g, order))
+    dt0 = api.initial_dt(g, s0, 0.4)
+    bc = (hydro.PERIODIC, hydro.PERIODIC, bcz)
+    want, t1, dt1, n1, _ = _single(g, params, s0, dt0, 0.4, steps, exact, integ, bc)
+    d = hydro.Domain(g, params, bc=bc, exact=exact, integrator=integ,
+                     transport=hydro.XCHG_STORE, devices=(0,) * nslabs)
+    assert d.nslabs == nslabs
+    d.scatter(s0)
+    d.set_time(0.0, dt0, 0.4)
+    d.step(steps)
+    t2, dt2, n2 = d.sync()
+    out = want.copy()
+    out[g.ghost:-g.ghost] = 0.0
+    d.gather(out)
+    # a second scatter re-primes the halos (peer copies for the first stage again)
+    d.scatter(s0)
+    d.set_time(0.0, dt0, 0.4)
+    d.step(steps)
+    out2 = want.copy()
+    d.gather(out2)
+    d.close()
+    gh = g.ghost
+    act = np.s_[gh:-gh, gh:-gh, gh:-gh]
+    assert (out[act].view(np.uint64) == want[act].view(np.uint64)).all(), \
+        np.abs(out[act] - want[act]).max()
+    assert (out2[act].view(np.uint64) == want[act].view(np.uint64)).all()
+    assert (t2, dt2, n2) == (t1, dt1, n1)

@@ -1,7 +1,10 @@
 """One configs[4] slab (512^2 x 64 planes, O3, FMA build) stepped through the C-ABI multi-GPU
 domain on one GPU -- the slab exchanging its z halos with itself (NCCL self send/recv, or peer
-copies), sequential or overlapped with the interior planes -- against the plain stepper that
-owns every boundary. ms per step, CUDA-event timed. Usage: python tools/domain_bench.py [n nz]"""
+copies), sequential or overlapped with the interior planes, or the fused kernels storing the
+boundary planes into the ghost planes themselves (store) -- against the plain stepper that
+owns every boundary; then the same mesh as two 32-plane slabs on this GPU (peer copies vs
+stores between two steppers). ms per step, CUDA-event timed.
+Usage: python tools/domain_bench.py [n nz]"""
 import json
 import sys
 import os
@@ -43,9 +46,14 @@ st.upload(s0)
 st.set_time(0.0, dt0, 0.4)
 res["stepper_ms"] = timed(lambda: st.step(1), st.sync)
 st.close()
-for name, tr, ov in (("nccl", hydro.XCHG_NCCL, False), ("nccl_overlap", hydro.XCHG_NCCL, True),
-                     ("peer", hydro.XCHG_PEER, False), ("peer_overlap", hydro.XCHG_PEER, True)):
-    d = hydro.Domain(g, params, exact=False, transport=tr, overlap=ov)
+for name, tr, ov, devs in (("nccl", hydro.XCHG_NCCL, False, (0,)),
+                           ("nccl_overlap", hydro.XCHG_NCCL, True, (0,)),
+                           ("peer", hydro.XCHG_PEER, False, (0,)),
+                           ("peer_overlap", hydro.XCHG_PEER, True, (0,)),
+                           ("store", hydro.XCHG_STORE, False, (0,)),
+                           ("two_slabs_peer", hydro.XCHG_PEER, False, (0, 0)),
+                           ("two_slabs_store", hydro.XCHG_STORE, False, (0, 0))):
+    d = hydro.Domain(g, params, exact=False, transport=tr, overlap=ov, devices=devs)
     d.scatter(s0)
     d.set_time(0.0, dt0, 0.4)
     res[name + "_ms"] = timed(lambda: d.step(1), d.sync)

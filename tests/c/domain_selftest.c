@@ -1,7 +1,8 @@
 /* domain_selftest.c -- the multi-GPU domain through the C ABI alone (no Python, no torch):
  * a z-periodic vortex stepped by hc_domain_create_local(ngpu = 1) -- the slab exchanges its
  * halos with itself through ncclSend/ncclRecv and all-reduces dt_next through NCCL, the N > 1
- * code path -- and by hc_domain_create(rank 0 of world 1, NCCL unique id), against a single
+ * code path -- by hc_domain_create(rank 0 of world 1, NCCL unique id), by peer copies and by
+ * the fused kernels storing the halos themselves (HC_XCHG_STORE), against a single
  * hc_stepper owning all its boundaries. Both builds, ADER and SSP-RK3: the final states and
  * dt must be bit-identical. Prints "ok" and exits 0, or the first difference and exits 1.
  * Build: gcc -O2 -I include tests/c/domain_selftest.c -L paper_2211_13295_b200 -lhydro_cuda */
@@ -84,7 +85,8 @@ static int run_case(int exact, int integrator, int mode) {
 
     /* the domain */
     hc_domain_opts o = {{HC_PERIODIC, HC_PERIODIC, HC_PERIODIC}, exact, integrator, 0,
-                        mode == 2 ? HC_XCHG_PEER : HC_XCHG_NCCL, mode == 1};
+                        mode == 3 ? HC_XCHG_STORE : (mode == 2 ? HC_XCHG_PEER : HC_XCHG_NCCL),
+                        mode == 1};
     hc_domain* d = NULL;
     if (mode == 1) {
         unsigned char id[128];
@@ -133,7 +135,7 @@ int main(void) {
     int bad = 0;
     for (int exact = 0; exact <= 1; ++exact)
         for (int ig = 0; ig < 2; ++ig)
-            for (int mode = 0; mode <= 2; ++mode) bad |= run_case(exact, ig ? 3 : 0, mode);
+            for (int mode = 0; mode <= 3; ++mode) bad |= run_case(exact, ig ? 3 : 0, mode);
     if (!bad) printf("ok\n");
     return bad;
 }

@@ -31,7 +31,7 @@ SOURCES = {
     "fused_exact.cu": ["--fmad=false"] + TUNE,
     "fused_fast.cu": ["--fmad=true"] + TUNE,
     "peak.cu": ["--fmad=true"],
-    "mhd.cu": ["--fmad=false"],
+    "mhd.cu": ["--fmad=false"] + TUNE,
     "ced.cu": ["--fmad=false"],
     "domain.cu": ["--fmad=false"],
     "ader4.cu": ["--fmad=true"] + TUNE,

@@ -734,8 +734,8 @@ __global__ void k_mhd_dt(MArgs a, double cfl, double* out, int stage) {
 // ============================================================ order 4 (space-time ADER)
 // The O2/O3 kernels keep the reference's ADER structure (face state + the zone's tau/2), second
 // order in time. Order 4 (smooth flows; no positivity fallback):
-//   k_mhd4_predict  one CTA per ring zone, one thread per space-time node (4 x 4 x 4 Gauss-
-//                   Legendre points x 4 Gauss times): the degree-3 polynomial of the 8 cell
+//   k_mhd4_predict  one CTA per ring zone, one thread per spatial node (4 x 4 x 4 Gauss-
+//                   Legendre points) holding its 4 Gauss times: the degree-3 polynomial of the 8 cell
 //                   variables (fluid averages, fourth-order cell B from k_mhd_cellb; WENO-AO pure
 //                   terms, central mixed terms, as ader4.cu), four Picard iterations of the local
 //                   space-time predictor with the MHD flux; outputs the states at the 2 x 2 Gauss
@@ -760,14 +760,26 @@ __device__ __forceinline__ void psi4m(double s, double* p) {
     p[3] = s2 * s2 - (3.0 / 14.0) * s2 + 3.0 / 560.0;
 }
 
-__global__ void __launch_bounds__(M4_NT) k_mhd4_predict(MArgs a) {
+// One CTA of 64 threads per ring zone; thread t owns spatial node t and its 4 time nodes in
+// registers (the time integral and the output time contraction are register work); the
+// fluxes go through shared memory two time nodes at a time, SoA with the node slot
+// n ^ 5 * bit4(n), so the x / y / z neighbour reads of a warp hit distinct banks (the layout
+// of ader4.cu's predictor). The 96 output points are contracted separably: one axis first
+// (the face normal with the face values, or the edge direction with the Gauss values), then
+// the two transverse ones.
+#ifndef M4_MINB
+#define M4_MINB 6
+#endif
+constexpr int M4_NS = 64;                        // spatial nodes = threads per CTA
+constexpr int M4_F = 2 * 3 * NM * M4_NS;         // flux staging (2 time nodes)
+constexpr int M4_T = NM * 2 * M4_NS;             // predictor at the 2 Gauss times
+constexpr int M4_SQ = 384 + 24;                  // one-axis contractions per variable (skewed)
+constexpr int M4_U = (M4_F > M4_T + NM * M4_SQ) ? M4_F : M4_T + NM * M4_SQ;
+__global__ void __launch_bounds__(M4_NS, M4_MINB) k_mhd4_predict(MArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     __shared__ double coef[NM][M4_NCOEF];
-    extern __shared__ double smm[];
-    double* Q = smm;                  // [256][8]
-    double* FL = Q + M4_NT * NM;      // [3][256][8]
-    double* DV = FL + 3 * M4_NT * NM; // [256][8]
+    __shared__ double U[M4_U];
     const int rx = b.n[0] + 2, ry = b.n[1] + 2;
     const int zr = blockIdx.x;
     const int i = zr % rx - 1 + b.gh, j = (zr / rx) % ry - 1 + b.gh,
@@ -778,41 +790,51 @@ __global__ void __launch_bounds__(M4_NT) k_mhd4_predict(MArgs a) {
     const int t = threadIdx.x;
     const double dt = a.ctl->dt;
     auto Wv = [&](int q, long long off) { return wvar(a, q, size_t((long long)o + off)); };
-    if (t < 24) {
-        const int q = t / 3, ax = t % 3;
-        double m[4];
-        Fault f;
-        f.clear();
-        weno_ao<0>(Wv(q, -2 * st3[ax]), Wv(q, -st3[ax]), Wv(q, 0), Wv(q, st3[ax]), Wv(q, 2 * st3[ax]),
-                   a.lim, m, f);
+    // reconstruction: 24 WENO-AO tasks (the long ones first), then 80 mixed terms
+    for (int task = t; task < 24 + NM * 10; task += M4_NS) {
+        if (task < 24) {
+            const int q = task / 3, ax = task % 3;
+            double m[4];
+            Fault f;
+            f.clear();
+            weno_ao<0>(Wv(q, -2 * st3[ax]), Wv(q, -st3[ax]), Wv(q, 0), Wv(q, st3[ax]),
+                       Wv(q, 2 * st3[ax]), a.lim, m, f);
 #pragma unroll
-        for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
-        if (ax == 0) coef[q][0] = Wv(q, 0);
-    } else if (t < 24 + NM * 10) {
-        const int q = (t - 24) / 10, term = (t - 24) % 10;
-        auto val = [&](int p1, int s1, int p2, int s2) { return Wv(q, s1 * st3[p1] + s2 * st3[p2]); };
-        double v;
-        if (term < 3) {
-            const int p1 = term, r = (term + 1) % 3;
-            v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) - (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
-        } else if (term < 9) {
-            const int pair = (term - 3) / 2, sw = (term - 3) % 2;
-            const int a1 = pair, a2 = (pair + 1) % 3;
-            const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
-            auto d2 = [&](int sg) { return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg); };
-            v = 0.25 * (d2(1) - d2(-1));
+            for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
+            if (ax == 0) coef[q][0] = Wv(q, 0);
         } else {
-            double acc = 0.0;
-            for (int cc = -1; cc <= 1; cc += 2)
-                for (int bb = -1; bb <= 1; bb += 2)
-                    for (int aa = -1; aa <= 1; aa += 2)
-                        acc += double(aa * bb * cc) * Wv(q, aa * st3[0] + bb * st3[1] + cc * st3[2]);
-            v = 0.125 * acc;
+            const int q = (task - 24) / 10, term = (task - 24) % 10;
+            auto val = [&](int p1, int s1, int p2, int s2) {
+                return Wv(q, s1 * st3[p1] + s2 * st3[p2]);
+            };
+            double v;
+            if (term < 3) {
+                const int p1 = term, r = (term + 1) % 3;
+                v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) -
+                            (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
+            } else if (term < 9) {
+                const int pair = (term - 3) / 2, sw = (term - 3) % 2;
+                const int a1 = pair, a2 = (pair + 1) % 3;
+                const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
+                auto d2 = [&](int sg) {
+                    return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg);
+                };
+                v = 0.25 * (d2(1) - d2(-1));
+            } else {
+                double acc = 0.0;
+                for (int cc = -1; cc <= 1; cc += 2)
+                    for (int bb = -1; bb <= 1; bb += 2)
+                        for (int aa = -1; aa <= 1; aa += 2)
+                            acc += double(aa * bb * cc) *
+                                   Wv(q, aa * st3[0] + bb * st3[1] + cc * st3[2]);
+                v = 0.125 * acc;
+            }
+            coef[q][13 + term] = v;
         }
-        coef[q][13 + term] = v;
     }
     __syncthreads();
-    const int ni = t & 3, nj = (t >> 2) & 3, nk = (t >> 4) & 3, nm = t >> 6;
+    const int ni = t & 3, nj = (t >> 2) & 3, nk = t >> 4;
+    auto sw = [](int n) { return n ^ (((n >> 4) & 1) * 5); };
     double p0[NM];
     {
         double px[4], py[4], pz[4];
@@ -831,120 +853,143 @@ __global__ void __launch_bounds__(M4_NT) k_mhd4_predict(MArgs a) {
             v += c[20] * pz[1] * px[0] + c[21] * pz[0] * px[1];
             v += c[22] * px[0] * py[0] * pz[0];
             p0[q] = v;
-            Q[t * NM + q] = v;
         }
     }
-    __syncthreads();
+    double Q[4][NM];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < NM; ++q) Q[m][q] = p0[q];
+    double wx[4], wy[4], wz[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        wx[l] = c_mb.D[ni][l] * a.id[0];
+        wy[l] = c_mb.D[nj][l] * a.id[1];
+        wz[l] = c_mb.D[nk][l] * a.id[2];
+    }
+    // F[mm][axis][q][slot]
+    auto F = [&](int mm, int ax, int q, int slot) -> double& {
+        return U[((mm * 3 + ax) * NM + q) * M4_NS + slot];
+    };
+    const int ts = sw(t);
     Fault f;
     f.clear();
     for (int it = 0; it < 4; ++it) {
-        {
-            double u[NM], fl[NM];
+        double dv[4][NM];
 #pragma unroll
-            for (int q = 0; q < NM; ++q) u[q] = Q[t * NM + q];
-            const MPrim pr = mhd_prim<0>(u, a.gamma, f);
-            mhd_flux<0>(u, pr, fl);
+        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int q = 0; q < NM; ++q) FL[(0 * M4_NT + t) * NM + q] = fl[q];
-            mhd_flux<1>(u, pr, fl);
+            for (int mm = 0; mm < 2; ++mm) {
+                const int m = 2 * h + mm;
+                const MPrim pr = mhd_prim<0>(Q[m], a.gamma, f);
+                double fl[NM];
+                mhd_flux<0>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NM; ++q) FL[(1 * M4_NT + t) * NM + q] = fl[q];
-            mhd_flux<2>(u, pr, fl);
+                for (int q = 0; q < NM; ++q) F(mm, 0, q, ts) = fl[q];
+                mhd_flux<1>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NM; ++q) FL[(2 * M4_NT + t) * NM + q] = fl[q];
-        }
-        __syncthreads();
-        {
-            double dv[NM];
+                for (int q = 0; q < NM; ++q) F(mm, 1, q, ts) = fl[q];
+                mhd_flux<2>(Q[m], pr, fl);
 #pragma unroll
-            for (int q = 0; q < NM; ++q) dv[q] = 0.0;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
-                const double wx = c_mb.D[ni][l] * a.id[0], wy = c_mb.D[nj][l] * a.id[1],
-                             wz = c_mb.D[nk][l] * a.id[2];
-#pragma unroll
-                for (int q = 0; q < NM; ++q)
-                    dv[q] += wx * FL[(0 * M4_NT + tx) * NM + q] + wy * FL[(1 * M4_NT + ty) * NM + q] +
-                             wz * FL[(2 * M4_NT + tz) * NM + q];
+                for (int q = 0; q < NM; ++q) F(mm, 2, q, ts) = fl[q];
             }
+            __syncthreads();
 #pragma unroll
-            for (int q = 0; q < NM; ++q) DV[t * NM + q] = dv[q];
-        }
-        __syncthreads();
-        {
-            double qn[NM];
+            for (int mm = 0; mm < 2; ++mm) {
+                const int m = 2 * h + mm;
 #pragma unroll
-            for (int q = 0; q < NM; ++q) qn[q] = p0[q];
+                for (int q = 0; q < NM; ++q) dv[m][q] = 0.0;
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tl = (t & 63) | (l << 6);
-                const double w = dt * c_mb.IT[nm][l];
+                for (int l = 0; l < 4; ++l) {
+                    const int tx = sw((t & ~3) | l), ty = sw((t & ~12) | (l << 2)),
+                              tz = sw((t & ~48) | (l << 4));
 #pragma unroll
-                for (int q = 0; q < NM; ++q) qn[q] -= w * DV[tl * NM + q];
+                    for (int q = 0; q < NM; ++q)
+                        dv[m][q] += wx[l] * F(mm, 0, q, tx) + wy[l] * F(mm, 1, q, ty) +
+                                    wz[l] * F(mm, 2, q, tz);
+                }
             }
-#pragma unroll
-            for (int q = 0; q < NM; ++q) Q[t * NM + q] = qn[q];
+            __syncthreads();
         }
-        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int q = 0; q < NM; ++q) {
+                double qn = p0[q];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) qn -= (dt * c_mb.IT[m][l]) * dv[l][q];
+                Q[m][q] = qn;
+            }
     }
     if (f.code) record_fault(a.eb, ST_PREDICT, f, i - b.gh, j - b.gh, k - b.gh, 0);
-    // outputs: (1) time -> the 2 Gauss times, T[tg][node][8] (in FL)
-    double* T = FL;
-    if (t < 128) {
-        const int tg = t >> 6, node = t & 63;
+    // outputs. (1) time -> the 2 Gauss times, in registers: T[q][tg][slotT(node)]
+    double* T = U;
+    double* S = U + M4_T;  // S[q][r + r / 16], r < 384
+    auto slotT = [](int n) { return n ^ ((n >> 4) * 5); };
+#pragma unroll
+    for (int tg = 0; tg < 2; ++tg)
+#pragma unroll
+        for (int q = 0; q < NM; ++q) {
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) v += c_mb.LT[tg][m] * Q[m][q];
+            T[(q * 2 + tg) * M4_NS + slotT(t)] = v;
+        }
+    __syncthreads();
+    // (2) one axis: r < 192 faces ((A * 2 + side) * 2 + tg) * 16 + b1 * 4 + b2, the normal
+    //     axis A at its face (LF[side]); r >= 192 edges ((C * 2 + g) * 2 + tg) * 16 + ..., the
+    //     edge axis C at Gauss point g (LG[g]); b1, b2 the nodes along the axes +1 / +2 of it
+    for (int r = t; r < 384; r += M4_NS) {
+        const int rr = r < 192 ? r : r - 192;
+        const int ax = rr >> 6, sel = (rr >> 5) & 1, tg = (rr >> 4) & 1, b1 = (rr >> 2) & 3,
+                  b2 = rr & 3;
+        const double* w = r < 192 ? c_mb.LF[sel] : c_mb.LG[sel];
         double v[NM];
 #pragma unroll
         for (int q = 0; q < NM; ++q) v[q] = 0.0;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const double w = c_mb.LT[tg][m];
+        for (int l = 0; l < 4; ++l) {
+            int c[3];
+            c[ax] = l;
+            c[(ax + 1) % 3] = b1;
+            c[(ax + 2) % 3] = b2;
+            const int node = (c[2] * 4 + c[1]) * 4 + c[0];
 #pragma unroll
-            for (int q = 0; q < NM; ++q) v[q] += w * Q[((m << 6) | node) * NM + q];
+            for (int q = 0; q < NM; ++q) v[q] += w[l] * T[(q * 2 + tg) * M4_NS + slotT(node)];
         }
 #pragma unroll
-        for (int q = 0; q < NM; ++q) T[t * NM + q] = v[q];
+        for (int q = 0; q < NM; ++q) S[q * M4_SQ + r + (r >> 4)] = v[q];
     }
     __syncthreads();
-    // (2) the points: faces e < 48: ((face * 4 + g1 * 2 + g2) * 2 + tg), face = 2A + side;
-    //     edges e - 48 < 48: ((C * 4 + 2 lb + la) * 2 + g) * 2 + tg (corner la, lb at +-1/2 in
-    //     the (C+1, C+2) plane, la = 0: +1/2; g along C)
-    if (t < M4_OUT) {
-        double w[3][4];
-        int tg;
-        if (t < 48) {
-            tg = t & 1;
-            const int g = (t >> 1) & 3, face = t >> 3, A = face >> 1, side = face & 1;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                w[A][l] = c_mb.LF[side][l];
-                w[(A + 1) % 3][l] = c_mb.LG[g >> 1][l];
-                w[(A + 2) % 3][l] = c_mb.LG[g & 1][l];
-            }
-        } else {
-            const int e = t - 48;
-            tg = e & 1;
-            const int g = (e >> 1) & 1, corner = (e >> 2) & 3, C = e >> 4;
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                w[C][l] = c_mb.LG[g][l];
-                w[(C + 1) % 3][l] = c_mb.LF[corner & 1][l];
-                w[(C + 2) % 3][l] = c_mb.LF[corner >> 1][l];
-            }
+    // (3) the two transverse axes: faces at the 2 x 2 Gauss points, edges at the corner
+    for (int e = t; e < M4_OUT; e += M4_NS) {
+        int base;
+        const double *w1, *w2;
+        if (e < 48) {  // ((face * 4 + g1 * 2 + g2) * 2 + tg), face = 2A + side
+            const int tg = e & 1, g = (e >> 1) & 3, face = e >> 3;
+            base = (face * 2 + tg) * 16;
+            w1 = c_mb.LG[g >> 1];
+            w2 = c_mb.LG[g & 1];
+        } else {  // ((C * 4 + corner) * 2 + g) * 2 + tg, corner = la + 2 lb
+            const int x = e - 48, tg = x & 1, g = (x >> 1) & 1, corner = (x >> 2) & 3, C = x >> 4;
+            base = 192 + ((C * 2 + g) * 2 + tg) * 16;
+            w1 = c_mb.LF[corner & 1];
+            w2 = c_mb.LF[corner >> 1];
         }
         double v[NM];
 #pragma unroll
         for (int q = 0; q < NM; ++q) v[q] = 0.0;
-        for (int kk = 0; kk < 4; ++kk)
-            for (int jj = 0; jj < 4; ++jj)
-                for (int ii = 0; ii < 4; ++ii) {
-                    const double ww = w[2][kk] * w[1][jj] * w[0][ii];
-                    const int node = (kk * 4 + jj) * 4 + ii;
 #pragma unroll
-                    for (int q = 0; q < NM; ++q) v[q] += ww * T[((tg << 6) | node) * NM + q];
-                }
+        for (int b1 = 0; b1 < 4; ++b1)
 #pragma unroll
-        for (int q = 0; q < NM; ++q) __stcs(a.states + (size_t(t) * NM + q) * N + o, v[q]);
+            for (int b2 = 0; b2 < 4; ++b2) {
+                const double ww = w1[b1] * w2[b2];
+                const int r = base + b1 * 4 + b2;
+#pragma unroll
+                for (int q = 0; q < NM; ++q) v[q] += ww * S[q * M4_SQ + r + (r >> 4)];
+            }
+#pragma unroll
+        for (int q = 0; q < NM; ++q) __stcs(a.states + (size_t(e) * NM + q) * N + o, v[q]);
     }
 }
 
@@ -1194,7 +1239,6 @@ int launch_ghosts(hc_mhd* m) {
 
 // the front kernels of a step for the active z range [zlo, zhi): cell B, predictor, face
 // fluxes and edge EMFs of every face/edge the update of those zones reads
-constexpr size_t kMhd4Smem = sizeof(double) * 5 * M4_NT * NM;
 
 int launch_front4(hc_mhd* m, int zlo, int zhi) {
     MArgs a = margs(m);
@@ -1205,7 +1249,7 @@ int launch_front4(hc_mhd* m, int zlo, int zhi) {
     const size_t cb = size_t(b.P) * b.Q * (nz + 6);
     const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (nz + 2);
     k_mhd_cellb<true><<<blocks(cb, 256), 256, 0, m->st>>>(a);
-    k_mhd4_predict<<<unsigned(ring), M4_NT, kMhd4Smem, m->st>>>(a);
+    k_mhd4_predict<<<unsigned(ring), M4_NS, 0, m->st>>>(a);
     const size_t fx = size_t(b.n[0] + 1) * b.n[1] * nz;
     const size_t fy = size_t(b.n[0]) * (b.n[1] + 1) * nz;
     const size_t fz = size_t(b.n[0]) * b.n[1] * (nz + 1);
@@ -1384,8 +1428,8 @@ int hc_mhd_create(const hc_geom* g, const hc_mhd_params* p, hc_mhd** out) {
         MhdBasis bs = make_mhd_basis();
         e = cudaMemcpyToSymbol(c_mb, &bs, sizeof bs);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_mhd4_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kMhd4Smem));
+            e = cudaFuncSetAttribute(k_mhd4_predict,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     if (e != cudaSuccess) {
         hc_mhd_destroy(m);

@@ -32,7 +32,7 @@ SOURCES = {
     "fused_fast.cu": ["--fmad=true"] + TUNE,
     "peak.cu": ["--fmad=true"],
     "mhd.cu": ["--fmad=false"] + TUNE,
-    "ced.cu": ["--fmad=false"],
+    "ced.cu": ["--fmad=false"] + TUNE,
     "domain.cu": ["--fmad=false"],
     "ader4.cu": ["--fmad=true"] + TUNE,
 }

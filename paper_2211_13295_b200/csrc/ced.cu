@@ -326,8 +326,8 @@ __global__ void k_ced_update(CArgs a) {
 // second order in time. Order 4 is the scheme of the paper's CED runs: a
 // local space-time predictor with the stiff conduction source solved IMPLICITLY inside it by
 // small block inversions, then edge E and H integrated at space-time Gauss points:
-//   k_ced4_predict  one CTA per ring zone, one thread per space-time node (4 x 4 x 4 Gauss-
-//                   Legendre points x 4 Radau IIA times in [t, t + dt]): the degree-3 polynomial
+//   k_ced4_predict  one CTA per ring zone, one thread per spatial node (4 x 4 x 4 Gauss-
+//                   Legendre points) with its 4 Radau IIA times in [t, t + dt]: the degree-3 polynomial
 //                   of the six cell fields (WENO-AO pure terms, central mixed terms, as
 //                   ader4.cu), then Picard iterations of the collocation system
 //                     q(tau_m) = P - dt sum_l A_ml (div F(q(tau_l)) + s q_D(tau_l)),  s = sigma/eps
@@ -359,15 +359,25 @@ __device__ __forceinline__ void psi4(double s, double* p) {
     p[3] = s2 * s2 - (3.0 / 14.0) * s2 + 3.0 / 560.0;
 }
 
-__global__ void __launch_bounds__(C4_NT) k_ced4_predict(CArgs a) {
+// One CTA of 64 threads per ring zone; thread t owns spatial node t and its 4 Radau times in
+// registers, so the implicit conduction solve over those times (minv) and the time integral
+// are register work; the fluxes go through shared memory two time nodes at a time, SoA with
+// the node slot n ^ 5 * bit4(n) (conflict-free neighbour reads, as ader4.cu); the 48 edge
+// points are contracted separably (the edge axis first, then the two transverse ones).
+#ifndef C4_MINB
+#define C4_MINB 6
+#endif
+constexpr int C4_NS = 64;
+constexpr int C4_F = 2 * 3 * NF * C4_NS;
+constexpr int C4_T = NF * 2 * C4_NS;
+constexpr int C4_SQ = 192 + 12;
+constexpr int C4_U = (C4_F > C4_T + NF * C4_SQ) ? C4_F : C4_T + NF * C4_SQ;
+__global__ void __launch_bounds__(C4_NS, C4_MINB) k_ced4_predict(CArgs a) {
     if (a.ctl->done) return;
     const Box& b = a.b;
     __shared__ double coef[NF][C4_NCOEF];
     __shared__ double minv[4][4];
-    extern __shared__ double sm4[];
-    double* Q = sm4;                // [256][6] nodal fields
-    double* FL = Q + C4_NT * NF;    // [3][256][6] flux components
-    double* DV = FL + 3 * C4_NT * NF;  // [256][6] divergence
+    __shared__ double U[C4_U];
     const int rx = b.n[0] + 2, ry = b.n[1] + 2;
     const int zr = blockIdx.x;
     const int i = zr % rx - 1 + b.gh, j = (zr / rx) % ry - 1 + b.gh, k = zr / (rx * ry) - 1 + b.gh;
@@ -378,63 +388,73 @@ __global__ void __launch_bounds__(C4_NT) k_ced4_predict(CArgs a) {
     const double dt = a.ctl->dt;
     auto W = [&](int q, long long off) { return __ldg(a.w + size_t(q) * N + size_t((long long)o + off)); };
     auto offs = [&](int ax, int s1) { return (long long)s1 * (long long)st3[ax]; };
-    // -- reconstruction (see ader4.cu): [0] mean, [1..4] x, [5..8] y, [9..12] z, [13..22] mixed
-    if (t < 18) {
-        const int q = t / 3, ax = t % 3;
-        double m[4];
-        Fault f;
-        f.clear();
-        weno_ao<0>(W(q, offs(ax, -2)), W(q, offs(ax, -1)), W(q, 0), W(q, offs(ax, 1)),
-                   W(q, offs(ax, 2)), a.lim, m, f);
+    // -- reconstruction (see ader4.cu): [0] mean, [1..4] x, [5..8] y, [9..12] z, [13..22]
+    //    mixed; 18 WENO-AO tasks, 60 mixed terms and the 4 x 4 implicit-source inverse
+    for (int task = t; task < 18 + NF * 10 + 1; task += C4_NS) {
+        if (task < 18) {
+            const int q = task / 3, ax = task % 3;
+            double m[4];
+            Fault f;
+            f.clear();
+            weno_ao<0>(W(q, offs(ax, -2)), W(q, offs(ax, -1)), W(q, 0), W(q, offs(ax, 1)),
+                       W(q, offs(ax, 2)), a.lim, m, f);
 #pragma unroll
-        for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
-        if (ax == 0) coef[q][0] = W(q, 0);
-    } else if (t < 18 + NF * 10) {
-        const int q = (t - 18) / 10, term = (t - 18) % 10;
-        auto val = [&](int p1, int s1, int p2, int s2) { return W(q, offs(p1, s1) + offs(p2, s2)); };
-        double v;
-        if (term < 3) {
-            const int p1 = term, r = (term + 1) % 3;
-            v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) - (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
-        } else if (term < 9) {
-            const int pair = (term - 3) / 2, sw = (term - 3) % 2;
-            const int a1 = pair, a2 = (pair + 1) % 3;
-            const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
-            auto d2 = [&](int sg) { return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg); };
-            v = 0.25 * (d2(1) - d2(-1));
-        } else {
-            double acc = 0.0;
-            for (int cc = -1; cc <= 1; cc += 2)
-                for (int bb = -1; bb <= 1; bb += 2)
-                    for (int aa = -1; aa <= 1; aa += 2)
-                        acc += double(aa * bb * cc) * W(q, offs(0, aa) + offs(1, bb) + offs(2, cc));
-            v = 0.125 * acc;
-        }
-        coef[q][13 + term] = v;
-    } else if (t == 255) {
-        // (I + z A)^-1, z = dt sigma / eps (Gauss-Jordan on 4 x 4; the system is diagonally
-        // dominant for z >= 0, no pivoting needed)
-        const double z = dt * a.sigma[o] / a.eps;
-        double m[4][8];
-        for (int r = 0; r < 4; ++r)
-            for (int c = 0; c < 4; ++c) {
-                m[r][c] = (r == c ? 1.0 : 0.0) + z * c_cb.A[r][c];
-                m[r][4 + c] = r == c ? 1.0 : 0.0;
+            for (int l = 0; l < 4; ++l) coef[q][1 + 4 * ax + l] = m[l];
+            if (ax == 0) coef[q][0] = W(q, 0);
+        } else if (task < 18 + NF * 10) {
+            const int q = (task - 18) / 10, term = (task - 18) % 10;
+            auto val = [&](int p1, int s1, int p2, int s2) {
+                return W(q, offs(p1, s1) + offs(p2, s2));
+            };
+            double v;
+            if (term < 3) {
+                const int p1 = term, r = (term + 1) % 3;
+                v = 0.25 * ((val(p1, 1, r, 1) - val(p1, 1, r, -1)) -
+                            (val(p1, -1, r, 1) - val(p1, -1, r, -1)));
+            } else if (term < 9) {
+                const int pair = (term - 3) / 2, sw = (term - 3) % 2;
+                const int a1 = pair, a2 = (pair + 1) % 3;
+                const int p1 = sw == 0 ? a1 : a2, r = sw == 0 ? a2 : a1;
+                auto d2 = [&](int sg) {
+                    return (val(p1, 1, r, sg) - 2.0 * val(p1, 0, r, sg)) + val(p1, -1, r, sg);
+                };
+                v = 0.25 * (d2(1) - d2(-1));
+            } else {
+                double acc = 0.0;
+                for (int cc = -1; cc <= 1; cc += 2)
+                    for (int bb = -1; bb <= 1; bb += 2)
+                        for (int aa = -1; aa <= 1; aa += 2)
+                            acc += double(aa * bb * cc) *
+                                   W(q, offs(0, aa) + offs(1, bb) + offs(2, cc));
+                v = 0.125 * acc;
             }
-        for (int c = 0; c < 4; ++c) {
-            const double ip = 1.0 / m[c][c];
-            for (int cc = 0; cc < 8; ++cc) m[c][cc] *= ip;
+            coef[q][13 + term] = v;
+        } else {
+            // (I + z A)^-1, z = dt sigma / eps (Gauss-Jordan on 4 x 4; the system is diagonally
+            // dominant for z >= 0, no pivoting needed)
+            const double z = dt * a.sigma[o] / a.eps;
+            double m[4][8];
             for (int r = 0; r < 4; ++r)
-                if (r != c) {
-                    const double fct = m[r][c];
-                    for (int cc = 0; cc < 8; ++cc) m[r][cc] -= fct * m[c][cc];
+                for (int c = 0; c < 4; ++c) {
+                    m[r][c] = (r == c ? 1.0 : 0.0) + z * c_cb.A[r][c];
+                    m[r][4 + c] = r == c ? 1.0 : 0.0;
                 }
+            for (int c = 0; c < 4; ++c) {
+                const double ip = 1.0 / m[c][c];
+                for (int cc = 0; cc < 8; ++cc) m[c][cc] *= ip;
+                for (int r = 0; r < 4; ++r)
+                    if (r != c) {
+                        const double fct = m[r][c];
+                        for (int cc = 0; cc < 8; ++cc) m[r][cc] -= fct * m[c][cc];
+                    }
+            }
+            for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) minv[r][c] = m[r][4 + c];
         }
-        for (int r = 0; r < 4; ++r)
-            for (int c = 0; c < 4; ++c) minv[r][c] = m[r][4 + c];
     }
     __syncthreads();
-    const int ni = t & 3, nj = (t >> 2) & 3, nk = (t >> 4) & 3, nm = t >> 6;
+    const int ni = t & 3, nj = (t >> 2) & 3, nk = t >> 4;
+    auto sw = [](int n) { return n ^ (((n >> 4) & 1) * 5); };
     double p0[NF];
     {
         double px[4], py[4], pz[4];
@@ -453,109 +473,136 @@ __global__ void __launch_bounds__(C4_NT) k_ced4_predict(CArgs a) {
             v += c[20] * pz[1] * px[0] + c[21] * pz[0] * px[1];
             v += c[22] * px[0] * py[0] * pz[0];
             p0[q] = v;
-            Q[t * NF + q] = v;
         }
     }
-    __syncthreads();
+    double Q[4][NF];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int q = 0; q < NF; ++q) Q[m][q] = p0[q];
+    double wx[4], wy[4], wz[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        wx[l] = c_cb.D[ni][l] * a.id[0];
+        wy[l] = c_cb.D[nj][l] * a.id[1];
+        wz[l] = c_cb.D[nk][l] * a.id[2];
+    }
+    auto F = [&](int mm, int ax, int q, int slot) -> double& {
+        return U[((mm * 3 + ax) * NF + q) * C4_NS + slot];
+    };
+    const int ts = sw(t);
     const double ie = 1.0 / a.eps, im = 1.0 / a.mu;
-    double* RH = FL;  // right-hand sides reuse the flux storage after the divergence
     for (int it = 0; it < 4; ++it) {
-        {
-            double u[NF], f[NF];
+        double dv[4][NF];
 #pragma unroll
-            for (int q = 0; q < NF; ++q) u[q] = Q[t * NF + q];
-            maxwell_flux<0>(u, ie, im, f);
+        for (int h = 0; h < 2; ++h) {
 #pragma unroll
-            for (int q = 0; q < NF; ++q) FL[(0 * C4_NT + t) * NF + q] = f[q];
-            maxwell_flux<1>(u, ie, im, f);
+            for (int mm = 0; mm < 2; ++mm) {
+                const int m = 2 * h + mm;
+                double fl[NF];
+                maxwell_flux<0>(Q[m], ie, im, fl);
 #pragma unroll
-            for (int q = 0; q < NF; ++q) FL[(1 * C4_NT + t) * NF + q] = f[q];
-            maxwell_flux<2>(u, ie, im, f);
+                for (int q = 0; q < NF; ++q) F(mm, 0, q, ts) = fl[q];
+                maxwell_flux<1>(Q[m], ie, im, fl);
 #pragma unroll
-            for (int q = 0; q < NF; ++q) FL[(2 * C4_NT + t) * NF + q] = f[q];
+                for (int q = 0; q < NF; ++q) F(mm, 1, q, ts) = fl[q];
+                maxwell_flux<2>(Q[m], ie, im, fl);
+#pragma unroll
+                for (int q = 0; q < NF; ++q) F(mm, 2, q, ts) = fl[q];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int mm = 0; mm < 2; ++mm) {
+                const int m = 2 * h + mm;
+#pragma unroll
+                for (int q = 0; q < NF; ++q) dv[m][q] = 0.0;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    const int tx = sw((t & ~3) | l), ty = sw((t & ~12) | (l << 2)),
+                              tz = sw((t & ~48) | (l << 4));
+#pragma unroll
+                    for (int q = 0; q < NF; ++q)
+                        dv[m][q] += wx[l] * F(mm, 0, q, tx) + wy[l] * F(mm, 1, q, ty) +
+                                    wz[l] * F(mm, 2, q, tz);
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        {
-            double dv[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        // right-hand sides P - dt sum_l A_ml div_l; D: the implicit source over this node's
+        // time nodes (minv); B: explicit
+        double r[4][NF];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tx = (t & ~3) | l, ty = (t & ~12) | (l << 2), tz = (t & ~48) | (l << 4);
-                const double wx = c_cb.D[ni][l] * a.id[0], wy = c_cb.D[nj][l] * a.id[1],
-                             wz = c_cb.D[nk][l] * a.id[2];
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-                for (int q = 0; q < NF; ++q)
-                    dv[q] += wx * FL[(0 * C4_NT + tx) * NF + q] + wy * FL[(1 * C4_NT + ty) * NF + q] +
-                             wz * FL[(2 * C4_NT + tz) * NF + q];
+            for (int q = 0; q < NF; ++q) {
+                double v = p0[q];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) v -= (dt * c_cb.A[m][l]) * dv[l][q];
+                r[m][q] = v;
             }
 #pragma unroll
-            for (int q = 0; q < NF; ++q) DV[t * NF + q] = dv[q];
-        }
-        __syncthreads();
-        {  // right-hand sides P - dt sum_l A_ml div_l
-            double r[NF];
-#pragma unroll
-            for (int q = 0; q < NF; ++q) r[q] = p0[q];
-#pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int tl = (t & 63) | (l << 6);
-                const double w = dt * c_cb.A[nm][l];
-#pragma unroll
-                for (int q = 0; q < NF; ++q) r[q] -= w * DV[tl * NF + q];
-            }
-#pragma unroll
-            for (int q = 0; q < NF; ++q) RH[t * NF + q] = r[q];
-        }
-        __syncthreads();
-        {  // D: the implicit source over the time nodes of this spatial node; B: explicit
+        for (int m = 0; m < 4; ++m) {
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 double v = 0.0;
 #pragma unroll
-                for (int l = 0; l < 4; ++l) v += minv[nm][l] * RH[((t & 63) | (l << 6)) * NF + q];
-                Q[t * NF + q] = v;
+                for (int l = 0; l < 4; ++l) v += minv[m][l] * r[l][q];
+                Q[m][q] = v;
             }
 #pragma unroll
-            for (int q = 3; q < NF; ++q) Q[t * NF + q] = RH[t * NF + q];
+            for (int q = 3; q < NF; ++q) Q[m][q] = r[m][q];
         }
-        __syncthreads();
     }
-    // -- outputs, contracted one dimension at a time: (1) time -> the 2 Gauss times
-    double* T = FL;
-    if (t < 128) {
-        const int tg = t >> 6, node = t & 63;
-        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    // -- outputs: (1) time -> the 2 Gauss times, in registers: T[q][tg][slotT(node)]
+    double* T = U;
+    double* S = U + C4_T;  // S[q][r + r / 16], r = ((C * 2 + g) * 2 + tg) * 16 + b1 * 4 + b2
+    auto slotT = [](int n) { return n ^ ((n >> 4) * 5); };
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const double w = c_cb.LT[tg][m];
+    for (int tg = 0; tg < 2; ++tg)
 #pragma unroll
-            for (int q = 0; q < NF; ++q) v[q] += w * Q[((m << 6) | node) * NF + q];
+        for (int q = 0; q < NF; ++q) {
+            double v = 0.0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) v += c_cb.LT[tg][m] * Q[m][q];
+            T[(q * 2 + tg) * C4_NS + slotT(t)] = v;
         }
-#pragma unroll
-        for (int q = 0; q < NF; ++q) T[t * NF + q] = v[q];
-    }
     __syncthreads();
-    // (2) the edge points: edge axis C, corner (la, lb) in the (C+1, C+2) plane at +-1/2, the
-    //     Gauss point g along C, the Gauss time tg: e = ((C * 4 + 2 lb + la) * 2 + g) * 2 + tg
-    if (t < C4_EDGE) {
-        const int tg = t & 1, g = (t >> 1) & 1, corner = (t >> 2) & 3, C = t >> 4;
-        const int la = corner & 1, lb = corner >> 1;
-        const int AA = (C + 1) % 3, BB = (C + 2) % 3;
-        double w[3][4];
+    // (2) the edge axis C at its Gauss point g
+    for (int r = t; r < 192; r += C4_NS) {
+        const int C = r >> 6, g = (r >> 5) & 1, tg = (r >> 4) & 1, b1 = (r >> 2) & 3, b2 = r & 3;
+        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            w[C][l] = c_cb.LG[g][l];
-            w[AA][l] = c_cb.LF[la][l];  // la = 0: +1/2
-            w[BB][l] = c_cb.LF[lb][l];
-        }
-        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int kk = 0; kk < 4; ++kk)
-            for (int jj = 0; jj < 4; ++jj)
-                for (int ii = 0; ii < 4; ++ii) {
-                    const double ww = w[2][kk] * w[1][jj] * w[0][ii];
-                    const int node = (kk * 4 + jj) * 4 + ii;
+            int c[3];
+            c[C] = l;
+            c[(C + 1) % 3] = b1;
+            c[(C + 2) % 3] = b2;
+            const int node = (c[2] * 4 + c[1]) * 4 + c[0];
+            const double w = c_cb.LG[g][l];
 #pragma unroll
-                    for (int q = 0; q < NF; ++q) v[q] += ww * T[((tg << 6) | node) * NF + q];
-                }
+            for (int q = 0; q < NF; ++q) v[q] += w * T[(q * 2 + tg) * C4_NS + slotT(node)];
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) S[q * C4_SQ + r + (r >> 4)] = v[q];
+    }
+    __syncthreads();
+    // (3) the edge points: corner (la, lb) in the (C+1, C+2) plane at +-1/2 (la = 0: +1/2),
+    //     e = ((C * 4 + 2 lb + la) * 2 + g) * 2 + tg
+    if (t < C4_EDGE) {
+        const int tg = t & 1, g = (t >> 1) & 1, corner = (t >> 2) & 3, C = t >> 4;
+        const double* w1 = c_cb.LF[corner & 1];
+        const double* w2 = c_cb.LF[corner >> 1];
+        const int base = ((C * 2 + g) * 2 + tg) * 16;
+        double v[NF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int b1 = 0; b1 < 4; ++b1)
+#pragma unroll
+            for (int b2 = 0; b2 < 4; ++b2) {
+                const double ww = w1[b1] * w2[b2];
+                const int r = base + b1 * 4 + b2;
+#pragma unroll
+                for (int q = 0; q < NF; ++q) v[q] += ww * S[q * C4_SQ + r + (r >> 4)];
+            }
 #pragma unroll
         for (int q = 0; q < NF; ++q) __stcs(a.states + (size_t(t) * NF + q) * N + o, v[q]);
     }
@@ -781,7 +828,6 @@ CArgs cargs(const hc_ced* m) {
     return a;
 }
 
-constexpr size_t kCed4Smem = sizeof(double) * 5 * C4_NT * NF;
 
 int launch_step4(hc_ced* m) {
     CArgs a = cargs(m);
@@ -790,7 +836,7 @@ int launch_step4(hc_ced* m) {
     k_ced_ghosts<<<blocks(shell_count(b), 256), 256, 0, st>>>(a, 0);
     k_ced_cell<true><<<blocks(b.N, 256), 256, 0, st>>>(a);
     const size_t ring = size_t(b.n[0] + 2) * (b.n[1] + 2) * (b.n[2] + 2);
-    k_ced4_predict<<<unsigned(ring), C4_NT, kCed4Smem, st>>>(a);
+    k_ced4_predict<<<unsigned(ring), C4_NS, 0, st>>>(a);
     const size_t ex = size_t(b.n[0]) * (b.n[1] + 1) * (b.n[2] + 1);
     const size_t ey = size_t(b.n[0] + 1) * b.n[1] * (b.n[2] + 1);
     const size_t ez = size_t(b.n[0] + 1) * (b.n[1] + 1) * b.n[2];
@@ -905,8 +951,8 @@ int hc_ced_create(const hc_geom* g, const hc_ced_params* p, hc_ced** out) {
         CedBasis bs = make_ced_basis();
         e = cudaMemcpyToSymbol(c_cb, &bs, sizeof bs);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_ced4_predict, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(kCed4Smem));
+            e = cudaFuncSetAttribute(k_ced4_predict,
+                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     }
     if (e != cudaSuccess) {
         hc_ced_destroy(m);

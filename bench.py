@@ -258,6 +258,8 @@ def ext_roofline(name, order, n, ms_step, bytes_per_zone, max_mhz):
     with open(os.path.join(ROOT, "profiles", "r2_ext_flops.json")) as f:
         c = json.load(f)[f"{name}_o{order}"]
     fpz = c["a"] + c["b"] / n + c["c"] / n ** 2
+    fsrc = c.get("source", "profiles/r2_ext_flops.json (restatement as written, "
+                           "tools/count_flops_ext.py)")
     t = ms_step * 1e-3
     fp = fpz * zones / t / 1e12
     fp_peak = fp64_nominal_tflops(torch.cuda.current_device(), max_mhz or 1965)
@@ -267,15 +269,15 @@ def ext_roofline(name, order, n, ms_step, bytes_per_zone, max_mhz):
     tpath = os.path.join(ROOT, "profiles", "r2_ext_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(name, {}).get("dram_bytes_per_zone")
+            # (measured at order 3 only)
+            traffic = json.load(f).get(name, {}).get("dram_bytes_per_zone") if order == 3 else None
     fp_frac, hb_frac = fp / fp_peak, hb / hbm_peak
     r = {"bound": "fp64" if fp_frac >= hb_frac else "hbm",
          "achieved": fp if fp_frac >= hb_frac else hb,
          "peak": fp_peak if fp_frac >= hb_frac else hbm_peak,
          "unit": "TFLOP/s" if fp_frac >= hb_frac else "GB/s",
          "frac": max(fp_frac, hb_frac),
-         "flops_per_zone": fpz, "flops_source": "profiles/r2_ext_flops.json (restatement as "
-                                                "written, tools/count_flops_ext.py)",
+         "flops_per_zone": fpz, "flops_source": fsrc,
          "fp64": {"achieved": fp, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp_frac,
                   "peak_source": "nominal DFMA rate at the max SM clock"},
          "hbm": {"achieved": hb, "peak": hbm_peak, "unit": "GB/s", "frac": hb_frac,
@@ -302,7 +304,8 @@ def bench_mhd(args):
     import torch
 
     from paper_2211_13295_b200 import mhd, mhd_slabs
-    n = args.n if args.n != 256 else 384
+    # (order 4 materialises 96 x 8 solver states per zone: 192^3 fits, 384^3 would not)
+    n = args.n if args.n != 256 else (192 if args.order == 4 else 384)
     order = args.order
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -165,3 +165,18 @@ def test_domain_peer_store_slabs_bitwise(exact, integ, nslabs, bcz, shape):
         np.abs(out[act] - want[act]).max()
     assert (out2[act].view(np.uint64) == want[act].view(np.uint64)).all()
     assert (t2, dt2, n2) == (t1, dt1, n1)
+
+
+def test_stepper_set_zpeer_validates():
+    """hc_stepper_set_zpeer: rejected when the stepper fills its own z ghosts, or with no
+    neighbour at all"""
+    import ctypes as C
+    lib = hydro.load_library()
+    g = hydro.make_geometry(32, 8, 8, 3)
+    st = hydro.Stepper(g, hydro.make_params(3))  # owns its z boundary (bc[2] = periodic)
+    bufs = (C.c_void_p * 3)()
+    nb = C.c_int()
+    assert lib.hc_stepper_buffers(st.h, bufs, C.byref(nb)) == 0
+    assert lib.hc_stepper_set_zpeer(st.h, bufs, bufs) != 0
+    assert lib.hc_stepper_set_zpeer(st.h, None, None) != 0
+    st.close()

@@ -565,8 +565,6 @@ __global__ void __launch_bounds__(FusedShape<(ORD >= 3), TX, TY>::NT, MINB)
                     double* dst = sbuf[1] + zi;
 #pragma unroll
                     for (int q = 0; q < NV; ++q) dst[q] = un[q];
-                    if (a.zstore)
-                        zpeer_store(a, p - 1, zi - size_t(p - 1 + a.gh) * plane_stride, un);
                     if (!RK || a.want_dt) {
                         Fault f;
                         f.clear();

@@ -128,10 +128,10 @@ static int launch_solver(const FusedArgs& a, int solver, cudaStream_t st, const 
     }
 }
 
-template <int ORD, int SOLVER, bool RK>
+template <int ORD, int SOLVER, bool RK, bool ZP>
 static int seam_one(const FusedArgs& a, const SeamArgs& sa, cudaStream_t st, int* blocks_per_sm) {
     using S = SeamShape<ORD>;
-    auto kern = seam_ader_kernel<ORD, SOLVER, RK>;
+    auto kern = seam_ader_kernel<ORD, SOLVER, RK, ZP>;
     static unsigned long long configured = 0;  // per device, as launch_cfg
     int dev = 0;
     cudaError_t de = cudaGetDevice(&dev);
@@ -157,7 +157,7 @@ static int seam_one(const FusedArgs& a, const SeamArgs& sa, cudaStream_t st, int
     // per plane: y-seam faces, x-seam faces, tile-corner zones (one launch, disjoint zones)
     const unsigned nby = unsigned(sa.nty * sa.nx + 127) / 128, nbx = unsigned(sa.ntx * sa.ny + 127) / 128,
                    nbc = unsigned(4 * sa.ntx * sa.nty + 127) / 128;
-    seam_fix_kernel<SOLVER, RK><<<dim3(nby + nbx + nbc, unsigned(nplanes)), 128, 0, st>>>(a, sa);
+    seam_fix_kernel<SOLVER, RK, ZP><<<dim3(nby + nbx + nbc, unsigned(nplanes)), 128, 0, st>>>(a, sa);
     e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "seam_fix_kernel launch");
 }
@@ -166,10 +166,14 @@ template <int ORD, bool RK>
 static int seam_solver(const FusedArgs& a, const SeamArgs& sa, int solver, cudaStream_t st,
                        int* bps) {
     switch (solver) {
-        case 0: return seam_one<ORD, 0, RK>(a, sa, st, bps);
-        case 1: return seam_one<ORD, 1, RK>(a, sa, st, bps);
-        case 2: return seam_one<ORD, 2, RK>(a, sa, st, bps);
-        default: return seam_one<ORD, 3, RK>(a, sa, st, bps);
+        case 0: return a.zstore ? seam_one<ORD, 0, RK, true>(a, sa, st, bps)
+                           : seam_one<ORD, 0, RK, false>(a, sa, st, bps);
+        case 1: return a.zstore ? seam_one<ORD, 1, RK, true>(a, sa, st, bps)
+                           : seam_one<ORD, 1, RK, false>(a, sa, st, bps);
+        case 2: return a.zstore ? seam_one<ORD, 2, RK, true>(a, sa, st, bps)
+                           : seam_one<ORD, 2, RK, false>(a, sa, st, bps);
+        default: return a.zstore ? seam_one<ORD, 3, RK, true>(a, sa, st, bps)
+                         : seam_one<ORD, 3, RK, false>(a, sa, st, bps);
     }
 }
 

@@ -104,7 +104,7 @@ __device__ __forceinline__ double* edge_x(const SeamArgs& s, int k, int sx, int 
 //     south fluxes back to YPF
 //  D  accumulator -= cy (N - S)
 // Missing seam fluxes count as zero; seam_fix_x / seam_fix_y add them.
-template <int ORD, int SOLVER, bool RK>
+template <int ORD, int SOLVER, bool RK, bool ZP>
 __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
     seam_ader_kernel(const __grid_constant__ FusedArgs a, const SeamArgs sa) {
     using S = SeamShape<ORD>;
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                             double* dst = sbuf[1] + zi;
 #pragma unroll
                             for (int q = 0; q < NV; ++q) dst[q] = un[q];
-                            if (a.zstore)
+                            if (ZP)
                                 zpeer_store(a, p - 1, zi - size_t(p - 1 + a.gh) * plane_stride, un);
                         }
                     } else {
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
                         double* dst = sbuf[1] + zi;
 #pragma unroll
                         for (int q = 0; q < NV; ++q) dst[q] = un[q];
-                        if (a.zstore && !edge)  // (edge zones: seam_fix_kernel stores them)
+                        if (ZP && !edge)  // (edge zones: seam_fix_kernel stores them)
                             zpeer_store(a, p - 1, zi - size_t(p - 1 + a.gh) * plane_stride, un);
                     }
                     double dloc = 1.0e32;
@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(SeamShape<ORD>::NT, SeamShape<ORD>::MINB)
 // A face's flux is subtracted from the zone on its low side and added to the zone on its high
 // side (times cx or cy, and b at an RK stage); every thread then takes the CFL estimate of the
 // zones it completed; min-reduced per block. Grid (blocks of the three groups, planes).
-template <int SOLVER, bool RK>
+template <int SOLVER, bool RK, bool ZP>
 __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ FusedArgs a,
                                                        const SeamArgs sa) {
     if (a.ctl->done) return;
@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
                         out[zh + q] = vh[q];
                     }
                 }
-                if (a.zstore) {
+                if (ZP) {
                     const size_t pz = size_t(p + a.gh) * a.my_pad * a.pitch;
                     zpeer_store(a, p, zl - pz, vl);
                     zpeer_store(a, p, zh - pz, vh);
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
                 out[z + q] = v[q];
             }
         }
-        if (a.zstore) zpeer_store(a, p, z - size_t(p + a.gh) * a.my_pad * a.pitch, v);
+        if (ZP) zpeer_store(a, p, z - size_t(p + a.gh) * a.my_pad * a.pitch, v);
         dloc = cfl(v, i, j);
     }
     if (RK && !a.want_dt) return;

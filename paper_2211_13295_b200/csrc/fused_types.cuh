@@ -53,7 +53,10 @@ struct FusedArgs {
 // The peer store of one finished zone of active plane kz (in-plane storage offset `inplane`).
 // Not inlined: a call on the rare boundary-plane path keeps the fused kernels' register
 // allocation as it is without peer stores (inlined, the headline lost 0.7 %).
-__device__ __noinline__ void zpeer_store(const FusedArgs& a, int kz, size_t inplane,
+// (The seam kernels take it as a template switch, instantiated twice, so the kernels of a
+// stepper without peer stores carry no trace of it: even an untaken inlined branch cost the
+// headline 0.7 %, an out-of-line call 3.7 %. Ring-kernel steppers get k_zpeer_planes.)
+__device__ __forceinline__ void zpeer_store(const FusedArgs& a, int kz, size_t inplane,
                                             const double* v) {
     const int ob = (a.ctl->cur + a.out_rel) % a.nbuf;
     const size_t ps = size_t(a.my_pad) * a.pitch;

@@ -85,6 +85,24 @@ __global__ void k_stepper_ghosts(Bufs bufs, int nbuf, int rel, const StepCtl* c,
     ghost_copy(u, g, bx, by, bz, i, j, k);
 }
 
+// z peer stores after the ring kernel (the seam kernels store in place): the gh lowest /
+// highest active planes of the buffer the step wrote, into the z neighbours' ghost planes
+__global__ void k_zpeer_planes(const __grid_constant__ FusedArgs a) {
+    if (a.ctl->done) return;
+    const int kz = int(blockIdx.y);
+    if ((kz >= a.gh && kz < a.nz - a.gh) || kz < a.kz_first || kz >= a.kz_last) return;
+    const int r = int(blockIdx.x * blockDim.x + threadIdx.x);
+    if (r >= a.nx * a.ny) return;
+    const int i = r % a.nx, j = r / a.nx;
+    const size_t inplane = size_t(j + a.gh) * a.pitch + size_t(i + a.gh) * NV;
+    const double* src = a.buf[(a.ctl->cur + a.out_rel) % a.nbuf] +
+                        size_t(kz + a.gh) * a.my_pad * a.pitch + inplane;
+    double v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = src[q];
+    zpeer_store(a, kz, inplane, v);
+}
+
 __global__ void k_advance(StepCtl* c, const ErrBlock* eb, int flip) {
     if (c->done) return;
     for (int s = 0; s < ST_COUNT; ++s)
@@ -638,6 +656,13 @@ static int launch_step(hc_stepper* s, FusedArgs a, bool rk, cudaStream_t st) {
     rc = s->o.exact ? launch_fused_exact(a, s->p.order, s->p.solver, rk, st, pl)
                     : launch_fused_fast(a, s->p.order, s->p.solver, rk, st, pl);
     if (rc) return rc;
+    if (s->zstore) {
+        const dim3 grid(unsigned((s->g.nx * s->g.ny + 255) / 256), unsigned(s->g.nz));
+        k_zpeer_planes<<<grid, 256, 0, st>>>(a);
+        s->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "k_zpeer_planes");
+    }
     s->launches++;
     return HC_OK;
 }

@@ -37,3 +37,22 @@ def test_reference_arm_c1_line_matches_our_config_keys():
     d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
     assert d["config"]["n"] == [128, 128, 4] and d["warmup"] == 3
     assert "build" not in d["config"] and "reference" in d["build"]
+
+
+def test_reference_arm_rk3_and_unavailable_extensions():
+    """--integrator rk3 runs the reference's own rk_step on the host (the paper's CFD RK row);
+    the extension workloads have no reference arm and say so in one line"""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--n", "16", "--steps", "1", "--warmup", "1", "--integrator", "rk3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    assert d["config"]["integrator"] == "rk3" and d["value"] > 0
+    assert "RK3" in d["cpu_baseline"]["sample"]
+    for w in ("mhd", "ced", "ader4"):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl",
+                            "reference", "--workload", w], capture_output=True, text=True,
+                           timeout=120, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+        assert d["impl"] == "reference" and "unavailable" in d

@@ -57,28 +57,44 @@ struct Bufs {
     double* b[3];
 };
 
+// Up to four plane ranges of one ghost fill, each in ring mode (the planes are active: their
+// x/y ghost ring, 2*gh full rows + 2*gh columns of the ny active rows) or full mode (z-ghost
+// planes: every zone). Every ghost zone copies its composed active image (ghost_copy), so the
+// ranges are independent and go in ONE launch (three launches per fill before: ~6 us each on
+// the launch-bound configs[0] mesh).
+struct GhostSegs {
+    int lo[4], mode[4];
+    unsigned start[5];  // prefix thread counts; start[n] = total
+    int n;
+};
+
 __global__ void k_stepper_ghosts(Bufs bufs, int nbuf, int rel, const StepCtl* c, SG g, int bx,
-                                 int by, int bz, int k_lo, int ring_mode) {
+                                 int by, int bz, GhostSegs segs) {
     if (c->done) return;
     double* u = bufs.b[(c->cur + rel) % nbuf];
-    const int k = k_lo + blockIdx.y;
-    size_t r = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
+    const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+    int sg = 0;
+    while (sg < segs.n && r >= segs.start[sg + 1]) ++sg;
+    if (sg >= segs.n) return;
+    const unsigned ring = unsigned(2 * g.gh * (g.mx + g.ny)), plane = unsigned(g.mx * g.my);
+    const unsigned loc = r - segs.start[sg];
+    const unsigned per = segs.mode[sg] ? ring : plane;
+    const int k = segs.lo[sg] + int(loc / per);
+    const unsigned t = loc % per;
     int i, j;
-    if (!ring_mode) {
-        if (r >= size_t(g.mx) * g.my) return;
-        i = int(r % g.mx);
-        j = int(r / g.mx);
+    if (!segs.mode[sg]) {
+        i = int(t % g.mx);
+        j = int(t / g.mx);
     } else {
-        const size_t rows = size_t(2 * g.gh) * g.mx;
-        if (r >= rows + size_t(2 * g.gh) * g.ny) return;
-        if (r < rows) {  // full ghost rows j < gh or j >= gh + ny
-            int jr = int(r / g.mx);
-            i = int(r % g.mx);
+        const unsigned rows = unsigned(2 * g.gh) * g.mx;
+        if (t < rows) {  // full ghost rows j < gh or j >= gh + ny
+            const int jr = int(t / g.mx);
+            i = int(t % g.mx);
             j = jr < g.gh ? jr : g.ny + jr;
         } else {  // ghost columns of the active rows
-            size_t t = r - rows;
-            int col = int(t % (2 * g.gh));
-            j = g.gh + int(t / (2 * g.gh));
+            const unsigned tt = t - rows;
+            const int col = int(tt % (2 * g.gh));
+            j = g.gh + int(tt / (2 * g.gh));
             i = col < g.gh ? col : g.nx + col;
         }
     }
@@ -609,23 +625,27 @@ static int fill_planes(hc_stepper* s, int k_lo, int k_hi, cudaStream_t st) {
     const int a_lo = std::max(k_lo, g.gh), a_hi = std::min(k_hi, g.gh + g.nz);
     const unsigned ring = unsigned(2 * g.gh * (g.mx + g.ny));
     const unsigned plane = unsigned(g.mx * g.my);
-    auto launch = [&](int lo, int hi, int ring_mode) {
+    GhostSegs segs{};
+    auto add = [&](int lo, int hi, int ring_mode) {
         if (hi <= lo) return;
-        dim3 grid(((ring_mode ? ring : plane) + 255) / 256, unsigned(hi - lo));
-        Bufs b{{s->buf[0], s->buf[1], s->buf[2]}};
-        k_stepper_ghosts<<<grid, 256, 0, st>>>(b, s->nbuf, stage_in_rel(s), s->ctl, g,
-                                               s->o.bc[0], s->o.bc[1], s->o.bc[2], lo, ring_mode);
-        s->launches++;
+        segs.lo[segs.n] = lo;
+        segs.mode[segs.n] = ring_mode;
+        segs.start[segs.n + 1] = segs.start[segs.n] + unsigned(hi - lo) * (ring_mode ? ring : plane);
+        ++segs.n;
     };
-    if (s->o.bc[0] >= 0) launch(a_lo, a_hi, 1);  // (all -1: a patch set fills every ghost)
-    if (s->zstore && s->o.bc[0] >= 0) {  // z-ghost planes hold the neighbours' active zones
-        launch(k_lo, std::min(k_hi, g.gh), 1);
-        launch(std::max(k_lo, g.gh + g.nz), k_hi, 1);
+    if (s->o.bc[0] >= 0) add(a_lo, a_hi, 1);  // (all -1: a patch set fills every ghost)
+    if (s->o.bc[0] >= 0 && s->zstore) {  // z-ghost planes hold the neighbours' active zones
+        add(k_lo, std::min(k_hi, g.gh), 1);
+        add(std::max(k_lo, g.gh + g.nz), k_hi, 1);
+    } else if (s->o.bc[2] >= 0) {
+        add(k_lo, std::min(k_hi, g.gh), 0);
+        add(std::max(k_lo, g.gh + g.nz), k_hi, 0);
     }
-    if (s->o.bc[2] >= 0) {
-        launch(k_lo, std::min(k_hi, g.gh), 0);
-        launch(std::max(k_lo, g.gh + g.nz), k_hi, 0);
-    }
+    if (segs.n == 0) return HC_OK;
+    Bufs b{{s->buf[0], s->buf[1], s->buf[2]}};
+    k_stepper_ghosts<<<(segs.start[segs.n] + 255) / 256, 256, 0, st>>>(
+        b, s->nbuf, stage_in_rel(s), s->ctl, g, s->o.bc[0], s->o.bc[1], s->o.bc[2], segs);
+    s->launches++;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? HC_OK : cuda_fail(e, "k_stepper_ghosts");
 }

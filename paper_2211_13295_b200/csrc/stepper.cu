@@ -193,8 +193,17 @@ int set_dev(const hc_stepper* s) {
 // Planes per CTA z-chunk. Each chunk re-runs reconstruction + predictor on its two z-ring
 // planes (~0.6 of a plane's cost each), and the grid runs in waves of `slots` resident CTAs:
 // pick the chunk height minimising waves x (tz + 1.2). HC_TZ overrides (tuning).
-int choose_tz(int tiles, int nz, int slots) {
-    if (const char* v = std::getenv("HC_TZ")) return std::max(4, std::min(nz, std::atoi(v)));
+int choose_tz(int tiles, int nz, int slots, int sms) {
+    if (const char* v = std::getenv("HC_TZ"))
+        if (std::atoi(v) > 0) return std::max(1, std::min(nz, std::atoi(v)));
+    // Thin meshes (fewer planes than the shortest chunk below): as many chunks as keep one CTA
+    // per SM -- a CTA's fixed cost (pipeline fill, z-ring planes) is worth ~5 planes, and two
+    // co-resident CTAs of a latency-bound launch run slower than one. configs[0] (64 tiles,
+    // 4 planes): 2 chunks of 2 planes, measured 1.36 G zone/s vs 1.25 (4 x 1) and 1.14 (1 x 4).
+    if (nz < 8) {
+        const int chunks = std::max(1, std::min(nz, sms / std::max(1, tiles)));
+        return (nz + chunks - 1) / chunks;
+    }
     int best = std::min(32, nz);
     double best_cost = 1e300;
     for (int tz = 8; tz <= 96; ++tz) {
@@ -208,7 +217,7 @@ int choose_tz(int tiles, int nz, int slots) {
             best = eff;
         }
     }
-    return std::max(4, std::min(best, nz));
+    return std::max(1, std::min(best, nz));
 }
 
 FusedArgs fused_args(const hc_stepper* s) {
@@ -380,7 +389,7 @@ static int setup_seam(hc_stepper* s) {
     if (rc) return rc;
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->o.device));
     if (bps < 1) return HC_OK;
-    s->seam_tz = choose_tz(sa.ntx * sa.nty, g.nz, sms * bps);
+    s->seam_tz = choose_tz(sa.ntx * sa.nty, g.nz, sms * bps, sms);
     if ((rc = encode_maps(s, SEAM_TYM + 2 * (s->p.order >= 3 ? 2 : 1)))) return rc;
     sa.maps = s->maps;
     const size_t nsx = size_t(g.nz) * sa.ntx * g.ny * 2 * NV;
@@ -494,7 +503,7 @@ int hc_stepper_create(const hc_geom* g, const hc_params* p, const hc_stepper_opt
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o->device);
         const int tiles = ((g->nx + TX - 1) / TX) * ((g->ny + TY - 1) / TY);
-        s->tz = choose_tz(tiles, g->nz, sms * FusedTile<true>::MINB);
+        s->tz = choose_tz(tiles, g->nz, sms * FusedTile<true>::MINB, sms);
     }
     s->bytes = (size_t(sg.mz) * sg.my_pad * sg.pitch + slack) * sizeof(double);
     cudaError_t e = cudaMalloc(&s->buf[0], s->bytes);

@@ -227,6 +227,10 @@ int hc_stepper_compute(hc_stepper* s);
  * then the two boundary ranges. */
 int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last);
 int hc_stepper_advance(hc_stepper* s);
+/* hc_stepper_compute, and when that was the step's last stage also hc_stepper_advance -- for a
+ * driver with nothing to reduce in between (one domain): the seam kernel pair then runs the
+ * advance in its last CTA, one launch fewer per step. */
+int hc_stepper_compute_step(hc_stepper* s);
 /* fused launches per step: 1 (ADER), 2 or 3 (RK); a multi-GPU step repeats fill_ghosts +
  * halo exchange + compute per stage, then all-reduce + advance */
 int hc_stepper_stages(hc_stepper* s);

@@ -625,8 +625,18 @@ __global__ void __launch_bounds__(128) seam_fix_kernel(const __grid_constant__ F
     dloc = warp_min(dloc);
     if ((t & 31) == 0) red[t >> 5] = dloc;
     __syncthreads();
-    if (t == 0)
+    if (t == 0) {
         atomic_min_pos_sparse(&a.ctl->acc, smin(smin(red[0], red[1]), smin(red[2], red[3])));
+        if (a.fold_adv) {  // the last CTA to finish runs the step's advance (k_advance)
+            __threadfence();
+            const unsigned total = gridDim.x * gridDim.y;
+            if (atomicAdd(&a.ctl->blocks, 1u) == total - 1) {
+                __threadfence();
+                a.ctl->blocks = 0;
+                advance_ctl(a.ctl, a.eb, a.flip);
+            }
+        }
+    }
 }
 
 }  // namespace HC_FUSED_NS

@@ -18,7 +18,32 @@ struct StepCtl {
     long long steps;
     int done;  // 1: t_final reached, 2: a step failed (unphysical); later steps are no-ops
     int cur;   // which of the two state buffers holds the current state
+    unsigned blocks;  // CTAs of a launch that folds the advance in, finished so far (else 0)
 };
+
+// The end-of-step hand-off (harness.cpp:155-170): error check, t += dt, dt <- dt_next (clipped
+// at t_final), the buffer flip. k_advance runs it as its own launch; a seam step folds it into
+// the last CTA of seam_fix_kernel.
+__device__ __forceinline__ void advance_ctl(StepCtl* c, const ErrBlock* eb, int flip) {
+    if (c->done) return;
+    for (int s = 0; s < ST_COUNT; ++s)
+        if (eb->rec[s].flag) {  // the reference would have thrown out of this step
+            c->done = 2;
+            return;
+        }
+    c->t = c->t + c->dt;  // harness.cpp:167-168
+    c->steps += 1;
+    double dn = c->acc;
+    c->dt_next = dn;
+    c->acc = 1.0e32;
+    if (c->t_final > 0.0) {  // harness.cpp:156-160
+        double rem = c->t_final - c->t;
+        if (rem <= 1e-12 * c->t_final) c->done = 1;
+        else if (dn >= rem) dn = rem;
+    }
+    c->dt = dn;
+    if (flip) c->cur ^= 1;  // ADER wrote the other buffer; RK stages end in buffer cur
+}
 
 struct FusedArgs {
     double* buf[3];  // state buffers; ctl->cur holds the start-of-step state
@@ -48,6 +73,8 @@ struct FusedArgs {
     double* zlo[3];
     double* zhi[3];
     int zstore;
+    // 1: the launch closes the step and folds the advance in (flip = ADER's buffer flip)
+    int fold_adv, flip;
 };
 
 // The peer store of one finished zone of active plane kz (in-plane storage offset `inplane`).

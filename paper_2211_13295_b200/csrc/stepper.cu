@@ -119,26 +119,7 @@ __global__ void k_zpeer_planes(const __grid_constant__ FusedArgs a) {
     zpeer_store(a, kz, inplane, v);
 }
 
-__global__ void k_advance(StepCtl* c, const ErrBlock* eb, int flip) {
-    if (c->done) return;
-    for (int s = 0; s < ST_COUNT; ++s)
-        if (eb->rec[s].flag) {  // the reference would have thrown out of this step
-            c->done = 2;
-            return;
-        }
-    c->t = c->t + c->dt;  // harness.cpp:167-168
-    c->steps += 1;
-    double dn = c->acc;
-    c->dt_next = dn;
-    c->acc = 1.0e32;
-    if (c->t_final > 0.0) {  // harness.cpp:156-160
-        double rem = c->t_final - c->t;
-        if (rem <= 1e-12 * c->t_final) c->done = 1;
-        else if (dn >= rem) dn = rem;
-    }
-    c->dt = dn;
-    if (flip) c->cur ^= 1;  // ADER wrote the other buffer; RK stages end in buffer cur
-}
+__global__ void k_advance(StepCtl* c, const ErrBlock* eb, int flip) { advance_ctl(c, eb, flip); }
 
 }  // namespace
 }  // namespace hc
@@ -181,6 +162,9 @@ struct hc_stepper {
     double* zlo[3] = {nullptr, nullptr, nullptr};
     double* zhi[3] = {nullptr, nullptr, nullptr};
     bool zstore = false;
+    // enqueue_step: the next whole-range closing launch folds the advance in (seam pair)
+    bool fold_next = false;
+    bool folded = false;  // ... and it did
 };
 
 namespace {
@@ -257,6 +241,8 @@ FusedArgs fused_args(const hc_stepper* s) {
         a.zhi[i] = s->zhi[i];
     }
     a.zstore = s->zstore ? 1 : 0;
+    a.fold_adv = 0;
+    a.flip = s->o.integrator == 0 ? 1 : 0;
     return a;
 }
 
@@ -725,6 +711,17 @@ int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last)
         a.rk_b = ab[1];
         a.want_dt = k == ns - 1;
     }
+    s->folded = false;
+    // (only where launches dominate: every fix CTA takes a turn on one counter, which costs
+    // ~2 us per thousand CTAs -- 2 % of the 256^3 step, more than the launch it saves)
+    const SeamArgs& sa = s->sa;
+    const long fix_ctas = long((sa.nty * sa.nx + 127) / 128 + (sa.ntx * sa.ny + 127) / 128 +
+                               (4 * sa.ntx * sa.nty + 127) / 128) * s->g.nz;
+    if (s->fold_next && s->seam && kz_first == 0 && kz_last == s->g.nz && a.want_dt &&
+        fix_ctas <= 2048) {
+        a.fold_adv = 1;
+        s->folded = true;
+    }
     if (kz_last > kz_first) {
         if ((rc = launch_step(s, a, rk, s->st))) return rc;
     }
@@ -734,6 +731,24 @@ int hc_stepper_compute_range(hc_stepper* s, int kz_first, int kz_last, int last)
     else
         s->cur = 1 - s->cur;  // host-side guess; the device's ctl->cur is authoritative
     return HC_OK;
+}
+
+// The next stage, and -- when it is the step's last -- the advance: folded into the seam
+// pair's last CTA, else k_advance (no all-reduce of dt_next between the two).
+int hc_stepper_compute_step(hc_stepper* s) {
+    const bool last = s->o.integrator == 0 || s->stage == s->o.integrator - 1;
+    if (!last) return hc_stepper_compute(s);
+    const char* nf = std::getenv("HC_NO_FOLD");  // (A/B: 1 keeps k_advance)
+    s->fold_next = !(nf && std::atoi(nf) != 0);
+    int rc = hc_stepper_compute(s);
+    s->fold_next = false;
+    if (rc) return rc;
+    if (s->folded) {
+        s->folded = false;
+        s->stage = 0;
+        return HC_OK;
+    }
+    return hc_stepper_advance(s);
 }
 
 int hc_stepper_advance(hc_stepper* s) {
@@ -751,9 +766,8 @@ static int enqueue_step(hc_stepper* s) {
     int rc = HC_OK;
     for (int k = 0; k < ns && !rc; ++k) {
         rc = hc_stepper_fill_ghosts(s);  // rk_step: apply_boundary before every stage
-        if (!rc) rc = hc_stepper_compute(s);
+        if (!rc) rc = k == ns - 1 ? hc_stepper_compute_step(s) : hc_stepper_compute(s);
     }
-    if (!rc) rc = hc_stepper_advance(s);
     return rc;
 }
 

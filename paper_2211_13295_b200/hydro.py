@@ -387,6 +387,11 @@ class Stepper:
     def advance(self):
         _check(self.lib.hc_stepper_advance(self.h))
 
+    def compute_step(self):
+        """compute(); when it is the step's last stage, also the advance (no all-reduce in
+        between: a stepper owning its dt)"""
+        _check(self.lib.hc_stepper_compute_step(self.h))
+
     def sync(self):
         """Returns (t, dt_of_next_step, steps_done); raises the first device error."""
         t, dt, n = C.c_double(), C.c_double(), C.c_long()

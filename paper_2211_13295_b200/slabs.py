@@ -229,6 +229,10 @@ class SlabDomain:
             self.st.step(1)
             return
         G = self.order  # stencil halo R + 1 (R = 1 at order 2, 2 at order 3)
+        # no all-reduce between the last stage and the advance: the stepper closes the step
+        # itself (the seam pair folds the advance into its last CTA)
+        local = not (self.world > 1 or self.collectives)
+        advanced = False
         with torch.cuda.stream(s):
             for k in range(self.st.stages):  # 1 (ADER) or 2/3 RK stages
                 self.st.fill_ghosts()
@@ -252,13 +256,18 @@ class SlabDomain:
                         exchange_z_halos(self._planes(), self.geom.ghost, self.nloc,
                                          self.rank, self.world, self.periodic,
                                          p2p=self.collectives)
-                    self.st.compute()
+                    if local and k == self.st.stages - 1:
+                        self.st.compute_step()
+                        advanced = True
+                    else:
+                        self.st.compute()
             if kernel_events is not None:
                 kernel_events[1].record(s)
             if self.world > 1 or self.collectives:
                 import torch.distributed as dist
                 dist.all_reduce(self._acc(), op=dist.ReduceOp.MIN)
-            self.st.advance()
+            if not advanced:
+                self.st.advance()
 
     def sync(self):
         return self.st.sync()

@@ -351,17 +351,13 @@ static int launch_seam(const hc_stepper* s, const FusedArgs& a, const SeamArgs& 
 // periodic (the zone across the mesh edge is the last tile's edge zone), nx a multiple of 32,
 // ny >= 2 (every tile has two rows), storage ghosts equal to the kernel's x halo and an even
 // row pitch (TMA box origins on 16-byte boundaries). Both builds; the bit-exact one also keeps
-// the edge zones' rate parts (SeamArgs ex / ey), which only pays where the ring's re-predicted
-// zones cost more than those records: order >= 3 and nz >= 16 (measured: O2 256^3-512^3 1 %
-// slower, C1 128 x 128 x 4 10 % slower than the exact ring kernel). HC_SEAM=0 keeps the ring
-// kernel, HC_SEAM=1 takes the pair wherever the mesh allows it.
+// the edge zones' rate parts (SeamArgs ex / ey). HC_SEAM=0 keeps the ring kernel.
 static int setup_seam(hc_stepper* s) {
     int force = -1;
     if (const char* v = std::getenv("HC_SEAM")) force = std::atoi(v) != 0;
     if (force == 0) return HC_OK;
     const hc_geom& g = s->g;
     if (s->persist || g.ny < 2) return HC_OK;
-    if (force < 0 && s->o.exact && (s->p.order < 3 || g.nz < 16)) return HC_OK;
     if (s->o.bc[0] != HC_PERIODIC || s->o.bc[1] != HC_PERIODIC) return HC_OK;
     if (g.nx % SEAM_TX || (s->sg.pitch & 1) || g.ghost != (s->p.order >= 3 ? 3 : 2)) return HC_OK;
     const bool rk = s->o.integrator != 0;

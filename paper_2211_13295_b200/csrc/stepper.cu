@@ -358,6 +358,9 @@ static int setup_seam(hc_stepper* s) {
     if (force == 0) return HC_OK;
     const hc_geom& g = s->g;
     if (s->persist || g.ny < 2) return HC_OK;
+    // the bit-exact build's rate records do not pay at order 2 (cheap predictor): equal for
+    // ADER, 7 % slower for RK2 at 256^3 than the exact ring kernel (measured)
+    if (force < 0 && s->o.exact && s->p.order == 2) return HC_OK;
     if (s->o.bc[0] != HC_PERIODIC || s->o.bc[1] != HC_PERIODIC) return HC_OK;
     if (g.nx % SEAM_TX || (s->sg.pitch & 1) || g.ghost != (s->p.order >= 3 ? 3 : 2)) return HC_OK;
     const bool rk = s->o.integrator != 0;

@@ -25,7 +25,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -65,8 +64,27 @@ def fp64_nominal_tflops(device, max_mhz):
 BYTES_PER_ZONE = 80.0  # read + write U_skinny (5 doubles), SURVEY.md 8(d)
 
 
+def _clock_proc(device, stop, out):
+    """ClockSampler's child process: polls NVML every 0.5 ms until told to stop (a separate
+    process, so the Python GIL of the timing thread cannot starve it)."""
+    import pynvml
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(device)
+    samples, bits = [], 0
+    out.put("ready")
+    while not stop.is_set():
+        try:
+            samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            pass
+        time.sleep(0.0005)
+    out.put((samples, bits))
+
+
 class ClockSampler:
-    """Samples SM clock and throttle reasons via NVML during the timed region."""
+    """Samples SM clock and throttle reasons via NVML during the timed region, from a forked
+    child process (NVML only; no CUDA in the child)."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -76,8 +94,9 @@ class ClockSampler:
     }
 
     def __init__(self, device):
+        self.device = device
         self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
+        self.proc = None
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -87,36 +106,46 @@ class ClockSampler:
         except Exception:
             self.nv = None
 
+    def _add_bits(self, r):
+        for bit, name in self.REASONS.items():
+            if r & bit and bit != 0x1:
+                self.reasons.add(name)
+
     def _sample(self):
         try:
             self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-            for bit, name in self.REASONS.items():
-                if r & bit and bit != 0x1:
-                    self.reasons.add(name)
+            self._add_bits(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
         except Exception:
             pass
 
-    def _run(self):
-        while not self._stop.is_set():
-            self._sample()
-            time.sleep(0.001)
-
     def __enter__(self):
         if self.nv:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-            time.sleep(0.001)  # let the sampler take its first reading
+            try:
+                import multiprocessing as mp
+                ctx = mp.get_context("fork")
+                self.stop, self.q = ctx.Event(), ctx.Queue()
+                self.proc = ctx.Process(target=_clock_proc, args=(self.device, self.stop, self.q),
+                                        daemon=True)
+                self.proc.start()
+                self.q.get(timeout=30)  # sampling before the timed region starts
+            except Exception:
+                self.proc = None
+            self._sample()
         return self
 
     def __exit__(self, *a):
-        # (and one sample from the main thread at the end of the timed region, still under
-        # load: a short region must not go unsampled if the thread was starved)
-        if self.nv:
-            self._sample()
-        self._stop.set()
-        if self.nv:
-            self.t.join()
+        if not self.nv:
+            return
+        self._sample()  # (one more from this process, still under load)
+        if self.proc is not None:
+            try:
+                self.stop.set()
+                samples, bits = self.q.get(timeout=30)
+                self.samples.extend(samples)
+                self._add_bits(bits)
+                self.proc.join(timeout=10)
+            except Exception:
+                pass
 
     def summary(self):
         med = statistics.median(self.samples) if self.samples else None

@@ -65,7 +65,7 @@ BYTES_PER_ZONE = 80.0  # read + write U_skinny (5 doubles), SURVEY.md 8(d)
 
 
 def _clock_proc(device, stop, out):
-    """ClockSampler's child process: polls NVML every 0.5 ms until told to stop (a separate
+    """ClockSampler's child process: polls NVML every 2 ms until told to stop (a separate
     process, so the Python GIL of the timing thread cannot starve it)."""
     import pynvml
     pynvml.nvmlInit()
@@ -78,7 +78,7 @@ def _clock_proc(device, stop, out):
             bits |= pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
             pass
-        time.sleep(0.0005)
+        time.sleep(0.002)  # (each NVML query takes the driver; launch-bound runs feel it)
     out.put((samples, bits))
 
 

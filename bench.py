@@ -354,7 +354,8 @@ def bench_mhd(args):
     else:
         g = mhd.make_geometry(n, n, n, order, (0, 0, 0), (1, 1, 1))
         s0 = mhd.orszag_tang(g, order)
-        st = mhd.MhdStepper(g, mhd.make_params(order))
+        st = mhd.MhdStepper(g, mhd.make_params(order, face_solver=mhd.HLLD if args.mhd_hlld
+                                                else mhd.HLL))
         st.upload(s0)
         st.set_time(0.0, st.cfl_dt(cfl), cfl)
         stream = torch.cuda.ExternalStream(st.stream_ptr)
@@ -420,7 +421,8 @@ def bench_mhd(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Orszag-Tang IC sampled on the host, B from a vector potential)",
-        "config": {"workload": f"C3: 3D ideal MHD Orszag-Tang {n}^3, WENO-ADER O{order}, HLL "
+        "config": {"workload": f"C3: 3D ideal MHD Orszag-Tang {n}^3, WENO-ADER O{order}, "
+                               f"{'HLLD' if args.mhd_hlld else 'HLL'} "
                                "faces + 2D-HLL (UCT) edge EMFs, constrained transport "
                                "(configs[2]; extension, no reference counterpart)",
                    "n": n, "order": order, "build": "bit-exact (--fmad=false)",
@@ -608,6 +610,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--mhd-hlld", action="store_true",
+                    help="--workload mhd with the HLLD face solver (default HLL)")
     ap.add_argument("--integrator", default="ader", choices=list(INTEGRATORS),
                     help="ader (the reference's one-step ADER, the headline) or the reference's "
                          "rk2 / rk3 (stepper.cpp rk_step; the paper's CFD RK row)")

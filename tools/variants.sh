@@ -5,7 +5,7 @@
 set -e
 mkdir -p gpurun_out
 out=gpurun_out/variants.jsonl; : > $out
-for a in "--workload c1" "--order 2" "--order 4" "--n 384" "--n 384 --order 2" "--n 512" "--n 512 --order 2" "--workload mhd" "--workload ced" "--workload ader4" "--integrator rk2 --order 2" "--integrator rk3 --order 3" "--workload mhd --order 4" "--workload ced --order 4"; do
+for a in "--workload c1" "--order 2" "--order 4" "--n 384" "--n 384 --order 2" "--n 512" "--n 512 --order 2" "--workload mhd" "--workload ced" "--workload ader4" "--integrator rk2 --order 2" "--integrator rk3 --order 3" "--workload mhd --order 4" "--workload ced --order 4" "--workload mhd --mhd-hlld"; do
   python bench.py $a --no-cpu-baseline --e2e-steps 2 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); d['args']='$a'; print(json.dumps(d))" >> $out
 done
 python - <<'P'
